@@ -1,0 +1,93 @@
+/* modeswitch-b200: C ABI of the host controller (libmodeswitch.so).
+ *
+ * Flat C entry points over the C++ controller (include/modeswitch/*.hpp) so
+ * non-C++ callers (ctypes, cgo, JNI) bind it without C++ name mangling. Each
+ * one replaces a reference call site:
+ *   msw_route_rule        <- RulePolicy::route          (routing.cpp:186-194)
+ *                            + classify/extract_features (classifier.cpp:69-113)
+ *                            + resolve_family            (classifier.cpp:115-136)
+ *   msw_trace_parse_line  <- parse_trace_line           (trace_io.cpp:34-76)
+ *   msw_trace_format_line <- format_trace_line          (trace_io.cpp:78-92)
+ *   msw_trace_generate    <- generate_trace             (workload.cpp:61-91)
+ *   msw_route_cost        <- the per-decision overhead stamp (routing.cpp:188-192)
+ *
+ * Return codes mirror the reference CLI's exit codes (tools/modeswitch.cpp:26-30):
+ *   0 ok, 2 ConfigError, 3 DataError, 1 anything else. Message via
+ *   msw_host_last_error() (thread-local). No exception crosses this ABI.
+ */
+#ifndef MSW_HOST_H_
+#define MSW_HOST_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSW_OK 0
+#define MSW_ERR_OTHER 1
+#define MSW_ERR_CONFIG 2
+#define MSW_ERR_DATA 3
+
+typedef struct msw_descriptor {
+  const char* request_id; /* nonempty, NUL-terminated */
+  int32_t prompt_tokens;
+  int32_t expected_output_tokens;
+  int32_t shared_prefix;   /* 0/1 */
+  int32_t memory_pressure; /* 0/1 */
+  int32_t batch_pressure;
+  int32_t workload_tag; /* WorkloadFamily value, -1 = untagged */
+} msw_descriptor;
+
+typedef struct msw_classifier_cfg {
+  int32_t long_prompt_threshold; /* 512 */
+  int32_t long_output_threshold; /* 64 */
+  double decode_heavy_ratio;     /* 0.5 */
+  int32_t batch_threshold;       /* 2 */
+} msw_classifier_cfg;
+
+typedef struct msw_route_out {
+  int32_t mode;   /* InferenceMode value */
+  int32_t reason; /* RoutingReason value */
+  int32_t workload_class;
+  int32_t family; /* resolve_family */
+  double overhead_ms;
+} msw_route_out;
+
+/* cfg may be NULL for the reference defaults. */
+int msw_route_rule(const msw_descriptor* d, const msw_classifier_cfg* cfg,
+                   msw_route_out* out);
+
+/* Routes every line of an NDJSON trace held in memory; out arrays sized n_max.
+ * *n_out receives the request count. ids_out (optional) receives the request
+ * ids, NUL-separated, into a caller buffer of ids_cap bytes. */
+int msw_route_ndjson(const char* ndjson, const msw_classifier_cfg* cfg,
+                     int32_t n_max, msw_route_out* out, int32_t* n_out);
+
+/* Parses one trace line. The id is copied into id_buf (cap bytes). */
+int msw_trace_parse_line(const char* line, msw_descriptor* out, char* id_buf,
+                         size_t id_cap);
+
+/* Canonical single-line JSON; *needed = bytes incl. NUL. */
+int msw_trace_format_line(const msw_descriptor* d, char* buf, size_t cap,
+                          size_t* needed);
+
+/* generate_trace(): counts[11] per family in enum order. Writes NDJSON
+ * (newline-terminated lines) into buf; *needed = bytes incl. NUL. */
+int msw_trace_generate(const int32_t counts[11], double jitter, uint64_t seed,
+                       int32_t batch_pressure, double batched_fraction,
+                       char* buf, size_t cap, size_t* needed);
+
+/* Routes the trace `passes` times with RulePolicy and returns the mean of the
+ * policy's own overhead stamps and the wall time per decision (ms). */
+int msw_route_cost(const char* ndjson, int32_t passes, double* mean_stamp_ms,
+                   double* wall_ms_per_decision);
+
+const char* msw_host_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MSW_HOST_H_ */

@@ -1,0 +1,643 @@
+/* CPU ORACLE — TEST INFRASTRUCTURE ONLY (see oracle_model.h for scope and
+ * parity status). Restates DESIGN.md's numerics contract in plain C11 with
+ * OpenMP over output rows / heads. Nothing here is shipped.
+ */
+#include "oracle_model.h"
+
+#include <math.h>
+#include <omp.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- fp16 --- */
+typedef uint16_t h16;
+static inline float h2f(h16 h) {
+  _Float16 v;
+  memcpy(&v, &h, 2);
+  return (float)v;
+}
+static inline h16 f2h(float f) { /* IEEE round-to-nearest-even */
+  _Float16 v = (_Float16)f;
+  h16 h;
+  memcpy(&h, &v, 2);
+  return h;
+}
+static inline float rnd16(float f) { return h2f(f2h(f)); }
+
+/* ------------------------------------------------- K16 deterministic init */
+static inline uint64_t mix64(uint64_t z) { /* splitmix64 */
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static inline uint64_t tensor_key(uint64_t seed, uint64_t tid) {
+  return mix64(seed ^ (tid * 0xD1B54A32D192ED03ull));
+}
+/* uniform in [-1, 1) with 2^-23 resolution; exact in fp32 */
+static inline float unif(uint64_t key, uint64_t idx) {
+  const uint64_t r = mix64(key + idx);
+  const int32_t u = (int32_t)(r >> 40);
+  return (float)(u - 8388608) * 0x1.0p-23f;
+}
+
+void orc_fill_fp16(uint16_t* dst, int64_t rows, int64_t cols, uint64_t seed,
+                   uint64_t tid, int32_t scale_log2) {
+  const uint64_t key = tensor_key(seed, tid);
+  const float sc = ldexpf(1.0f, -scale_log2);
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t c = 0; c < cols; ++c)
+      dst[r * cols + c] = f2h(unif(key, (uint64_t)(r * cols + c)) * sc);
+}
+
+static void fill_norm(h16* dst, int64_t n, uint64_t seed, uint64_t tid) {
+  const uint64_t key = tensor_key(seed, tid);
+  for (int64_t i = 0; i < n; ++i) dst[i] = f2h(1.0f + unif(key, (uint64_t)i) * 0.125f);
+}
+
+/* Tensor ids. */
+#define TID_DRAFT_BASE (1ull << 32)
+#define TID_EMBED 1ull
+#define TID_FINAL_NORM 3ull
+#define TID_LAYER(l, k) (256ull + 16ull * (uint64_t)(l) + (uint64_t)(k))
+enum { K_Q = 0, K_K, K_V, K_O, K_GATE, K_UP, K_DOWN, K_ATTN_NORM, K_FFN_NORM };
+#define SUCC_SALT 0x5375636365737373ull
+#define AGREE_SALT 0x4167726565416772ull
+
+static int ceil_log2(int64_t x) {
+  int l = 0;
+  while ((1ll << l) < x) ++l;
+  return l;
+}
+static int floor_log2(int64_t x) {
+  int l = 0;
+  while ((2ll << l) <= x) ++l;
+  return l;
+}
+static int in_shift(int64_t k) { return (ceil_log2(k) + 1) / 2; }
+static int res_shift(int layers) { return floor_log2(layers) / 2; }
+
+/* ------------------------------------------------------------ quantisers */
+void orc_quant_int8_rows(const uint16_t* w, int32_t n, int32_t k, int8_t* q,
+                         float* scales) {
+#pragma omp parallel for schedule(static)
+  for (int32_t r = 0; r < n; ++r) {
+    float amax = 0.0f;
+    for (int32_t c = 0; c < k; ++c) amax = fmaxf(amax, fabsf(h2f(w[(int64_t)r * k + c])));
+    const float s = amax / 127.0f;
+    scales[r] = s;
+    for (int32_t c = 0; c < k; ++c) {
+      float v = 0.0f;
+      if (amax > 0.0f) v = rintf(h2f(w[(int64_t)r * k + c]) / s);
+      v = fminf(fmaxf(v, -127.0f), 127.0f);
+      q[(int64_t)r * k + c] = (int8_t)v;
+    }
+  }
+}
+
+void orc_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* q_out,
+                       uint16_t* scales) {
+  const int32_t groups = k / MSW_W4_GROUP;
+#pragma omp parallel for schedule(static)
+  for (int32_t r = 0; r < n; ++r)
+    for (int32_t g = 0; g < groups; ++g) {
+      const uint16_t* src = w + (int64_t)r * k + (int64_t)g * MSW_W4_GROUP;
+      float amax = 0.0f;
+      for (int i = 0; i < MSW_W4_GROUP; ++i) amax = fmaxf(amax, fabsf(h2f(src[i])));
+      const h16 sh = f2h((2.0f * amax) / 15.0f);
+      const float s = h2f(sh);
+      scales[(int64_t)r * groups + g] = sh;
+      for (int i = 0; i < MSW_W4_GROUP; ++i) {
+        int q = 8;
+        if (s > 0.0f) {
+          q = (int)rintf(h2f(src[i]) / s) + 8;
+          q = q < 0 ? 0 : (q > 15 ? 15 : q);
+        }
+        q_out[(int64_t)r * k + (int64_t)g * MSW_W4_GROUP + i] = (uint8_t)q;
+      }
+    }
+}
+
+void orc_gemv_i8_acc(const int8_t* w, const int8_t* x, int32_t n, int32_t k,
+                     int32_t* acc) {
+#pragma omp parallel for schedule(static)
+  for (int32_t r = 0; r < n; ++r) {
+    int32_t a = 0;
+    for (int32_t c = 0; c < k; ++c) a += (int32_t)w[(int64_t)r * k + c] * (int32_t)x[c];
+    acc[r] = a;
+  }
+}
+
+/* ------------------------------------------------------------ linears --- */
+/* Activation handling per weight format:
+ *   FP16 / W4: x is rounded to fp16, products accumulated in fp32.
+ *   INT8: x quantised per token: s = absmax/127, q = clamp(rint(x/s)), y =
+ *         ((float)acc * s) * s_w[n]; absmax == 0 gives y = 0.
+ *   W4:   w = fp16((q - 8) * s_g), q one nibble per byte here.          */
+static float dot8(const float* a, const float* b, int64_t k) {
+  float acc[8] = {0};
+  int64_t c = 0;
+  for (; c + 8 <= k; c += 8)
+    for (int j = 0; j < 8; ++j) acc[j] += a[c + j] * b[c + j];
+  float s = 0.0f;
+  for (int j = 0; j < 8; ++j) s += acc[j];
+  for (; c < k; ++c) s += a[c] * b[c];
+  return s;
+}
+
+static void linear_fp16(const h16* w, int32_t n, int32_t k, const float* x16,
+                        float* y) {
+#pragma omp parallel
+  {
+    float* row = (float*)malloc(sizeof(float) * (size_t)k);
+#pragma omp for schedule(static)
+    for (int32_t r = 0; r < n; ++r) {
+      for (int32_t c = 0; c < k; ++c) row[c] = h2f(w[(int64_t)r * k + c]);
+      y[r] = dot8(row, x16, k);
+    }
+    free(row);
+  }
+}
+
+static void linear_w4(const uint8_t* q, const h16* s, int32_t n, int32_t k,
+                      const float* x16, float* y) {
+  const int32_t groups = k / MSW_W4_GROUP;
+#pragma omp parallel
+  {
+    float* row = (float*)malloc(sizeof(float) * (size_t)k);
+#pragma omp for schedule(static)
+    for (int32_t r = 0; r < n; ++r) {
+      for (int32_t g = 0; g < groups; ++g) {
+        float lut[16];
+        const float sc = h2f(s[(int64_t)r * groups + g]);
+        for (int v = 0; v < 16; ++v) lut[v] = rnd16((float)(v - 8) * sc);
+        const uint8_t* src = q + (int64_t)r * k + (int64_t)g * MSW_W4_GROUP;
+        for (int i = 0; i < MSW_W4_GROUP; ++i) row[g * MSW_W4_GROUP + i] = lut[src[i]];
+      }
+      y[r] = dot8(row, x16, k);
+    }
+    free(row);
+  }
+}
+
+static void linear_i8(const int8_t* w, const float* ws, int32_t n, int32_t k,
+                      const float* x, float* y) {
+  float amax = 0.0f;
+  for (int32_t c = 0; c < k; ++c) amax = fmaxf(amax, fabsf(x[c]));
+  if (!(amax > 0.0f)) {
+    for (int32_t r = 0; r < n; ++r) y[r] = 0.0f;
+    return;
+  }
+  const float s = amax / 127.0f;
+  int8_t* qx = (int8_t*)malloc((size_t)k);
+  for (int32_t c = 0; c < k; ++c) {
+    float v = rintf(x[c] / s);
+    v = fminf(fmaxf(v, -127.0f), 127.0f);
+    qx[c] = (int8_t)v;
+  }
+#pragma omp parallel for schedule(static)
+  for (int32_t r = 0; r < n; ++r) {
+    int32_t a = 0;
+    const int8_t* wr = w + (int64_t)r * k;
+    for (int32_t c = 0; c < k; ++c) a += (int32_t)wr[c] * (int32_t)qx[c];
+    y[r] = ((float)a * s) * ws[r];
+  }
+  free(qx);
+}
+
+void orc_linear(int wtype, const void* w, const void* scales, int32_t n,
+                int32_t k, const float* x, int32_t t, float* y) {
+  float* x16 = (float*)malloc(sizeof(float) * (size_t)k);
+  for (int32_t i = 0; i < t; ++i) {
+    const float* xi = x + (int64_t)i * k;
+    float* yi = y + (int64_t)i * n;
+    if (wtype == MSW_W_INT8) {
+      linear_i8((const int8_t*)w, (const float*)scales, n, k, xi, yi);
+      continue;
+    }
+    for (int32_t c = 0; c < k; ++c) x16[c] = rnd16(xi[c]);
+    if (wtype == MSW_W_FP16)
+      linear_fp16((const h16*)w, n, k, x16, yi);
+    else
+      linear_w4((const uint8_t*)w, (const h16*)scales, n, k, x16, yi);
+  }
+  free(x16);
+}
+
+/* -------------------------------------------------------------- model --- */
+typedef struct {
+  void* w[3];        /* per format: fp16 h16*, int8 int8_t*, w4 uint8_t* (nibble/byte) */
+  void* s[3];        /* NULL, float* [n], h16* [n, k/128] */
+  int32_t n, k;
+} orc_lin;
+
+typedef struct {
+  orc_lin qkv, o, gate, up, down;
+  h16* attn_norm;
+  h16* ffn_norm;
+} orc_layer;
+
+struct orc_model {
+  msw_model_cfg c;
+  uint64_t seed;
+  int is_draft;
+  uint32_t modes;
+  int32_t max_ctx;
+  h16* embed;   /* [V, h] */
+  h16* lm_head; /* [V, h] */
+  h16* final_norm;
+  orc_layer* layers;
+  int32_t* succ; /* successor map (this model's prediction for t) */
+  float* inv_freq;
+  /* per-mode KV caches: [L][ctx][Hk][D] (fp16-rounded values) */
+  float* kc;
+  float* vc;
+};
+
+static int fmt_of_mode(int mode) {
+  return mode == MSW_MODE_INT8 ? MSW_W_INT8 : (mode == MSW_MODE_GPTQ4 ? MSW_W_W4G128 : MSW_W_FP16);
+}
+
+static void build_lin(orc_lin* L, const orc_model* m, int32_t n, int32_t k,
+                      const uint64_t* tids, const int32_t* rows, int nparts,
+                      int32_t sh) {
+  /* The logical weight is the row-concatenation of nparts generated tensors. */
+  L->n = n;
+  L->k = k;
+  h16* full = (h16*)malloc(sizeof(h16) * (size_t)n * k);
+  int64_t off = 0;
+  for (int p = 0; p < nparts; ++p) {
+    orc_fill_fp16(full + off * k, rows[p], k, m->seed, tids[p], sh);
+    off += rows[p];
+  }
+  memset(L->w, 0, sizeof L->w);
+  memset(L->s, 0, sizeof L->s);
+  if (m->modes & ((1u << MSW_MODE_FP16) | (1u << MSW_MODE_SPECULATIVE))) {
+    L->w[MSW_W_FP16] = full;
+  }
+  if (m->modes & ((1u << MSW_MODE_INT8) | (1u << MSW_MODE_INT8_CONT_BATCHING))) {
+    L->w[MSW_W_INT8] = malloc((size_t)n * k);
+    L->s[MSW_W_INT8] = malloc(sizeof(float) * (size_t)n);
+    orc_quant_int8_rows(full, n, k, (int8_t*)L->w[MSW_W_INT8], (float*)L->s[MSW_W_INT8]);
+  }
+  if (m->modes & ((1u << MSW_MODE_GPTQ4) | (1u << MSW_MODE_GPTQ_PREFIX_CACHING))) {
+    L->w[MSW_W_W4G128] = malloc((size_t)n * k);
+    L->s[MSW_W_W4G128] = malloc(sizeof(h16) * (size_t)n * (k / MSW_W4_GROUP));
+    orc_quant_w4_rows(full, n, k, (uint8_t*)L->w[MSW_W_W4G128], (h16*)L->s[MSW_W_W4G128]);
+  }
+  if (L->w[MSW_W_FP16] != full) free(full);
+}
+
+static void free_lin(orc_lin* L) {
+  for (int i = 0; i < 3; ++i) {
+    free(L->w[i]);
+    free(L->s[i]);
+  }
+}
+
+typedef struct {
+  uint64_t key;
+  int32_t v;
+} keyed;
+static int cmp_keyed(const void* a, const void* b) {
+  const keyed* x = (const keyed*)a;
+  const keyed* y = (const keyed*)b;
+  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+  return x->v < y->v ? -1 : (x->v > y->v);
+}
+
+static int agrees(uint64_t seed, int32_t t, int32_t permille) {
+  return (int32_t)(mix64(mix64(seed ^ AGREE_SALT) + (uint64_t)t) % 1000ull) < permille;
+}
+
+static void build_rope(orc_model* m) {
+  const int half = m->c.head_dim / 2;
+  m->inv_freq = (float*)malloc(sizeof(float) * half);
+  for (int j = 0; j < half; ++j) {
+    double inv = pow((double)m->c.rope_theta, -(2.0 * j) / (double)m->c.head_dim);
+    if (m->c.rope_factor > 0.0f) {
+      const double lo_wl = m->c.rope_orig_ctx / m->c.rope_low_freq_factor;
+      const double hi_wl = m->c.rope_orig_ctx / m->c.rope_high_freq_factor;
+      const double wl = 2.0 * 3.14159265358979323846 / inv;
+      if (wl > lo_wl) {
+        inv = inv / m->c.rope_factor;
+      } else if (wl >= hi_wl) {
+        const double sm = (m->c.rope_orig_ctx / wl - m->c.rope_low_freq_factor) /
+                          (m->c.rope_high_freq_factor - m->c.rope_low_freq_factor);
+        inv = (1.0 - sm) * inv / m->c.rope_factor + sm * inv;
+      }
+    }
+    m->inv_freq[j] = (float)inv;
+  }
+}
+
+orc_model* orc_model_create(const msw_model_cfg* cfg, uint64_t seed, int is_draft,
+                            int32_t agree_permille, uint32_t modes, int32_t max_ctx) {
+  orc_model* m = (orc_model*)calloc(1, sizeof(orc_model));
+  m->c = *cfg;
+  m->seed = seed;
+  m->is_draft = is_draft;
+  m->modes = modes;
+  m->max_ctx = max_ctx;
+  const int32_t H = cfg->hidden, V = cfg->vocab, L = cfg->n_layers;
+  const int32_t D = cfg->head_dim, Hq = cfg->n_heads, Hk = cfg->n_kv_heads, F = cfg->ffn;
+  const uint64_t base = is_draft ? TID_DRAFT_BASE : 0ull;
+
+  m->embed = (h16*)malloc(sizeof(h16) * (size_t)V * H);
+  orc_fill_fp16(m->embed, V, H, seed, base + TID_EMBED, 0);
+  m->final_norm = (h16*)malloc(sizeof(h16) * H);
+  fill_norm(m->final_norm, H, seed, base + TID_FINAL_NORM);
+
+  /* successor permutation (shared by target and draft): one V-cycle */
+  keyed* order = (keyed*)malloc(sizeof(keyed) * V);
+  const uint64_t skey = mix64(seed ^ SUCC_SALT);
+  for (int32_t v = 0; v < V; ++v) {
+    order[v].key = mix64(skey + (uint64_t)v);
+    order[v].v = v;
+  }
+  qsort(order, V, sizeof(keyed), cmp_keyed);
+  int32_t* tsucc = (int32_t*)malloc(sizeof(int32_t) * V);
+  int32_t* tpred = (int32_t*)malloc(sizeof(int32_t) * V);
+  for (int32_t i = 0; i < V; ++i) {
+    const int32_t a = order[i].v, b = order[(i + 1) % V].v;
+    tsucc[a] = b;
+    tpred[b] = a;
+  }
+  free(order);
+  m->succ = (int32_t*)malloc(sizeof(int32_t) * V);
+  m->lm_head = (h16*)malloc(sizeof(h16) * (size_t)V * H);
+#pragma omp parallel for schedule(static)
+  for (int32_t u = 0; u < V; ++u) {
+    h16* row = m->lm_head + (int64_t)u * H;
+    if (!is_draft) {
+      memcpy(row, m->embed + (int64_t)tpred[u] * H, sizeof(h16) * H);
+    } else {
+      const int32_t p1 = tpred[u], p2 = tpred[tpred[u]];
+      const int a1 = agrees(seed, p1, agree_permille);
+      const int a2 = agrees(seed, p2, agree_permille);
+      for (int32_t j = 0; j < H; ++j) {
+        float r = 0.0f;
+        if (a1) r += h2f(m->embed[(int64_t)p1 * H + j]);
+        if (!a2) r += h2f(m->embed[(int64_t)p2 * H + j]);
+        row[j] = f2h(r);
+      }
+    }
+  }
+  for (int32_t t = 0; t < V; ++t)
+    m->succ[t] = (!is_draft || agrees(seed, t, agree_permille)) ? tsucc[t] : tsucc[tsucc[t]];
+  free(tsucc);
+  free(tpred);
+
+  m->layers = (orc_layer*)calloc((size_t)L, sizeof(orc_layer));
+  const int rs = res_shift(L);
+  for (int32_t l = 0; l < L; ++l) {
+    orc_layer* ly = &m->layers[l];
+    {
+      const uint64_t t[3] = {base + TID_LAYER(l, K_Q), base + TID_LAYER(l, K_K), base + TID_LAYER(l, K_V)};
+      const int32_t r[3] = {Hq * D, Hk * D, Hk * D};
+      build_lin(&ly->qkv, m, (Hq + 2 * Hk) * D, H, t, r, 3, in_shift(H));
+    }
+    {
+      const uint64_t t[1] = {base + TID_LAYER(l, K_O)};
+      const int32_t r[1] = {H};
+      build_lin(&ly->o, m, H, Hq * D, t, r, 1, in_shift(Hq * D) + rs);
+    }
+    {
+      const uint64_t t[1] = {base + TID_LAYER(l, K_GATE)};
+      const int32_t r[1] = {F};
+      build_lin(&ly->gate, m, F, H, t, r, 1, in_shift(H));
+    }
+    {
+      const uint64_t t[1] = {base + TID_LAYER(l, K_UP)};
+      const int32_t r[1] = {F};
+      build_lin(&ly->up, m, F, H, t, r, 1, in_shift(H));
+    }
+    {
+      const uint64_t t[1] = {base + TID_LAYER(l, K_DOWN)};
+      const int32_t r[1] = {H};
+      build_lin(&ly->down, m, H, F, t, r, 1, in_shift(F) + rs);
+    }
+    ly->attn_norm = (h16*)malloc(sizeof(h16) * H);
+    ly->ffn_norm = (h16*)malloc(sizeof(h16) * H);
+    fill_norm(ly->attn_norm, H, seed, base + TID_LAYER(l, K_ATTN_NORM));
+    fill_norm(ly->ffn_norm, H, seed, base + TID_LAYER(l, K_FFN_NORM));
+  }
+  build_rope(m);
+  const size_t kv = (size_t)L * max_ctx * Hk * D;
+  m->kc = (float*)malloc(sizeof(float) * kv);
+  m->vc = (float*)malloc(sizeof(float) * kv);
+  return m;
+}
+
+void orc_model_destroy(orc_model* m) {
+  if (!m) return;
+  for (int32_t l = 0; l < m->c.n_layers; ++l) {
+    orc_layer* ly = &m->layers[l];
+    free_lin(&ly->qkv);
+    free_lin(&ly->o);
+    free_lin(&ly->gate);
+    free_lin(&ly->up);
+    free_lin(&ly->down);
+    free(ly->attn_norm);
+    free(ly->ffn_norm);
+  }
+  free(m->layers);
+  free(m->embed);
+  free(m->lm_head);
+  free(m->final_norm);
+  free(m->succ);
+  free(m->inv_freq);
+  free(m->kc);
+  free(m->vc);
+  free(m);
+}
+
+int32_t orc_successor(orc_model* m, int32_t t) { return m->succ[t]; }
+int orc_threads(void) { return omp_get_max_threads(); }
+
+/* y = x * rsqrt(mean(x^2) + eps) * g, fp32 (sum in double) */
+static void rmsnorm(const float* x, const h16* g, int32_t n, float eps, float* y) {
+  double ss = 0.0;
+  for (int32_t i = 0; i < n; ++i) ss += (double)x[i] * (double)x[i];
+  const float r = (float)(1.0 / sqrt(ss / n + (double)eps));
+  for (int32_t i = 0; i < n; ++i) y[i] = (x[i] * r) * h2f(g[i]);
+}
+
+static void lin(const orc_lin* L, int fmt, const float* x, float* y) {
+  orc_linear(fmt, L->w[fmt], L->s[fmt], L->n, L->k, x, 1, y);
+}
+
+/* One decoder step for token `tok` at position `pos`; writes logits [V]. */
+static void forward(orc_model* m, int mode, int32_t tok, int32_t pos, float* logits) {
+  const msw_model_cfg* c = &m->c;
+  const int32_t H = c->hidden, D = c->head_dim, Hq = c->n_heads, Hk = c->n_kv_heads;
+  const int32_t F = c->ffn, half = D / 2, grp = Hq / Hk;
+  const int fmt = fmt_of_mode(mode);
+  float* h = (float*)malloc(sizeof(float) * H);
+  float* a = (float*)malloc(sizeof(float) * (F > H ? F : H));
+  float* qkv = (float*)malloc(sizeof(float) * (Hq + 2 * Hk) * D);
+  float* o = (float*)malloc(sizeof(float) * Hq * D);
+  float* g = (float*)malloc(sizeof(float) * F);
+  float* u = (float*)malloc(sizeof(float) * F);
+  float* y = (float*)malloc(sizeof(float) * H);
+  float* sc = (float*)malloc(sizeof(float) * (pos + 1) * Hq);
+  for (int32_t i = 0; i < H; ++i) h[i] = h2f(m->embed[(int64_t)tok * H + i]);
+  const float qscale = 1.0f / sqrtf((float)D);
+
+  for (int32_t l = 0; l < c->n_layers; ++l) {
+    const orc_layer* ly = &m->layers[l];
+    rmsnorm(h, ly->attn_norm, H, c->rms_eps, a);
+    lin(&ly->qkv, fmt, a, qkv);
+    /* RoPE (rotate-half pairs j, j+D/2) on q and k heads; round to fp16 */
+    for (int32_t hh = 0; hh < Hq + Hk; ++hh) {
+      float* v = qkv + (int64_t)hh * D;
+      for (int32_t j = 0; j < half; ++j) {
+        const float ang = (float)pos * m->inv_freq[j];
+        const float cs = cosf(ang), sn = sinf(ang);
+        const float x0 = v[j], x1 = v[j + half];
+        v[j] = x0 * cs - x1 * sn;
+        v[j + half] = x1 * cs + x0 * sn;
+      }
+    }
+    for (int32_t i = 0; i < (Hq + 2 * Hk) * D; ++i) qkv[i] = rnd16(qkv[i]);
+    float* kl = m->kc + ((size_t)l * m->max_ctx) * Hk * D;
+    float* vl = m->vc + ((size_t)l * m->max_ctx) * Hk * D;
+    memcpy(kl + (size_t)pos * Hk * D, qkv + Hq * D, sizeof(float) * Hk * D);
+    memcpy(vl + (size_t)pos * Hk * D, qkv + (Hq + Hk) * D, sizeof(float) * Hk * D);
+#pragma omp parallel for schedule(static)
+    for (int32_t hq = 0; hq < Hq; ++hq) {
+      const int32_t hk = hq / grp;
+      const float* q = qkv + (int64_t)hq * D;
+      float* s = sc + (int64_t)hq * (pos + 1);
+      float mx = -INFINITY;
+      for (int32_t p = 0; p <= pos; ++p) {
+        const float* kk = kl + ((size_t)p * Hk + hk) * D;
+        float d = 0.0f;
+        for (int32_t j = 0; j < D; ++j) d += q[j] * kk[j];
+        s[p] = d * qscale;
+        mx = fmaxf(mx, s[p]);
+      }
+      double den = 0.0;
+      for (int32_t p = 0; p <= pos; ++p) {
+        s[p] = expf(s[p] - mx);
+        den += s[p];
+      }
+      for (int32_t j = 0; j < D; ++j) {
+        double acc = 0.0;
+        for (int32_t p = 0; p <= pos; ++p) acc += (double)s[p] * vl[((size_t)p * Hk + hk) * D + j];
+        o[(int64_t)hq * D + j] = (float)(acc / den);
+      }
+    }
+    lin(&ly->o, fmt, o, y);
+    for (int32_t i = 0; i < H; ++i) h[i] += y[i];
+    rmsnorm(h, ly->ffn_norm, H, c->rms_eps, a);
+    lin(&ly->gate, fmt, a, g);
+    lin(&ly->up, fmt, a, u);
+    for (int32_t i = 0; i < F; ++i) a[i] = (g[i] / (1.0f + expf(-g[i]))) * u[i];
+    lin(&ly->down, fmt, a, y);
+    for (int32_t i = 0; i < H; ++i) h[i] += y[i];
+  }
+  rmsnorm(h, m->final_norm, H, c->rms_eps, a);
+  for (int32_t i = 0; i < H; ++i) a[i] = rnd16(a[i]);
+  linear_fp16(m->lm_head, c->vocab, H, a, logits);
+  free(h);
+  free(a);
+  free(qkv);
+  free(o);
+  free(g);
+  free(u);
+  free(y);
+  free(sc);
+}
+
+static int32_t argmax(const float* x, int32_t n) {
+  int32_t best = 0;
+  for (int32_t i = 1; i < n; ++i)
+    if (x[i] > x[best]) best = i; /* strict: lowest index wins ties */
+  return best;
+}
+
+int orc_generate(orc_model* m, int mode, const int32_t* prompt, int plen, int n_new,
+                 int32_t* out, float* logits) {
+  if (plen < 1 || n_new < 1 || plen + n_new > m->max_ctx) return 3;
+  const int32_t V = m->c.vocab;
+  float* lg = (float*)malloc(sizeof(float) * V);
+  for (int i = 0; i < plen; ++i) {
+    if (prompt[i] < 0 || prompt[i] >= V) {
+      free(lg);
+      return 3;
+    }
+    forward(m, mode, prompt[i], i, lg);
+  }
+  for (int t = 0; t < n_new; ++t) {
+    out[t] = argmax(lg, V);
+    if (logits) memcpy(logits + (size_t)t * V, lg, sizeof(float) * V);
+    if (t + 1 < n_new) forward(m, mode, out[t], plen + t, lg);
+  }
+  free(lg);
+  return 0;
+}
+
+int orc_spec_generate(orc_model* tg, orc_model* dr, int k, const int32_t* prompt,
+                      int plen, int n_new, int32_t* out, float* logits,
+                      int32_t* rounds, int32_t* proposed, int32_t* accepted) {
+  const int32_t V = tg->c.vocab;
+  if (plen < 1 || n_new < 1 || plen + n_new + k + 1 > tg->max_ctx ||
+      plen + n_new + k + 1 > dr->max_ctx)
+    return 3;
+  float* lg = (float*)malloc(sizeof(float) * V);
+  float* vlg = (float*)malloc(sizeof(float) * (size_t)(k + 1) * V);
+  int32_t* seq = (int32_t*)malloc(sizeof(int32_t) * (size_t)(plen + n_new + k + 2));
+  int32_t d[64];
+  memcpy(seq, prompt, sizeof(int32_t) * plen);
+  /* prefill both models; the target's last logits give the first token */
+  for (int i = 0; i < plen; ++i) {
+    forward(tg, MSW_MODE_FP16, prompt[i], i, lg);
+    forward(dr, MSW_MODE_FP16, prompt[i], i, vlg);
+  }
+  int n = plen;     /* committed tokens in seq */
+  int emitted = 0;
+  seq[n++] = argmax(lg, V);
+  out[emitted] = seq[n - 1];
+  if (logits) memcpy(logits, lg, sizeof(float) * V);
+  ++emitted;
+  int dlen = plen;  /* positions present in the draft cache */
+  *rounds = *proposed = *accepted = 0;
+  while (emitted < n_new) {
+    /* draft catch-up then k greedy proposals from the last committed token */
+    while (dlen < n - 1) {
+      forward(dr, MSW_MODE_FP16, seq[dlen], dlen, vlg);
+      ++dlen;
+    }
+    int32_t cur = seq[n - 1];
+    for (int i = 0; i < k; ++i) {
+      forward(dr, MSW_MODE_FP16, cur, n - 1 + i, vlg);
+      d[i] = argmax(vlg, V);
+      cur = d[i];
+    }
+    dlen = n - 1 + k;
+    /* target verify: tokens [seq[n-1], d0..d_{k-1}] at positions n-1 .. n-1+k */
+    int32_t g[65];
+    for (int i = 0; i <= k; ++i) {
+      forward(tg, MSW_MODE_FP16, i == 0 ? seq[n - 1] : d[i - 1], n - 1 + i, vlg + (size_t)i * V);
+      g[i] = argmax(vlg + (size_t)i * V, V);
+    }
+    int j = 0;
+    while (j < k && d[j] == g[j]) ++j;
+    *rounds += 1;
+    *proposed += k;
+    *accepted += j;
+    for (int i = 0; i <= j && emitted < n_new; ++i) {
+      seq[n++] = g[i];
+      out[emitted] = g[i];
+      if (logits) memcpy(logits + (size_t)emitted * V, vlg + (size_t)i * V, sizeof(float) * V);
+      ++emitted;
+    }
+    if (dlen > n - 1) dlen = n - 1; /* roll back draft positions past the commit */
+  }
+  free(lg);
+  free(vlg);
+  free(seq);
+  return 0;
+}

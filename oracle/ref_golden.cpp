@@ -1,0 +1,124 @@
+// Golden-fixture generator. TEST INFRASTRUCTURE ONLY: links the reference's
+// own proj/core library (compiled from /root/reference by oracle/Makefile
+// into oracle/_ref/, never copied) and writes the routing/trace fixtures that
+// pin the host controller under tests/golden/.
+//
+// Usage: ref_golden <out_dir>
+// Outputs (all deterministic):
+//   balanced_55_seed7.ndjson        reference write_trace(balanced_family_trace(55, 7))
+//   <name>.ndjson / <name>.decisions.csv for every trace below; each decision
+//   row is request_id,mode,reason,class,family from the reference's
+//   RulePolicy::route, classify(extract_features()) and resolve_family.
+#include <cstdio>
+#include <fstream>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "modeswitch/classifier.hpp"
+#include "modeswitch/routing.hpp"
+#include "modeswitch/trace_io.hpp"
+#include "modeswitch/workload.hpp"
+
+namespace ms = modeswitch;
+
+static void emit(const std::string& dir, const std::string& name,
+                 const std::vector<ms::RequestDescriptor>& trace) {
+  ms::write_trace(trace, dir + "/" + name + ".ndjson");
+  std::ofstream out(dir + "/" + name + ".decisions.csv");
+  out << "request_id,mode,reason,class,family\n";
+  const ms::RulePolicy policy;
+  const ms::ClassifierConfig cfg;
+  for (const auto& r : trace) {
+    const auto d = policy.route(r);
+    out << r.request_id << ',' << ms::to_string(d.mode) << ','
+        << ms::to_string(d.reason) << ','
+        << ms::to_string(ms::classify(ms::extract_features(r), cfg)) << ','
+        << ms::to_string(ms::resolve_family(r, cfg)) << '\n';
+  }
+}
+
+int main(int argc, char** argv) {
+  if (argc != 2) {
+    std::fprintf(stderr, "usage: %s <out_dir>\n", argv[0]);
+    return 2;
+  }
+  const std::string dir = argv[1];
+
+  // (1) SURVEY §8c golden: balanced_family_trace(55, seed 7), 605 lines.
+  emit(dir, "balanced_55_seed7", ms::balanced_family_trace(55, 7));
+
+  // (2) canonical families, zero jitter, unbatched and batch_pressure 4
+  //     (SPEC acceptance criterion 4).
+  {
+    ms::TraceSpec spec;
+    spec.jitter = 0.0;
+    spec.batched_fraction = 0.5;
+    spec.batch_pressure = 4;
+    for (auto f : ms::all_families()) spec.counts[f] = 2;
+    emit(dir, "canonical_families", ms::generate_trace(spec));
+  }
+
+  // (3) BASELINE config 1 workload: 5 per family, jitter 0.10, seed 7,
+  //     batched_fraction 0.2, batch_pressure 4.
+  {
+    ms::TraceSpec spec;
+    spec.seed = 7;
+    spec.batched_fraction = 0.2;
+    for (auto f : ms::all_families()) spec.counts[f] = 5;
+    emit(dir, "config1_mixed", ms::generate_trace(spec));
+  }
+
+  // (4) BASELINE config 5 deployment-mix families, tagged and untagged.
+  //     (the 8K variant is derived from the MemoryPressure rows by the host
+  //     code; routing does not depend on prompt length for memory_pressure.)
+  {
+    ms::TraceSpec spec;
+    spec.seed = 7;
+    spec.counts[ms::WorkloadFamily::SyntheticSS] = 64;
+    spec.counts[ms::WorkloadFamily::SyntheticSL] = 32;
+    spec.counts[ms::WorkloadFamily::GSM8K] = 32;
+    spec.counts[ms::WorkloadFamily::SharedPrefixChat] = 64;
+    spec.counts[ms::WorkloadFamily::MemoryPressureLongContext] = 64;
+    auto trace = ms::generate_trace(spec);
+    emit(dir, "deploy_mix_tagged", trace);
+    for (auto& r : trace) r.workload_tag.reset();
+    emit(dir, "deploy_mix_untagged", trace);
+  }
+
+  // (5) boundary fuzz: random descriptors concentrated around the classifier
+  //     thresholds (prompt 512, output 64, ratio 0.5, batch 2).
+  {
+    std::mt19937_64 rng(2605);
+    auto pick = [&rng](std::initializer_list<int> v) {
+      return *(v.begin() + rng() % v.size());
+    };
+    std::vector<ms::RequestDescriptor> trace;
+    for (int i = 0; i < 3000; ++i) {
+      ms::RequestDescriptor r;
+      r.request_id = "fuzz-" + std::to_string(i);
+      const int mode = int(rng() % 3);
+      if (mode == 0) {
+        r.prompt_tokens = pick({1, 2, 63, 64, 65, 127, 128, 255, 256, 257, 511,
+                                512, 513, 1024, 2048, 8192});
+        r.expected_output_tokens =
+            pick({1, 16, 31, 32, 63, 64, 65, 128, 255, 256, 257, 512, 1024});
+      } else if (mode == 1) {
+        // ratio exactly 0.5 and its neighbours
+        const int out = 64 + int(rng() % 200);
+        r.expected_output_tokens = out;
+        r.prompt_tokens = 2 * out + int(rng() % 3) - 1;
+      } else {
+        r.prompt_tokens = 1 + int(rng() % 9000);
+        r.expected_output_tokens = 1 + int(rng() % 1100);
+      }
+      r.shared_prefix = (rng() % 5) == 0;
+      r.memory_pressure = (rng() % 5) == 0;
+      r.batch_pressure = pick({1, 1, 1, 1, 2, 3, 4, 64});
+      if (rng() % 3 != 0) r.workload_tag = ms::all_families()[rng() % 11];
+      trace.push_back(r);
+    }
+    emit(dir, "boundary_fuzz", trace);
+  }
+  return 0;
+}

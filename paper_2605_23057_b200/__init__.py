@@ -1,0 +1,12 @@
+"""modeswitch-b200: B200-native executor for the inference modes routed by
+ModeSwitch-LLM's request-boundary controller (arXiv 2605.23057).
+
+Host controller (C++, libmodeswitch.so) + sm_100a CUDA engine
+(libmsw_engine.so) behind C ABIs in include/. This package is the Python
+handle over both; see DESIGN.md.
+"""
+from .configs import (ALL_MODES, MODE_FP16, MODE_GPTQ4, MODE_GPTQ_PC, MODE_INT8, MODE_INT8_CB,
+                      MODE_NAMES, MODE_SPEC, SHAPES, engine_cfg, model_cfg)
+
+__all__ = ["ALL_MODES", "MODE_FP16", "MODE_GPTQ4", "MODE_GPTQ_PC", "MODE_INT8", "MODE_INT8_CB",
+           "MODE_NAMES", "MODE_SPEC", "SHAPES", "engine_cfg", "model_cfg"]

@@ -1,0 +1,95 @@
+"""In-tree native build (no JIT cache): the .so files land under
+paper_2605_23057_b200/lib/ and oracle/, so gpurun ships them to the B200 box.
+
+  libmodeswitch.so   host controller (C++20) + executor, C ABI in include/msw_host.h
+  libmsw_engine.so   sm_100a CUDA engine, C ABI in include/msw_engine.h
+  oracle/liboracle.so, oracle/_ref/*  test-only checkers (built by build_oracle)
+"""
+from __future__ import annotations
+
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB = os.path.join(PKG, "lib")
+INC = os.path.join(ROOT, "include")
+CSRC = os.path.join(PKG, "csrc")
+NLOHMANN = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+ENGINE_SO = os.path.join(LIB, "libmsw_engine.so")
+HOST_SO = os.path.join(LIB, "libmodeswitch.so")
+
+
+def _stale(out: str, deps: list[str]) -> bool:
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list[str], cwd: str | None = None) -> None:
+    print("[build]", " ".join(cmd[:6]), "...", flush=True)
+    r = subprocess.run(cmd, cwd=cwd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {cmd[0]} (exit {r.returncode})")
+
+
+def _headers() -> list[str]:
+    return glob.glob(os.path.join(INC, "**", "*.h*"), recursive=True)
+
+
+def build_engine(force: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    srcs = sorted(glob.glob(os.path.join(CSRC, "engine", "*.cu")))
+    deps = srcs + glob.glob(os.path.join(CSRC, "engine", "*.cuh")) + _headers()
+    if not srcs:
+        raise RuntimeError("no engine sources")
+    if force or _stale(ENGINE_SO, deps):
+        objdir = os.path.join(ROOT, "build", "engine")
+        os.makedirs(objdir, exist_ok=True)
+        objs = []
+        for s in srcs:
+            o = os.path.join(objdir, os.path.basename(s) + ".o")
+            objs.append(o)
+            if force or _stale(o, [s] + deps[len(srcs):]):
+                _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                      "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", INC,
+                      "-I", os.path.join(CSRC, "engine"), "-c", s, "-o", o])
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", ENGINE_SO, *objs,
+              "-lpthread", "-ldl", "-lrt"])
+    return ENGINE_SO
+
+
+def build_host(force: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    srcs = sorted(glob.glob(os.path.join(CSRC, "host", "*.cpp")))
+    deps = srcs + _headers() + [ENGINE_SO]
+    if force or _stale(HOST_SO, deps):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra",
+              "-I", INC, "-I", NLOHMANN, *srcs, "-o", HOST_SO,
+              "-L", LIB, "-lmsw_engine", "-Wl,-rpath,$ORIGIN", "-lpthread"])
+    return HOST_SO
+
+
+def build_oracle(force: bool = False) -> None:
+    odir = os.path.join(ROOT, "oracle")
+    _run(["make", "-C", odir, "-j8", "all"] + (["-B"] if force else []))
+    if os.path.isdir("/root/reference/proj/core/src"):
+        _run(["make", "-C", odir, "-j8", "ref"])
+
+
+def build_all(force: bool = False) -> None:
+    build_engine(force)
+    build_host(force)
+    build_oracle(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

@@ -1,0 +1,115 @@
+// Shared device helpers for the sm_100a mode executor.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace msw {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ConfigErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DataErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define MSW_CUDA(expr)                                                            \
+  do {                                                                            \
+    cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess)                                                        \
+      throw ::msw::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define MSW_LAUNCH_CHECK() MSW_CUDA(cudaGetLastError())
+
+constexpr int kNumSMs = 148;
+constexpr int kKvBlock = 16;
+constexpr int kW4Group = 128;
+
+// ---- K16 deterministic init --------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t tensor_key(uint64_t seed, uint64_t tid) {
+  return mix64(seed ^ (tid * 0xD1B54A32D192ED03ull));
+}
+// uniform in [-1, 1), 2^-23 resolution, exact in fp32
+__host__ __device__ __forceinline__ float unif(uint64_t key, uint64_t idx) {
+  const uint64_t r = mix64(key + idx);
+  const int32_t u = static_cast<int32_t>(r >> 40);
+  return static_cast<float>(u - 8388608) * 1.1920928955078125e-07f;
+}
+
+constexpr uint64_t kTidDraftBase = 1ull << 32;
+constexpr uint64_t kTidEmbed = 1;
+constexpr uint64_t kTidFinalNorm = 3;
+__host__ __device__ constexpr uint64_t tid_layer(int l, int kind) {
+  return 256ull + 16ull * static_cast<uint64_t>(l) + static_cast<uint64_t>(kind);
+}
+enum TensorKind { kQ = 0, kK, kV, kO, kGate, kUp, kDown, kAttnNorm, kFfnNorm };
+constexpr uint64_t kSuccSalt = 0x5375636365737373ull;
+constexpr uint64_t kAgreeSalt = 0x4167726565416772ull;
+
+// ---- small device utilities -----------------------------------------------
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Streaming 128-bit weight load: read-only path, no L1 allocation.
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + expf(-g)); }
+
+// Block-wide reductions for <= 1024 threads; `red` needs 32 floats of smem.
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  float t = lane < nw ? red[lane] : 0.0f;
+  return warp_sum(t);
+}
+__device__ __forceinline__ float block_max(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  float t = lane < nw ? red[lane] : -3.402823466e38f;
+  return warp_max(t);
+}
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace msw

@@ -1,0 +1,1135 @@
+// The per-GPU mode executor behind include/msw_engine.h.
+//
+// All routable modes are resident at once (FP16, W8A8, W4 g128 weights of the
+// target plus the FP16 draft), so a mode switch at a request boundary is a
+// pointer switch. KV lives in a paged pool (16-token blocks) shared by all
+// modes; prefix caching maps content-hashed full prompt blocks (keyed by
+// weight format) onto already-computed physical blocks with refcounts and an
+// LRU of idle cached blocks. Batch-1 decode replays one CUDA graph per
+// (model, format) with the step state (token, position, slot, history) kept
+// on the device, so a request's decode loop never synchronises with the host.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <list>
+#include <memory>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels.cuh"
+#include "msw_engine.h"
+
+namespace msw {
+namespace {
+
+thread_local std::string g_last_error;
+
+constexpr int kPrefillChunk = 2048;
+constexpr int kMaxLogitRows = 64;
+
+int fmt_of_mode(int mode) {
+  switch (mode) {
+    case MSW_MODE_FP16:
+    case MSW_MODE_SPECULATIVE:
+      return kFP16;
+    case MSW_MODE_INT8:
+    case MSW_MODE_INT8_CONT_BATCHING:
+      return kINT8;
+    case MSW_MODE_GPTQ4:
+    case MSW_MODE_GPTQ_PREFIX_CACHING:
+      return kW4;
+    default:
+      throw ConfigErr("unsupported mode id " + std::to_string(mode));
+  }
+}
+
+int ceil_log2(long long x) {
+  int l = 0;
+  while ((1ll << l) < x) ++l;
+  return l;
+}
+int floor_log2(long long x) {
+  int l = 0;
+  while ((2ll << l) <= x) ++l;
+  return l;
+}
+int in_shift(long long k) { return (ceil_log2(k) + 1) / 2; }
+int res_shift(int layers) { return floor_log2(layers) / 2; }
+
+template <typename T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  MSW_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+// ---------------------------------------------------------------- block pool
+class BlockPool {
+ public:
+  void init(int n) {
+    n_ = n;
+    ref_.assign(n, 0);
+    key_.assign(n, 0);
+    lru_pos_.assign(n, lru_.end());
+    free_.clear();
+    for (int b = n - 1; b >= 0; --b) free_.push_back(b);
+  }
+  int alloc() {
+    int b;
+    if (!free_.empty()) {
+      b = free_.back();
+      free_.pop_back();
+    } else if (!lru_.empty()) {  // evict the least recently used idle cached block
+      b = lru_.front();
+      lru_.pop_front();
+      lru_pos_[b] = lru_.end();
+      cached_.erase(key_[b]);
+      key_[b] = 0;
+    } else {
+      throw DataErr("KV pool exhausted");
+    }
+    ref_[b] = 1;
+    return b;
+  }
+  int lookup(uint64_t key) {
+    auto it = cached_.find(key);
+    if (it == cached_.end()) return -1;
+    const int b = it->second;
+    if (ref_[b]++ == 0 && lru_pos_[b] != lru_.end()) {
+      lru_.erase(lru_pos_[b]);
+      lru_pos_[b] = lru_.end();
+    }
+    return b;
+  }
+  void publish(int b, uint64_t key) {
+    if (key == 0 || cached_.count(key)) return;
+    cached_[key] = b;
+    key_[b] = key;
+  }
+  void release(int b) {
+    if (--ref_[b] > 0) return;
+    if (key_[b] != 0) {
+      lru_.push_back(b);
+      lru_pos_[b] = std::prev(lru_.end());
+    } else {
+      free_.push_back(b);
+    }
+  }
+  void drop_cache() {
+    for (int b : lru_) {
+      lru_pos_[b] = lru_.end();
+      cached_.erase(key_[b]);
+      key_[b] = 0;
+      free_.push_back(b);
+    }
+    lru_.clear();
+    for (auto& kv : cached_) key_[kv.second] = 0;  // live blocks stay allocated, uncached
+    cached_.clear();
+  }
+  int available() const { return int(free_.size() + lru_.size()); }
+
+ private:
+  int n_ = 0;
+  std::vector<int> ref_;
+  std::vector<uint64_t> key_;
+  std::vector<int> free_;
+  std::list<int> lru_;
+  std::vector<std::list<int>::iterator> lru_pos_;
+  std::unordered_map<uint64_t, int> cached_;
+};
+
+// ---------------------------------------------------------------- model
+struct Layer {
+  half* attn_norm = nullptr;
+  half* ffn_norm = nullptr;
+  LinearW qkv[3], o[3], gu[3], down[3];
+};
+
+struct Model {
+  msw_model_cfg c{};
+  bool is_draft = false;
+  bool fmt_on[3] = {false, false, false};
+  half* embed = nullptr;
+  half* lm_head = nullptr;
+  half* final_norm = nullptr;
+  float* inv_freq = nullptr;
+  std::vector<Layer> layers;
+  half* kc = nullptr;
+  half* vc = nullptr;
+  size_t kv_layer_elems = 0;
+  int nblk = 0;
+  int max_blocks = 0;  // block-table row stride
+  int* block_table = nullptr;  // device [rows, max_blocks]
+  int bt_rows = 0;
+  int nsplit = 1;
+  AttnShape ash{};
+  BlockPool pool;
+  std::vector<void*> allocations;
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  int graph_nodes[3] = {0, 0, 0};
+
+  size_t weight_bytes(int fmt) const {
+    size_t b = size_t(c.vocab) * c.hidden * 2;  // fp16 lm_head in every mode
+    for (const Layer& l : layers)
+      b += l.qkv[fmt].bytes() + l.o[fmt].bytes() + l.gu[fmt].bytes() + l.down[fmt].bytes();
+    return b;
+  }
+};
+
+struct Scratch {
+  int tmax = 0;
+  float* h = nullptr;
+  float* qkv = nullptr;
+  half* q16 = nullptr;
+  float* o = nullptr;
+  float* act = nullptr;
+  half* xh = nullptr;
+  int8_t* xq = nullptr;
+  float* xscale = nullptr;
+  float* hsel = nullptr;
+  float* logits = nullptr;
+  float* part_o = nullptr;
+  float* part_ml = nullptr;
+  int* tok = nullptr;
+  int* pos = nullptr;
+  int* slot = nullptr;
+  int* seq_of = nullptr;
+  int* logit_rows = nullptr;
+  int* next = nullptr;
+  int* step = nullptr;
+  int* hist = nullptr;
+  int* stage = nullptr;  // pinned host staging
+  size_t stage_ints = 0;
+};
+
+}  // namespace
+}  // namespace msw
+
+struct msw_engine {
+  int device = 0;
+  msw_engine_cfg cfg{};
+  cudaStream_t st = nullptr;
+  msw::Model target, draft;
+  msw::Scratch sc;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  long long launches = 0;
+  std::vector<void*> owned;
+};
+
+namespace msw {
+namespace {
+
+// ------------------------------------------------------------ weight build
+void build_successor(const msw_engine_cfg& cfg, int V, std::vector<int>& pred,
+                     std::vector<uint8_t>& agree) {
+  std::vector<std::pair<uint64_t, int>> order(V);
+  const uint64_t skey = mix64(cfg.weight_seed ^ kSuccSalt);
+  for (int v = 0; v < V; ++v) order[v] = {mix64(skey + uint64_t(v)), v};
+  std::sort(order.begin(), order.end());
+  pred.assign(V, 0);
+  for (int i = 0; i < V; ++i) pred[order[(i + 1) % V].second] = order[i].second;
+  agree.assign(V, 0);
+  const uint64_t akey = mix64(cfg.weight_seed ^ kAgreeSalt);
+  for (int t = 0; t < V; ++t)
+    agree[t] = int(mix64(akey + uint64_t(t)) % 1000ull) < cfg.draft_agree_permille ? 1 : 0;
+}
+
+template <typename T>
+T* model_alloc(Model& m, size_t count) {
+  T* p = dalloc<T>(count);
+  m.allocations.push_back(p);
+  return p;
+}
+
+LinearW make_linear(Model& m, int fmt, const half* master, int n, int k, cudaStream_t st) {
+  LinearW L;
+  L.fmt = fmt;
+  L.n = n;
+  L.k = k;
+  if (fmt == kFP16) {
+    half* w = model_alloc<half>(m, size_t(n) * k);
+    MSW_CUDA(cudaMemcpyAsync(w, master, size_t(n) * k * 2, cudaMemcpyDeviceToDevice, st));
+    L.w = w;
+  } else if (fmt == kINT8) {
+    int8_t* q = model_alloc<int8_t>(m, size_t(n) * k);
+    float* s = model_alloc<float>(m, n);
+    launch_quant_int8(master, n, k, q, s, st);
+    L.w = q;
+    L.s = s;
+  } else {
+    uint32_t* q = model_alloc<uint32_t>(m, size_t(n) * k / 8);
+    half* s = model_alloc<half>(m, size_t(n) * (k / kW4Group));
+    launch_quant_w4(master, n, k, q, s, st);
+    L.w = q;
+    L.s = s;
+  }
+  return L;
+}
+
+void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engine_cfg& cfg,
+                 const std::vector<int>& pred, const std::vector<uint8_t>& agree, cudaStream_t st) {
+  m.c = c;
+  m.is_draft = is_draft;
+  const int H = c.hidden, V = c.vocab, L = c.n_layers, D = c.head_dim;
+  const int Hq = c.n_heads, Hk = c.n_kv_heads, F = c.ffn;
+  if (H % 128 || F % 128 || (Hq * D) % 128 || Hq % Hk || (D != 64 && D != 128))
+    throw ConfigErr("model shape: hidden/ffn/heads*head_dim must be multiples of 128, head_dim 64|128");
+  const uint64_t base = is_draft ? kTidDraftBase : 0ull;
+  const uint64_t seed = cfg.weight_seed;
+
+  m.embed = model_alloc<half>(m, size_t(V) * H);
+  launch_fill_fp16(m.embed, V, H, seed, base + kTidEmbed, 0, st);
+  m.final_norm = model_alloc<half>(m, H);
+  launch_fill_norm(m.final_norm, H, seed, base + kTidFinalNorm, st);
+  {
+    int* d_pred = dalloc<int>(V);
+    uint8_t* d_agree = dalloc<uint8_t>(V);
+    MSW_CUDA(cudaMemcpy(d_pred, pred.data(), sizeof(int) * V, cudaMemcpyHostToDevice));
+    MSW_CUDA(cudaMemcpy(d_agree, agree.data(), V, cudaMemcpyHostToDevice));
+    m.lm_head = model_alloc<half>(m, size_t(V) * H);
+    launch_lm_head(m.embed, d_pred, d_agree, is_draft ? 1 : 0, V, H, m.lm_head, st);
+    MSW_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_pred);
+    cudaFree(d_agree);
+  }
+
+  // which formats this model needs resident
+  const uint32_t mm = cfg.modes_mask;
+  if (is_draft) {
+    m.fmt_on[kFP16] = true;
+  } else {
+    m.fmt_on[kFP16] = mm & ((1u << MSW_MODE_FP16) | (1u << MSW_MODE_SPECULATIVE));
+    m.fmt_on[kINT8] = mm & ((1u << MSW_MODE_INT8) | (1u << MSW_MODE_INT8_CONT_BATCHING));
+    m.fmt_on[kW4] = mm & ((1u << MSW_MODE_GPTQ4) | (1u << MSW_MODE_GPTQ_PREFIX_CACHING));
+  }
+
+  const size_t max_elems = std::max({size_t(Hq + 2 * Hk) * D * H, size_t(2) * F * H,
+                                     size_t(H) * Hq * D, size_t(H) * F});
+  half* master = dalloc<half>(max_elems);
+  half* tmp_a = dalloc<half>(size_t(F) * H);
+  half* tmp_b = dalloc<half>(size_t(F) * H);
+  const int rs = res_shift(L);
+  m.layers.resize(L);
+  for (int l = 0; l < L; ++l) {
+    Layer& ly = m.layers[l];
+    ly.attn_norm = model_alloc<half>(m, H);
+    ly.ffn_norm = model_alloc<half>(m, H);
+    launch_fill_norm(ly.attn_norm, H, seed, base + tid_layer(l, kAttnNorm), st);
+    launch_fill_norm(ly.ffn_norm, H, seed, base + tid_layer(l, kFfnNorm), st);
+    auto each_fmt = [&](LinearW (&dst)[3], int n, int k) {
+      for (int f = 0; f < 3; ++f)
+        if (m.fmt_on[f]) dst[f] = make_linear(m, f, master, n, k, st);
+    };
+    // qkv: rows [q (Hq*D); k (Hk*D); v (Hk*D)]
+    launch_fill_fp16(master, size_t(Hq) * D, H, seed, base + tid_layer(l, kQ), in_shift(H), st);
+    launch_fill_fp16(master + size_t(Hq) * D * H, size_t(Hk) * D, H, seed,
+                     base + tid_layer(l, kK), in_shift(H), st);
+    launch_fill_fp16(master + size_t(Hq + Hk) * D * H, size_t(Hk) * D, H, seed,
+                     base + tid_layer(l, kV), in_shift(H), st);
+    each_fmt(ly.qkv, (Hq + 2 * Hk) * D, H);
+    launch_fill_fp16(master, H, size_t(Hq) * D, seed, base + tid_layer(l, kO),
+                     in_shift(Hq * D) + rs, st);
+    each_fmt(ly.o, H, Hq * D);
+    // gate/up interleaved by row (2i = gate_i, 2i+1 = up_i)
+    launch_fill_fp16(tmp_a, F, H, seed, base + tid_layer(l, kGate), in_shift(H), st);
+    launch_fill_fp16(tmp_b, F, H, seed, base + tid_layer(l, kUp), in_shift(H), st);
+    launch_interleave_rows(tmp_a, tmp_b, F, size_t(H) * 2, master, st);
+    each_fmt(ly.gu, 2 * F, H);
+    launch_fill_fp16(master, H, F, seed, base + tid_layer(l, kDown), in_shift(F) + rs, st);
+    each_fmt(ly.down, H, F);
+    MSW_CUDA(cudaStreamSynchronize(st));  // master is reused next layer
+  }
+  cudaFree(master);
+  cudaFree(tmp_a);
+  cudaFree(tmp_b);
+
+  // llama3 rope inverse frequencies (transformers _compute_llama3_parameters)
+  std::vector<float> inv(D / 2);
+  for (int j = 0; j < D / 2; ++j) {
+    double f = std::pow(double(c.rope_theta), -(2.0 * j) / double(D));
+    if (c.rope_factor > 0.0f) {
+      const double lo_wl = c.rope_orig_ctx / c.rope_low_freq_factor;
+      const double hi_wl = c.rope_orig_ctx / c.rope_high_freq_factor;
+      const double wl = 2.0 * 3.14159265358979323846 / f;
+      if (wl > lo_wl) {
+        f = f / c.rope_factor;
+      } else if (wl >= hi_wl) {
+        const double sm = (c.rope_orig_ctx / wl - c.rope_low_freq_factor) /
+                          (c.rope_high_freq_factor - c.rope_low_freq_factor);
+        f = (1.0 - sm) * f / c.rope_factor + sm * f;
+      }
+    }
+    inv[j] = float(f);
+  }
+  m.inv_freq = model_alloc<float>(m, D / 2);
+  MSW_CUDA(cudaMemcpy(m.inv_freq, inv.data(), sizeof(float) * inv.size(), cudaMemcpyHostToDevice));
+
+  // paged KV pool
+  m.nblk = cfg.kv_blocks;
+  m.kv_layer_elems = size_t(m.nblk) * Hk * kKvBlock * D;
+  m.kc = model_alloc<half>(m, m.kv_layer_elems * L);
+  m.vc = model_alloc<half>(m, m.kv_layer_elems * L);
+  m.max_blocks = (cfg.max_seq_len + kKvBlock - 1) / kKvBlock + 2;
+  m.bt_rows = is_draft ? 1 : std::max(1, cfg.max_batch);
+  m.block_table = model_alloc<int>(m, size_t(m.bt_rows) * m.max_blocks);
+  MSW_CUDA(cudaMemset(m.block_table, 0, sizeof(int) * size_t(m.bt_rows) * m.max_blocks));
+  m.pool.init(m.nblk);
+  m.ash = AttnShape{Hq, Hk, D, m.max_blocks};
+  m.nsplit = std::max(1, std::min(32, (2 * kNumSMs) / Hk));
+}
+
+void free_model(Model& m) {
+  for (auto& g : m.graph)
+    if (g) cudaGraphExecDestroy(g);
+  for (void* p : m.allocations) cudaFree(p);
+  m.allocations.clear();
+}
+
+void alloc_scratch(msw_engine* e) {
+  Scratch& s = e->sc;
+  const msw_model_cfg& t = e->cfg.target;
+  const msw_model_cfg& d = e->cfg.has_draft ? e->cfg.draft : e->cfg.target;
+  const int T = std::max({kPrefillChunk, e->cfg.max_batch, e->cfg.spec_k + 1, 8});
+  s.tmax = T;
+  auto mx = [&](auto f) { return std::max(f(t), f(d)); };
+  const size_t H = mx([](const msw_model_cfg& c) { return size_t(c.hidden); });
+  const size_t QKV = mx([](const msw_model_cfg& c) {
+    return size_t(c.n_heads + 2 * c.n_kv_heads) * c.head_dim;
+  });
+  const size_t QD = mx([](const msw_model_cfg& c) { return size_t(c.n_heads) * c.head_dim; });
+  const size_t F = mx([](const msw_model_cfg& c) { return size_t(c.ffn); });
+  const size_t V = mx([](const msw_model_cfg& c) { return size_t(c.vocab); });
+  const size_t K = std::max({H, QD, F});
+  const size_t HQ = mx([](const msw_model_cfg& c) { return size_t(c.n_heads); });
+  const size_t D = mx([](const msw_model_cfg& c) { return size_t(c.head_dim); });
+  const size_t tsplit = std::max<size_t>(kMaxLogitRows, e->cfg.spec_k + 1);
+  s.h = dalloc<float>(T * H);
+  s.qkv = dalloc<float>(T * QKV);
+  s.q16 = dalloc<half>(T * QD);
+  s.o = dalloc<float>(T * QD);
+  s.act = dalloc<float>(T * F);
+  s.xh = dalloc<half>(T * K);
+  s.xq = dalloc<int8_t>(T * K);
+  s.xscale = dalloc<float>(T);
+  s.hsel = dalloc<float>(kMaxLogitRows * H);
+  s.logits = dalloc<float>(kMaxLogitRows * V);
+  s.part_o = dalloc<float>(tsplit * HQ * 32 * D);
+  s.part_ml = dalloc<float>(tsplit * HQ * 32 * 2);
+  s.tok = dalloc<int>(T);
+  s.pos = dalloc<int>(T);
+  s.slot = dalloc<int>(T);
+  s.seq_of = dalloc<int>(T);
+  s.logit_rows = dalloc<int>(kMaxLogitRows);
+  s.next = dalloc<int>(kMaxLogitRows);
+  s.step = dalloc<int>(1);
+  s.hist = dalloc<int>(size_t(e->cfg.max_seq_len) + 64);
+  s.stage_ints = size_t(T) * 4 + 256;
+  MSW_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.stage), s.stage_ints * sizeof(int),
+                         cudaHostAllocDefault));
+  for (void* p : {(void*)s.h, (void*)s.qkv, (void*)s.q16, (void*)s.o, (void*)s.act, (void*)s.xh,
+                  (void*)s.xq, (void*)s.xscale, (void*)s.hsel, (void*)s.logits, (void*)s.part_o,
+                  (void*)s.part_ml, (void*)s.tok, (void*)s.pos, (void*)s.slot, (void*)s.seq_of,
+                  (void*)s.logit_rows, (void*)s.next, (void*)s.step, (void*)s.hist})
+    e->owned.push_back(p);
+}
+
+// ------------------------------------------------------------ forward pass
+// Runs T tokens (inputs already in sc.tok/pos/slot/seq_of) through model m in
+// format fmt; logits + argmax for the n_logits rows listed in sc.logit_rows
+// (rows == nullptr means rows 0..n_logits-1 == all T rows).
+void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_identity) {
+  Scratch& s = e->sc;
+  cudaStream_t st = e->st;
+  const msw_model_cfg& c = m.c;
+  const int H = c.hidden, D = c.head_dim, Hq = c.n_heads, Hk = c.n_kv_heads, F = c.ffn;
+  const float eps = c.rms_eps;
+  const bool small = T <= kGemvMaxTokens;
+  const int nsplit = T <= kMaxLogitRows ? m.nsplit : 1;
+  long long& n = e->launches;
+
+  launch_embed(m.embed, s.tok, T, H, s.h, st);
+  ++n;
+  for (int l = 0; l < c.n_layers; ++l) {
+    const Layer& ly = m.layers[l];
+    half* kc = m.kc + m.kv_layer_elems * l;
+    half* vc = m.vc + m.kv_layer_elems * l;
+    // attention block
+    if (small) {
+      launch_gemv(ly.qkv[fmt], kProNorm, kEpiStore, s.h, T, ly.attn_norm, eps, s.qkv, st);
+      ++n;
+    } else {
+      launch_prep_act(fmt, s.h, T, H, ly.attn_norm, eps, s.xh, s.xq, s.xscale, st);
+      launch_gemm(ly.qkv[fmt], kEpiStore, s.xh, s.xq, s.xscale, T, s.qkv, st);
+      n += 2;
+    }
+    launch_rope_append(s.qkv, T, s.pos, s.slot, m.inv_freq, m.ash, s.q16, kc, vc, st);
+    launch_attention(s.q16, T, s.pos, s.seq_of, m.block_table, kc, vc, m.ash, nsplit, s.part_o,
+                     s.part_ml, s.o, st);
+    n += nsplit > 1 ? 3 : 2;
+    if (small) {
+      launch_gemv(ly.o[fmt], kProPlain, kEpiResid, s.o, T, nullptr, eps, s.h, st);
+      launch_gemv(ly.gu[fmt], kProNorm, kEpiSwiglu, s.h, T, ly.ffn_norm, eps, s.act, st);
+      launch_gemv(ly.down[fmt], kProPlain, kEpiResid, s.act, T, nullptr, eps, s.h, st);
+      n += 3;
+    } else {
+      launch_prep_act(fmt, s.o, T, Hq * D, nullptr, eps, s.xh, s.xq, s.xscale, st);
+      launch_gemm(ly.o[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, st);
+      launch_prep_act(fmt, s.h, T, H, ly.ffn_norm, eps, s.xh, s.xq, s.xscale, st);
+      launch_gemm(ly.gu[fmt], kEpiSwiglu, s.xh, s.xq, s.xscale, T, s.act, st);
+      launch_prep_act(fmt, s.act, T, F, nullptr, eps, s.xh, s.xq, s.xscale, st);
+      launch_gemm(ly.down[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, st);
+      n += 6;
+    }
+    (void)Hk;
+  }
+  // final norm + fp16 lm_head on the requested rows, then greedy argmax
+  const float* hrows = s.h;
+  if (!rows_identity) {
+    launch_gather_rows(s.h, s.logit_rows, n_logits, H, s.hsel, st);
+    hrows = s.hsel;
+    ++n;
+  }
+  LinearW head;
+  head.fmt = kFP16;
+  head.n = c.vocab;
+  head.k = H;
+  head.w = m.lm_head;
+  if (n_logits <= kGemvMaxTokens) {
+    launch_gemv(head, kProNorm, kEpiStore, hrows, n_logits, m.final_norm, eps, s.logits, st);
+    ++n;
+  } else {
+    launch_prep_act(kFP16, hrows, n_logits, H, m.final_norm, eps, s.xh, s.xq, s.xscale, st);
+    launch_gemm(head, kEpiStore, s.xh, s.xq, s.xscale, n_logits, s.logits, st);
+    n += 2;
+  }
+  launch_argmax(s.logits, n_logits, c.vocab, s.next, st);
+  ++n;
+}
+
+// ------------------------------------------------------------ sequences
+struct SeqBlocks {
+  std::vector<int> blocks;
+  int hit_tokens = 0;
+  std::vector<uint64_t> keys;  // prefix keys of full prompt blocks (prefix caching)
+};
+
+uint64_t block_key(uint64_t prev, int fmt, const int32_t* toks) {
+  uint64_t h = mix64(prev ^ (0xB10C0000ull + uint64_t(fmt)));
+  for (int i = 0; i < kKvBlock; ++i) h = mix64(h ^ uint64_t(uint32_t(toks[i])));
+  return h == 0 ? 1 : h;
+}
+
+// Maps n_positions KV slots for a sequence onto pool blocks; with prefix
+// caching, leading full prompt blocks are looked up by content key.
+SeqBlocks map_sequence(Model& m, int row, int n_positions, const int32_t* prompt, int plen,
+                       bool prefix, int fmt, cudaStream_t st, int* stage) {
+  SeqBlocks sb;
+  const int nb = (n_positions + kKvBlock - 1) / kKvBlock;
+  if (nb > m.max_blocks) throw DataErr("sequence longer than max_seq_len");
+  int b = 0;
+  if (prefix) {
+    uint64_t key = 0x5EEDull;
+    const int full = plen / kKvBlock;
+    for (int i = 0; i < full; ++i) {
+      key = block_key(key, fmt, prompt + size_t(i) * kKvBlock);
+      sb.keys.push_back(key);
+    }
+    const int max_hit = (plen - 1) / kKvBlock;  // keep >= 1 prompt token to prefill
+    for (; b < max_hit; ++b) {
+      const int blk = m.pool.lookup(sb.keys[b]);
+      if (blk < 0) break;
+      sb.blocks.push_back(blk);
+    }
+    sb.hit_tokens = b * kKvBlock;
+  }
+  try {
+    for (; b < nb; ++b) sb.blocks.push_back(m.pool.alloc());
+  } catch (...) {
+    for (int blk : sb.blocks) m.pool.release(blk);
+    throw;
+  }
+  for (int i = 0; i < nb; ++i) stage[i] = sb.blocks[i];
+  MSW_CUDA(cudaMemcpyAsync(m.block_table + size_t(row) * m.max_blocks, stage, sizeof(int) * nb,
+                           cudaMemcpyHostToDevice, st));
+  MSW_CUDA(cudaStreamSynchronize(st));
+  return sb;
+}
+
+void publish_prefix(Model& m, const SeqBlocks& sb) {
+  for (size_t i = sb.hit_tokens / kKvBlock; i < sb.keys.size(); ++i)
+    m.pool.publish(sb.blocks[i], sb.keys[i]);
+}
+
+void release_sequence(Model& m, const SeqBlocks& sb) {
+  for (int b : sb.blocks) m.pool.release(b);
+}
+
+// Prefill tokens [from, plen) of one sequence (block-table row `row`), in
+// chunks; the last chunk yields logits/argmax for the last prompt token.
+void prefill(msw_engine* e, Model& m, int fmt, int row, const int32_t* prompt, int from, int plen,
+             const SeqBlocks& sb) {
+  Scratch& s = e->sc;
+  for (int c0 = from; c0 < plen; c0 += kPrefillChunk) {
+    const int T = std::min(kPrefillChunk, plen - c0);
+    int* st_tok = s.stage;
+    int* st_pos = s.stage + T;
+    int* st_slot = s.stage + 2 * T;
+    int* st_seq = s.stage + 3 * T;
+    for (int i = 0; i < T; ++i) {
+      const int p = c0 + i;
+      st_tok[i] = prompt[p];
+      st_pos[i] = p;
+      st_slot[i] = sb.blocks[p / kKvBlock] * kKvBlock + p % kKvBlock;
+      st_seq[i] = row;
+    }
+    MSW_CUDA(cudaMemcpyAsync(s.tok, st_tok, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+    MSW_CUDA(cudaMemcpyAsync(s.pos, st_pos, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+    MSW_CUDA(cudaMemcpyAsync(s.slot, st_slot, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+    MSW_CUDA(cudaMemcpyAsync(s.seq_of, st_seq, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+    const bool last = c0 + T >= plen;
+    if (last && T > 1) {
+      int* st_rows = s.stage + 4 * T;
+      st_rows[0] = T - 1;
+      MSW_CUDA(cudaMemcpyAsync(s.logit_rows, st_rows, sizeof(int), cudaMemcpyHostToDevice, e->st));
+    }
+    forward(e, m, fmt, T, 1, /*rows_identity=*/T == 1);
+    MSW_CUDA(cudaStreamSynchronize(e->st));  // staging is reused by the next chunk
+  }
+}
+
+// One batch-1 decode step for model m / fmt, as a graph or eagerly.
+void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph) {
+  Scratch& s = e->sc;
+  auto body = [&]() {
+    forward(e, m, fmt, 1, 1, true);
+    launch_advance(s.next, s.tok, s.pos, s.slot, s.step, s.hist, m.block_table, e->st);
+    ++e->launches;
+  };
+  if (!use_graph) {
+    body();
+    return;
+  }
+  if (!m.graph[fmt]) {
+    const long long before = e->launches;
+    cudaGraph_t g;
+    MSW_CUDA(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
+    try {
+      body();
+    } catch (...) {
+      cudaStreamEndCapture(e->st, &g);
+      throw;
+    }
+    MSW_CUDA(cudaStreamEndCapture(e->st, &g));
+    MSW_CUDA(cudaGraphInstantiate(&m.graph[fmt], g, 0));
+    cudaGraphDestroy(g);
+    m.graph_nodes[fmt] = int(e->launches - before);
+    e->launches = before;
+  }
+  MSW_CUDA(cudaGraphLaunch(m.graph[fmt], e->st));
+  e->launches += m.graph_nodes[fmt];
+}
+
+// Sets the batch-1 decode state so the next decode_step processes `tok_src`
+// (device int) at position pos; history[step0 ..] continues.
+void start_decode(msw_engine* e, Model& m, const int* next_src, int pos_before, int step0) {
+  Scratch& s = e->sc;
+  int* st = s.stage + s.stage_ints - 8;
+  st[0] = pos_before;
+  st[1] = step0;
+  MSW_CUDA(cudaMemcpyAsync(s.pos, &st[0], sizeof(int), cudaMemcpyHostToDevice, e->st));
+  MSW_CUDA(cudaMemcpyAsync(s.step, &st[1], sizeof(int), cudaMemcpyHostToDevice, e->st));
+  // advance: history[step0] = next, tok = next, pos = pos_before + 1, slot
+  launch_advance(next_src, s.tok, s.pos, s.slot, s.step, s.hist, m.block_table, e->st);
+  ++e->launches;
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+void check_request(msw_engine* e, const msw_request& r, int extra) {
+  if (r.prompt_len < 1 || r.max_new_tokens < 1) throw DataErr("prompt_len and max_new_tokens must be >= 1");
+  if (r.prompt_ids == nullptr) throw DataErr("prompt_ids is NULL");
+  if (r.prompt_len + r.max_new_tokens + extra > e->cfg.max_seq_len)
+    throw DataErr("request exceeds max_seq_len");
+  for (int i = 0; i < r.prompt_len; ++i)
+    if (r.prompt_ids[i] < 0 || r.prompt_ids[i] >= e->cfg.target.vocab)
+      throw DataErr("token id out of range");
+}
+
+void copy_logits_row(msw_engine* e, float* dst_host, int row) {
+  MSW_CUDA(cudaMemcpyAsync(dst_host, e->sc.logits + size_t(row) * e->cfg.target.vocab,
+                           sizeof(float) * e->cfg.target.vocab, cudaMemcpyDeviceToHost, e->st));
+}
+
+// ---------------------------------------------------------------- modes
+void run_single(msw_engine* e, const msw_request& r, msw_result& res) {
+  const int fmt = fmt_of_mode(r.mode);
+  Model& m = e->target;
+  if (!m.fmt_on[fmt]) throw ConfigErr("mode not resident in this engine");
+  check_request(e, r, 1);
+  const double t0 = now_ms();
+  const bool prefix = r.mode == MSW_MODE_GPTQ_PREFIX_CACHING;
+  const int n_new = r.max_new_tokens;
+  SeqBlocks sb = map_sequence(m, 0, r.prompt_len + n_new, r.prompt_ids, r.prompt_len, prefix, fmt,
+                              e->st, e->sc.stage);
+  const bool want_logits = res.logits != nullptr;
+  const bool graphs = e->cfg.use_graphs && !want_logits;
+  try {
+    MSW_CUDA(cudaEventRecord(e->ev[0], e->st));
+    prefill(e, m, fmt, 0, r.prompt_ids, sb.hit_tokens, r.prompt_len, sb);
+    if (want_logits) copy_logits_row(e, res.logits, 0);
+    start_decode(e, m, e->sc.next, r.prompt_len - 1, 0);
+    MSW_CUDA(cudaEventRecord(e->ev[1], e->st));
+    for (int i = 1; i < n_new; ++i) {
+      decode_step(e, m, fmt, graphs);
+      if (want_logits) copy_logits_row(e, res.logits + size_t(i) * m.c.vocab, 0);
+    }
+    MSW_CUDA(cudaEventRecord(e->ev[2], e->st));
+    MSW_CUDA(cudaMemcpyAsync(res.out_ids, e->sc.hist, sizeof(int) * n_new, cudaMemcpyDeviceToHost,
+                             e->st));
+    MSW_CUDA(cudaStreamSynchronize(e->st));
+  } catch (...) {
+    release_sequence(m, sb);
+    throw;
+  }
+  if (prefix) publish_prefix(m, sb);
+  release_sequence(m, sb);
+  float a = 0, b = 0;
+  MSW_CUDA(cudaEventElapsedTime(&a, e->ev[0], e->ev[1]));
+  MSW_CUDA(cudaEventElapsedTime(&b, e->ev[1], e->ev[2]));
+  res.prefill_ms = a;
+  res.decode_ms = b;
+  res.n_out = n_new;
+  res.prefix_hit_tokens = sb.hit_tokens;
+  res.total_ms = now_ms() - t0;
+}
+
+// Speculative decoding: FP16 target + FP16 draft, k greedy proposals, one
+// batched verify of k+1 tokens; emitted tokens are the target's greedy tokens.
+void run_spec(msw_engine* e, const msw_request& r, msw_result& res) {
+  if (!e->cfg.has_draft) throw ConfigErr("speculative decoding needs a draft model");
+  Model& tg = e->target;
+  Model& dr = e->draft;
+  if (!tg.fmt_on[kFP16]) throw ConfigErr("speculative decoding needs the FP16 target");
+  const int k = e->cfg.spec_k;
+  if (k < 1 || k + 1 > kGemvMaxTokens) throw ConfigErr("spec_k must be in [1, 5]");
+  check_request(e, r, k + 2);
+  Scratch& s = e->sc;
+  const int plen = r.prompt_len, n_new = r.max_new_tokens, V = tg.c.vocab;
+  const double t0 = now_ms();
+  const int npos = plen + n_new + k + 2;
+  SeqBlocks tb = map_sequence(tg, 0, npos, r.prompt_ids, plen, false, kFP16, e->st, s.stage);
+  SeqBlocks db;
+  try {
+    db = map_sequence(dr, 0, npos, r.prompt_ids, plen, false, kFP16, e->st, s.stage);
+  } catch (...) {
+    release_sequence(tg, tb);
+    throw;
+  }
+  const bool want_logits = res.logits != nullptr;
+  const bool graphs = e->cfg.use_graphs != 0;
+  std::vector<int32_t> seq(r.prompt_ids, r.prompt_ids + plen);
+  seq.reserve(npos + 8);
+  int rounds = 0, proposed = 0, accepted = 0;
+  float prefill_ms = 0, decode_ms = 0;
+  try {
+    MSW_CUDA(cudaEventRecord(e->ev[0], e->st));
+    prefill(e, dr, kFP16, 0, r.prompt_ids, 0, plen, db);
+    prefill(e, tg, kFP16, 0, r.prompt_ids, 0, plen, tb);
+    int first = 0;
+    MSW_CUDA(cudaMemcpyAsync(s.stage, s.next, sizeof(int), cudaMemcpyDeviceToHost, e->st));
+    if (want_logits) copy_logits_row(e, res.logits, 0);
+    MSW_CUDA(cudaEventRecord(e->ev[1], e->st));
+    MSW_CUDA(cudaStreamSynchronize(e->st));
+    first = s.stage[0];
+    seq.push_back(first);
+    res.out_ids[0] = first;
+    int emitted = 1;
+    int dlen = plen;  // positions present in the draft cache
+    std::vector<int> props(k), g(k + 1);
+    while (emitted < n_new) {
+      const int n = int(seq.size());
+      // draft catch-up (only after a fully accepted round): positions dlen .. n-2
+      if (dlen < n - 1) {
+        const int T = n - 1 - dlen;
+        for (int i = 0; i < T; ++i) {
+          const int p = dlen + i;
+          s.stage[i] = seq[p];
+          s.stage[T + i] = p;
+          s.stage[2 * T + i] = db.blocks[p / kKvBlock] * kKvBlock + p % kKvBlock;
+          s.stage[3 * T + i] = 0;
+        }
+        MSW_CUDA(cudaMemcpyAsync(s.tok, s.stage, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+        MSW_CUDA(cudaMemcpyAsync(s.pos, s.stage + T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+        MSW_CUDA(cudaMemcpyAsync(s.slot, s.stage + 2 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+        MSW_CUDA(cudaMemcpyAsync(s.seq_of, s.stage + 3 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+        if (T > 1) {
+          s.stage[4 * T] = T - 1;
+          MSW_CUDA(cudaMemcpyAsync(s.logit_rows, s.stage + 4 * T, sizeof(int), cudaMemcpyHostToDevice, e->st));
+        }
+        forward(e, dr, kFP16, T, 1, T == 1);
+        MSW_CUDA(cudaStreamSynchronize(e->st));
+        dlen = n - 1;
+      }
+      // k greedy draft proposals from seq[n-1] at position n-1 (device-resident loop)
+      s.stage[0] = seq[n - 1];
+      MSW_CUDA(cudaMemcpyAsync(s.next, s.stage, sizeof(int), cudaMemcpyHostToDevice, e->st));
+      start_decode(e, dr, s.next, n - 2, 0);  // tok = seq[n-1], pos = n-1, hist[0] = seq[n-1]
+      for (int i = 0; i < k; ++i) decode_step(e, dr, kFP16, graphs);
+      // hist[1..k] are the proposals
+      MSW_CUDA(cudaMemcpyAsync(s.stage + 8, s.hist + 1, sizeof(int) * k, cudaMemcpyDeviceToHost, e->st));
+      MSW_CUDA(cudaStreamSynchronize(e->st));
+      for (int i = 0; i < k; ++i) props[i] = s.stage[8 + i];
+      dlen = n - 1 + k;
+      // target verify: [seq[n-1], d_1..d_k] at positions n-1 .. n-1+k
+      const int T = k + 1;
+      for (int i = 0; i < T; ++i) {
+        const int p = n - 1 + i;
+        s.stage[i] = i == 0 ? seq[n - 1] : props[i - 1];
+        s.stage[T + i] = p;
+        s.stage[2 * T + i] = tb.blocks[p / kKvBlock] * kKvBlock + p % kKvBlock;
+        s.stage[3 * T + i] = 0;
+      }
+      MSW_CUDA(cudaMemcpyAsync(s.tok, s.stage, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+      MSW_CUDA(cudaMemcpyAsync(s.pos, s.stage + T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+      MSW_CUDA(cudaMemcpyAsync(s.slot, s.stage + 2 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+      MSW_CUDA(cudaMemcpyAsync(s.seq_of, s.stage + 3 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+      forward(e, tg, kFP16, T, T, true);
+      MSW_CUDA(cudaMemcpyAsync(s.stage + 8, s.next, sizeof(int) * T, cudaMemcpyDeviceToHost, e->st));
+      MSW_CUDA(cudaStreamSynchronize(e->st));
+      for (int i = 0; i < T; ++i) g[i] = s.stage[8 + i];
+      int j = 0;
+      while (j < k && props[j] == g[j]) ++j;
+      ++rounds;
+      proposed += k;
+      accepted += j;
+      for (int i = 0; i <= j && emitted < n_new; ++i) {
+        seq.push_back(g[i]);
+        res.out_ids[emitted] = g[i];
+        if (want_logits) {
+          copy_logits_row(e, res.logits + size_t(emitted) * V, i);
+          MSW_CUDA(cudaStreamSynchronize(e->st));
+        }
+        ++emitted;
+      }
+      dlen = std::min(dlen, int(seq.size()) - 1);
+    }
+    MSW_CUDA(cudaEventRecord(e->ev[2], e->st));
+    MSW_CUDA(cudaStreamSynchronize(e->st));
+    MSW_CUDA(cudaEventElapsedTime(&prefill_ms, e->ev[0], e->ev[1]));
+    MSW_CUDA(cudaEventElapsedTime(&decode_ms, e->ev[1], e->ev[2]));
+  } catch (...) {
+    release_sequence(tg, tb);
+    release_sequence(dr, db);
+    throw;
+  }
+  release_sequence(tg, tb);
+  release_sequence(dr, db);
+  res.n_out = n_new;
+  res.prefill_ms = prefill_ms;
+  res.decode_ms = decode_ms;
+  res.spec_rounds = rounds;
+  res.spec_proposed = proposed;
+  res.spec_accepted = accepted;
+  res.total_ms = now_ms() - t0;
+}
+
+// INT8 + continuous batching: iteration-level scheduling of a co-scheduled
+// cohort. Up to max_batch live sequences; each engine step decodes one token
+// for every live sequence (ragged positions, one block-table row each);
+// finished sequences retire and queued ones are admitted (prefilled) before
+// the next step. Per-request latency = its admission to its last token.
+void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
+  Model& m = e->target;
+  const int fmt = kINT8;
+  if (!m.fmt_on[fmt]) throw ConfigErr("INT8 weights not resident");
+  const int maxb = std::min(e->cfg.max_batch, std::min(m.bt_rows, kMaxLogitRows));
+  for (int i = 0; i < n; ++i) {
+    if (reqs[i].mode != MSW_MODE_INT8_CONT_BATCHING) throw ConfigErr("run_batch: mode must be int8_continuous_batching");
+    check_request(e, reqs[i], 1);
+  }
+  Scratch& s = e->sc;
+  struct Live {
+    int req;
+    int row;
+    int generated;
+    int last_tok;
+    SeqBlocks sb;
+    double t_admit;
+  };
+  std::vector<Live> live;
+  std::vector<int> free_rows;
+  for (int r = maxb - 1; r >= 0; --r) free_rows.push_back(r);
+  int next_req = 0;
+  const double t0 = now_ms();
+  double decode_time = 0, prefill_time = 0;
+  std::vector<int> step_tok(maxb);
+  try {
+    while (next_req < n || !live.empty()) {
+      // admission
+      while (next_req < n && !free_rows.empty()) {
+        const msw_request& r = reqs[next_req];
+        Live L;
+        L.req = next_req;
+        L.row = free_rows.back();
+        L.generated = 0;
+        L.t_admit = now_ms();
+        L.sb = map_sequence(m, L.row, r.prompt_len + r.max_new_tokens, r.prompt_ids, r.prompt_len,
+                            false, fmt, e->st, s.stage);
+        free_rows.pop_back();
+        const double tp = now_ms();
+        prefill(e, m, fmt, L.row, r.prompt_ids, 0, r.prompt_len, L.sb);
+        MSW_CUDA(cudaMemcpyAsync(s.stage, s.next, sizeof(int), cudaMemcpyDeviceToHost, e->st));
+        if (res[next_req].logits) copy_logits_row(e, res[next_req].logits, 0);
+        MSW_CUDA(cudaStreamSynchronize(e->st));
+        prefill_time += now_ms() - tp;
+        L.last_tok = s.stage[0];
+        res[next_req].out_ids[0] = L.last_tok;
+        L.generated = 1;
+        res[next_req].prefill_ms = now_ms() - tp;
+        if (L.generated >= r.max_new_tokens) {
+          release_sequence(m, L.sb);
+          free_rows.push_back(L.row);
+          res[next_req].n_out = L.generated;
+          res[next_req].total_ms = now_ms() - L.t_admit;
+        } else {
+          live.push_back(std::move(L));
+        }
+        ++next_req;
+      }
+      if (live.empty()) continue;
+      // one decode step for every live sequence
+      const int T = int(live.size());
+      for (int i = 0; i < T; ++i) {
+        const Live& L = live[i];
+        const int p = reqs[L.req].prompt_len + L.generated - 1;
+        s.stage[i] = L.last_tok;
+        s.stage[T + i] = p;
+        s.stage[2 * T + i] = L.sb.blocks[p / kKvBlock] * kKvBlock + p % kKvBlock;
+        s.stage[3 * T + i] = L.row;
+      }
+      const double ts = now_ms();
+      MSW_CUDA(cudaMemcpyAsync(s.tok, s.stage, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+      MSW_CUDA(cudaMemcpyAsync(s.pos, s.stage + T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+      MSW_CUDA(cudaMemcpyAsync(s.slot, s.stage + 2 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+      MSW_CUDA(cudaMemcpyAsync(s.seq_of, s.stage + 3 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+      forward(e, m, fmt, T, T, true);
+      MSW_CUDA(cudaMemcpyAsync(s.stage + 4 * T, s.next, sizeof(int) * T, cudaMemcpyDeviceToHost, e->st));
+      for (int i = 0; i < T; ++i) {
+        msw_result& rr = res[live[i].req];
+        if (rr.logits) copy_logits_row(e, rr.logits + size_t(live[i].generated) * m.c.vocab, i);
+      }
+      MSW_CUDA(cudaStreamSynchronize(e->st));
+      decode_time += now_ms() - ts;
+      // retire / advance
+      std::vector<Live> still;
+      for (int i = 0; i < T; ++i) {
+        Live& L = live[i];
+        msw_result& rr = res[L.req];
+        L.last_tok = s.stage[4 * T + i];
+        rr.out_ids[L.generated++] = L.last_tok;
+        if (L.generated >= reqs[L.req].max_new_tokens) {
+          release_sequence(m, L.sb);
+          free_rows.push_back(L.row);
+          rr.n_out = L.generated;
+          rr.total_ms = now_ms() - L.t_admit;
+          rr.decode_ms = rr.total_ms - rr.prefill_ms;
+        } else {
+          still.push_back(std::move(L));
+        }
+      }
+      live.swap(still);
+    }
+  } catch (...) {
+    for (Live& L : live) release_sequence(m, L.sb);
+    throw;
+  }
+  (void)t0;
+  (void)decode_time;
+  (void)prefill_time;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ConfigErr& ex) {
+    g_last_error = ex.what();
+    return 2;
+  } catch (const DataErr& ex) {
+    g_last_error = ex.what();
+    return 3;
+  } catch (const std::exception& ex) {
+    g_last_error = ex.what();
+    return 1;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return 1;
+  }
+}
+
+}  // namespace
+}  // namespace msw
+
+using namespace msw;
+
+extern "C" {
+
+int msw_engine_create(int device, const msw_engine_cfg* cfg, msw_engine** out) {
+  return guarded([&] {
+    if (!cfg || !out) throw ConfigErr("NULL argument");
+    *out = nullptr;
+    if (cfg->kv_blocks < 4 || cfg->max_seq_len < 16 || cfg->max_batch < 1)
+      throw ConfigErr("kv_blocks/max_seq_len/max_batch too small");
+    if (cfg->has_draft && cfg->draft.vocab != cfg->target.vocab)
+      throw ConfigErr("draft and target must share the vocabulary");
+    MSW_CUDA(cudaSetDevice(device));
+    auto e = std::make_unique<msw_engine>();
+    e->device = device;
+    e->cfg = *cfg;
+    if (e->cfg.max_batch > kMaxLogitRows) e->cfg.max_batch = kMaxLogitRows;
+    MSW_CUDA(cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking));
+    for (auto& ev : e->ev) MSW_CUDA(cudaEventCreate(&ev));
+    std::vector<int> pred;
+    std::vector<uint8_t> agree;
+    build_successor(e->cfg, cfg->target.vocab, pred, agree);
+    build_model(e->target, cfg->target, false, e->cfg, pred, agree, e->st);
+    if (cfg->has_draft) build_model(e->draft, cfg->draft, true, e->cfg, pred, agree, e->st);
+    alloc_scratch(e.get());
+    MSW_CUDA(cudaStreamSynchronize(e->st));
+    *out = e.release();
+  });
+}
+
+int msw_engine_run(msw_engine* e, const msw_request* req, msw_result* res) {
+  return guarded([&] {
+    if (!e || !req || !res || !res->out_ids) throw ConfigErr("NULL argument");
+    MSW_CUDA(cudaSetDevice(e->device));
+    res->n_out = 0;
+    res->spec_rounds = res->spec_proposed = res->spec_accepted = 0;
+    res->prefix_hit_tokens = 0;
+    const long long before = e->launches;
+    if (req->mode == MSW_MODE_SPECULATIVE) {
+      run_spec(e, *req, *res);
+    } else if (req->mode == MSW_MODE_INT8_CONT_BATCHING) {
+      run_cb(e, req, 1, res);
+    } else {
+      run_single(e, *req, *res);
+    }
+    res->kernel_launches = int(e->launches - before);
+  });
+}
+
+int msw_engine_run_batch(msw_engine* e, const msw_request* reqs, int32_t n, msw_result* res) {
+  return guarded([&] {
+    if (!e || !reqs || !res || n < 1) throw ConfigErr("bad arguments");
+    MSW_CUDA(cudaSetDevice(e->device));
+    for (int i = 0; i < n; ++i) {
+      if (!res[i].out_ids) throw ConfigErr("NULL out_ids");
+      res[i].n_out = 0;
+      res[i].spec_rounds = res[i].spec_proposed = res[i].spec_accepted = 0;
+      res[i].prefix_hit_tokens = 0;
+    }
+    const long long before = e->launches;
+    run_cb(e, reqs, n, res);
+    for (int i = 0; i < n; ++i) res[i].kernel_launches = int(e->launches - before);
+  });
+}
+
+void msw_engine_destroy(msw_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  cudaStreamSynchronize(e->st);
+  free_model(e->target);
+  free_model(e->draft);
+  for (void* p : e->owned) cudaFree(p);
+  if (e->sc.stage) cudaFreeHost(e->sc.stage);
+  for (auto& ev : e->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (e->st) cudaStreamDestroy(e->st);
+  delete e;
+}
+
+const char* msw_last_error(void) { return g_last_error.c_str(); }
+
+int msw_engine_weight_bytes(msw_engine* e, int32_t mode, int64_t* bytes) {
+  return guarded([&] {
+    if (!e || !bytes) throw ConfigErr("NULL argument");
+    const int fmt = fmt_of_mode(mode);
+    if (!e->target.fmt_on[fmt]) throw ConfigErr("mode not resident");
+    *bytes = int64_t(e->target.weight_bytes(fmt));
+  });
+}
+
+int msw_engine_reset_prefix_cache(msw_engine* e) {
+  return guarded([&] {
+    if (!e) throw ConfigErr("NULL argument");
+    e->target.pool.drop_cache();
+  });
+}
+
+int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n, int32_t k,
+               const float* x, int32_t t, float* y, void* stream) {
+  return guarded([&] {
+    LinearW W;
+    W.fmt = wtype;
+    W.n = n;
+    W.k = k;
+    W.w = w;
+    W.s = scales;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (t <= kGemvMaxTokens) {
+      launch_gemv(W, kProPlain, kEpiStore, x, t, nullptr, 1e-5f, y, st);
+    } else {
+      half* xh = dalloc<half>(size_t(t) * k);
+      int8_t* xq = dalloc<int8_t>(size_t(t) * k);
+      float* xs = dalloc<float>(t);
+      launch_prep_act(wtype, x, t, k, nullptr, 1e-5f, xh, xq, xs, st);
+      launch_gemm(W, kEpiStore, xh, xq, xs, t, y, st);
+      MSW_CUDA(cudaStreamSynchronize(st));
+      cudaFree(xh);
+      cudaFree(xq);
+      cudaFree(xs);
+    }
+  });
+}
+
+int msw_gemv_i8_acc(const int8_t* w, const int8_t* x, int32_t n, int32_t k, int32_t* acc,
+                    void* stream) {
+  return guarded([&] { launch_gemv_i8_acc(w, x, n, k, acc, static_cast<cudaStream_t>(stream)); });
+}
+
+int msw_fill_fp16(uint16_t* dst, int64_t rows, int64_t cols, uint64_t seed, uint64_t tensor_id,
+                  int32_t scale_log2, void* stream) {
+  return guarded([&] {
+    launch_fill_fp16(reinterpret_cast<half*>(dst), rows, cols, seed, tensor_id, scale_log2,
+                     static_cast<cudaStream_t>(stream));
+  });
+}
+
+int msw_quant_int8_rows(const uint16_t* w, int32_t n, int32_t k, int8_t* q, float* scales,
+                        void* stream) {
+  return guarded([&] {
+    launch_quant_int8(reinterpret_cast<const half*>(w), n, k, q, scales,
+                      static_cast<cudaStream_t>(stream));
+  });
+}
+
+int msw_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* packed, uint16_t* scales,
+                      void* stream) {
+  return guarded([&] {
+    launch_quant_w4(reinterpret_cast<const half*>(w), n, k, reinterpret_cast<uint32_t*>(packed),
+                    reinterpret_cast<half*>(scales), static_cast<cudaStream_t>(stream));
+  });
+}
+
+int msw_device_sync(void) {
+  return guarded([&] { MSW_CUDA(cudaDeviceSynchronize()); });
+}
+
+}  // extern "C"

@@ -1,0 +1,181 @@
+// T > 1 token linears (prefill, speculative verify, continuous-batching steps).
+//
+// prep_act: per-token RMSNorm + activation handling (fp16 rounding or per-token
+// int8 quantisation), identical to the GEMV prologue contract.
+// gemm_tiled: portable CUDA-core tile kernel, used for shapes the tcgen05
+// kernel (gemm_tc.cu) does not take and as its correctness fallback-free
+// reference on device; W8A8 accumulates in int32 exactly.
+#include "kernels.cuh"
+
+namespace msw {
+namespace {
+
+constexpr int kPrepThreads = 256;
+
+__global__ void __launch_bounds__(kPrepThreads)
+    prep_act_kernel(int fmt, const float* __restrict__ x, int K, const half* __restrict__ gamma,
+                    float eps, half* __restrict__ xh, int8_t* __restrict__ xq,
+                    float* __restrict__ xscale) {
+  __shared__ float red[32];
+  const size_t t = blockIdx.x;
+  const float* xr = x + t * K;
+  float r = 1.0f;
+  if (gamma != nullptr) {
+    float ss = 0.0f;
+    for (int i = threadIdx.x; i < K; i += kPrepThreads) ss = fmaf(xr[i], xr[i], ss);
+    ss = block_sum(ss, red);
+    r = 1.0f / sqrtf(ss / float(K) + eps);
+  }
+  auto act = [&](int i) -> float {
+    return gamma != nullptr ? (xr[i] * r) * __half2float(gamma[i]) : xr[i];
+  };
+  if (fmt == kINT8) {
+    float amax = 0.0f;
+    for (int i = threadIdx.x; i < K; i += kPrepThreads) amax = fmaxf(amax, fabsf(act(i)));
+    amax = block_max(amax, red);
+    const float s = amax / 127.0f;
+    for (int i = threadIdx.x; i < K; i += kPrepThreads) {
+      const float v = amax > 0.0f ? rintf(act(i) / s) : 0.0f;
+      xq[t * K + i] = static_cast<int8_t>(fminf(fmaxf(v, -127.0f), 127.0f));
+    }
+    if (threadIdx.x == 0) xscale[t] = s;
+  } else {
+    for (int i = threadIdx.x; i < K; i += kPrepThreads) xh[t * K + i] = __float2half_rn(act(i));
+  }
+}
+
+constexpr int BM = 64;  // tokens per tile
+constexpr int BN = 64;  // weight rows per tile
+constexpr int BK = 32;
+
+template <int FMT>
+__device__ __forceinline__ float dequant(const uint8_t* w, const void* ws, int n, int k, int K) {
+  if (FMT == kFP16) {
+    return __half2float(reinterpret_cast<const half*>(w)[size_t(n) * K + k]);
+  } else {
+    const uint32_t word = reinterpret_cast<const uint32_t*>(w)[size_t(n) * (K / 8) + k / 8];
+    const int idx = k & 7;
+    const int pos = (idx >> 1) + 4 * (idx & 1);
+    const int q = int((word >> (4 * pos)) & 0xF) - 8;
+    const half s = static_cast<const half*>(ws)[size_t(n) * (K / kW4Group) + k / kW4Group];
+    return __half2float(__hmul(__int2half_rn(q), s));
+  }
+}
+
+template <int FMT, int EPI>
+__global__ void __launch_bounds__(256)
+    gemm_tiled_kernel(const uint8_t* __restrict__ w, const void* __restrict__ ws, int N, int K,
+                      const half* __restrict__ xh, const int8_t* __restrict__ xq,
+                      const float* __restrict__ xscale, int T, float* __restrict__ y) {
+  using Acc = typename std::conditional<FMT == kINT8, int, float>::type;
+  __shared__ Acc Xs[BK][BM + 4];
+  __shared__ Acc Ws[BK][BN + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4x4 each
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  Acc acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    for (int e = threadIdx.x; e < BK * BM; e += 256) {
+      const int kk = e % BK, mm = e / BK;
+      const int m = m0 + mm, k = k0 + kk;
+      Acc v = 0;
+      if (m < T) {
+        if (FMT == kINT8) v = Acc(xq[size_t(m) * K + k]);
+        else v = Acc(__half2float(xh[size_t(m) * K + k]));
+      }
+      Xs[kk][mm] = v;
+    }
+    for (int e = threadIdx.x; e < BK * BN; e += 256) {
+      const int kk = e % BK, nn = e / BK;
+      const int n = n0 + nn, k = k0 + kk;
+      Acc v = 0;
+      if (n < N) {
+        if (FMT == kINT8) v = Acc(reinterpret_cast<const int8_t*>(w)[size_t(n) * K + k]);
+        else v = Acc(dequant<FMT>(w, ws, n, k, K));
+      }
+      Ws[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < BK; ++kk) {
+      Acc a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Xs[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Ws[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= T) continue;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (FMT == kINT8) {
+        v[j] = n < N ? (float(acc[i][j]) * xscale[m]) * static_cast<const float*>(ws)[n] : 0.0f;
+      } else {
+        v[j] = float(acc[i][j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j += 2) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      if (EPI == kEpiStore) {
+        y[size_t(m) * N + n] = v[j];
+        y[size_t(m) * N + n + 1] = v[j + 1];
+      } else if (EPI == kEpiResid) {
+        y[size_t(m) * N + n] += v[j];
+        y[size_t(m) * N + n + 1] += v[j + 1];
+      } else {
+        y[size_t(m) * (N / 2) + n / 2] = silu(v[j]) * v[j + 1];
+      }
+    }
+  }
+}
+
+template <int FMT>
+void gemm_fmt(const LinearW& W, int epi, const half* xh, const int8_t* xq, const float* xscale,
+              int T, float* y, cudaStream_t st) {
+  const dim3 grid(ceil_div(W.n, BN), ceil_div(T, BM));
+  const uint8_t* w = static_cast<const uint8_t*>(W.w);
+  if (epi == kEpiStore)
+    gemm_tiled_kernel<FMT, kEpiStore><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
+  else if (epi == kEpiResid)
+    gemm_tiled_kernel<FMT, kEpiResid><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
+  else
+    gemm_tiled_kernel<FMT, kEpiSwiglu><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
+  MSW_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void launch_prep_act(int fmt, const float* x, int T, int K, const half* gamma, float eps, half* xh,
+                     int8_t* xq, float* xscale, cudaStream_t st) {
+  prep_act_kernel<<<T, kPrepThreads, 0, st>>>(fmt, x, K, gamma, eps, xh, xq, xscale);
+  MSW_LAUNCH_CHECK();
+}
+
+void launch_gemm(const LinearW& W, int epi, const half* xh, const int8_t* xq, const float* xscale,
+                 int T, float* y, cudaStream_t st) {
+  if (W.k % BK != 0 || W.n % 2 != 0) throw ConfigErr("gemm: bad shape");
+  switch (W.fmt) {
+    case kFP16: return gemm_fmt<kFP16>(W, epi, xh, xq, xscale, T, y, st);
+    case kINT8: return gemm_fmt<kINT8>(W, epi, xh, xq, xscale, T, y, st);
+    case kW4: return gemm_fmt<kW4>(W, epi, xh, xq, xscale, T, y, st);
+    default: throw ConfigErr("gemm: bad format");
+  }
+}
+
+}  // namespace msw

@@ -1,0 +1,88 @@
+// Launcher declarations for the sm_100a mode-executor kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace msw {
+
+enum WFmt { kFP16 = 0, kINT8 = 1, kW4 = 2 };
+
+// A linear layer resident in HBM. y[n] = sum_k W[n,k] x[k].
+//   kFP16: w = half [n, k] row-major
+//   kINT8: w = int8 [n, k] row-major, s = float [n] per-row scale
+//   kW4  : w = uint32 [n, k/8] (8 nibbles per word, interleaved so that one
+//          lop3 yields the fp16 pair (k, k+1)), s = half [n, k/128]
+struct LinearW {
+  int fmt = kFP16;
+  int n = 0, k = 0;
+  const void* w = nullptr;
+  const void* s = nullptr;
+  size_t bytes() const {
+    const size_t nk = size_t(n) * size_t(k);
+    if (fmt == kFP16) return nk * 2;
+    if (fmt == kINT8) return nk + size_t(n) * 4;
+    return nk / 2 + size_t(n) * (k / kW4Group) * 2;
+  }
+};
+
+// ---- init.cu: K16 generator, quantisers, successor lm_head ----------------
+void launch_fill_fp16(half* dst, int64_t rows, int64_t cols, uint64_t seed, uint64_t tid,
+                      int scale_log2, cudaStream_t st);
+void launch_fill_norm(half* dst, int64_t n, uint64_t seed, uint64_t tid, cudaStream_t st);
+void launch_quant_int8(const half* w, int n, int k, int8_t* q, float* s, cudaStream_t st);
+void launch_quant_w4(const half* w, int n, int k, uint32_t* packed, half* s, cudaStream_t st);
+void launch_unpack_w4(const uint32_t* packed, int n, int k, uint8_t* nibbles, cudaStream_t st);
+void launch_lm_head(const half* emb, const int* pred, const uint8_t* agree, int is_draft,
+                    int V, int H, half* out, cudaStream_t st);
+// out row 2i = a row i, out row 2i+1 = b row i (gate/up interleave for the SwiGLU epilogue)
+void launch_interleave_rows(const void* a, const void* b, int n, size_t row_bytes, void* out,
+                            cudaStream_t st);
+
+// ---- gemv.cu: batch-1 decode GEMV ----------------------------------------
+enum Prologue { kProPlain = 0, kProNorm = 1 };
+enum Epilogue { kEpiStore = 0, kEpiResid = 1, kEpiSwiglu = 2 };
+// x: fp32 [k]. kProNorm: x <- x * rsqrt(mean(x^2)+eps) * gamma before the
+// format's activation handling (fp16 rounding, or int8 absmax quantisation).
+// kEpiStore: y[n] = v; kEpiResid: y[n] += v; kEpiSwiglu: y[i] = silu(v[2i]) * v[2i+1].
+// x is fp32 [T, k], 1 <= T <= kGemvMaxTokens; y rows are per token.
+constexpr int kGemvMaxTokens = 6;
+void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
+                 float eps, float* y, cudaStream_t st);
+void launch_gemv_i8_acc(const int8_t* w, const int8_t* x, int n, int k, int* acc, cudaStream_t st);
+
+// ---- gemm.cu: T > 1 tokens (prefill / verify / continuous batching) -----------
+// prep: per token row, optional RMSNorm, then fp16 rounding (xh) or int8
+// quantisation (xq + per-token scale).
+void launch_prep_act(int fmt, const float* x, int T, int K, const half* gamma, float eps,
+                     half* xh, int8_t* xq, float* xscale, cudaStream_t st);
+void launch_gemm(const LinearW& W, int epi, const half* xh, const int8_t* xq, const float* xscale,
+                 int T, float* y, cudaStream_t st);
+
+// ---- attention.cu -----------------------------------------------------------
+struct AttnShape {
+  int n_heads, n_kv_heads, head_dim;
+  int max_blocks_per_seq;  // block-table row stride
+};
+// qkv fp32 [T, (Hq+2Hk)*D] -> RoPE on q,k -> q fp16 [T,Hq,D]; k,v fp16 into the
+// paged cache at slot[t] (= block*16 + offset) of this layer.
+void launch_rope_append(const float* qkv, int T, const int* pos, const int* slot,
+                        const float* inv_freq, const AttnShape& a, half* q_out, half* kc, half* vc,
+                        cudaStream_t st);
+// o fp32 [T, Hq, D]: token t (sequence seq_of[t], position pos[t]) attends to
+// positions [0, pos[t]] of its sequence through block_table[seq_of[t]].
+void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
+                      const int* block_table, const half* kc, const half* vc, const AttnShape& a,
+                      int nsplit, float* part_o, float* part_ml, float* o, cudaStream_t st);
+
+// ---- misc.cu ------------------------------------------------------------------
+void launch_embed(const half* emb, const int* tok, int T, int H, float* h, cudaStream_t st);
+// out[t] = argmax_v logits[t, v] (lowest index on ties)
+void launch_argmax(const float* logits, int T, int V, int* out, cudaStream_t st);
+void launch_gather_rows(const float* src, const int* rows, int n, int width, float* dst,
+                        cudaStream_t st);
+// batch-1 decode bookkeeping for graph replay: tok = history[step] = next[0],
+// step += 1, pos += 1, slot from block-table row 0
+void launch_advance(const int* next, int* tok, int* pos, int* slot, int* step, int* history,
+                    const int* block_table, cudaStream_t st);
+
+}  // namespace msw

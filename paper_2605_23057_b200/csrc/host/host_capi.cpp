@@ -1,0 +1,202 @@
+// C ABI over the host controller (include/msw_host.h).
+#include <chrono>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "modeswitch/classifier.hpp"
+#include "modeswitch/routing.hpp"
+#include "modeswitch/trace_io.hpp"
+#include "modeswitch/workload.hpp"
+#include "msw_host.h"
+
+namespace ms = modeswitch;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& body) {
+  try {
+    body();
+    return MSW_OK;
+  } catch (const ms::ConfigError& e) {
+    g_err = e.what();
+    return MSW_ERR_CONFIG;
+  } catch (const ms::DataError& e) {
+    g_err = e.what();
+    return MSW_ERR_DATA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MSW_ERR_OTHER;
+  } catch (...) {
+    g_err = "unknown error";
+    return MSW_ERR_OTHER;
+  }
+}
+
+ms::RequestDescriptor to_cpp(const msw_descriptor& d) {
+  ms::RequestDescriptor r;
+  if (d.request_id == nullptr) throw ms::DataError("request_id is NULL");
+  r.request_id = d.request_id;
+  r.prompt_tokens = d.prompt_tokens;
+  r.expected_output_tokens = d.expected_output_tokens;
+  r.shared_prefix = d.shared_prefix != 0;
+  r.memory_pressure = d.memory_pressure != 0;
+  r.batch_pressure = d.batch_pressure;
+  if (d.workload_tag >= 0) {
+    if (d.workload_tag >= ms::kFamilyCount)
+      throw ms::DataError("workload_tag out of range");
+    r.workload_tag = static_cast<ms::WorkloadFamily>(d.workload_tag);
+  } else if (d.workload_tag != -1) {
+    throw ms::DataError("workload_tag out of range");
+  }
+  return r;
+}
+
+ms::ClassifierConfig to_cpp(const msw_classifier_cfg* c) {
+  ms::ClassifierConfig cfg;
+  if (c) {
+    cfg.long_prompt_threshold = c->long_prompt_threshold;
+    cfg.long_output_threshold = c->long_output_threshold;
+    cfg.decode_heavy_ratio = c->decode_heavy_ratio;
+    cfg.batch_threshold = c->batch_threshold;
+  }
+  ms::validate(cfg);
+  return cfg;
+}
+
+void fill(const ms::RequestDescriptor& r, const ms::ClassifierConfig& cfg,
+          const ms::RoutingDecision& d, msw_route_out* out) {
+  out->mode = static_cast<int32_t>(d.mode);
+  out->reason = static_cast<int32_t>(d.reason);
+  out->workload_class =
+      static_cast<int32_t>(ms::classify(ms::extract_features(r), cfg));
+  out->family = static_cast<int32_t>(ms::resolve_family(r, cfg));
+  out->overhead_ms = d.overhead_ms;
+}
+
+std::vector<ms::RequestDescriptor> parse_ndjson(const char* text) {
+  if (text == nullptr) throw ms::DataError("trace text is NULL");
+  std::vector<ms::RequestDescriptor> out;
+  std::istringstream in(text);
+  std::string line;
+  for (size_t lineno = 1; std::getline(in, line); ++lineno) {
+    if (line.empty()) continue;
+    try {
+      out.push_back(ms::parse_trace_line(line));
+    } catch (const ms::DataError& e) {
+      throw ms::DataError("line " + std::to_string(lineno) + ": " + e.what());
+    }
+  }
+  return out;
+}
+
+void copy_out(const std::string& s, char* buf, size_t cap, size_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (buf == nullptr || cap < s.size() + 1)
+    throw ms::Error("output buffer too small");
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+int msw_route_rule(const msw_descriptor* d, const msw_classifier_cfg* c,
+                   msw_route_out* out) {
+  return guarded([&] {
+    if (!d || !out) throw ms::DataError("NULL argument");
+    const ms::RequestDescriptor r = to_cpp(*d);
+    ms::validate(r);
+    const ms::ClassifierConfig cfg = to_cpp(c);
+    const ms::RulePolicy policy(cfg);
+    fill(r, cfg, policy.route(r), out);
+  });
+}
+
+int msw_route_ndjson(const char* ndjson, const msw_classifier_cfg* c,
+                     int32_t n_max, msw_route_out* out, int32_t* n_out) {
+  return guarded([&] {
+    const auto trace = parse_ndjson(ndjson);
+    if (n_out) *n_out = static_cast<int32_t>(trace.size());
+    if (static_cast<int64_t>(trace.size()) > n_max)
+      throw ms::Error("output array too small");
+    const ms::ClassifierConfig cfg = to_cpp(c);
+    const ms::RulePolicy policy(cfg);
+    for (size_t i = 0; i < trace.size(); ++i)
+      fill(trace[i], cfg, policy.route(trace[i]), &out[i]);
+  });
+}
+
+int msw_trace_parse_line(const char* line, msw_descriptor* out, char* id_buf,
+                         size_t id_cap) {
+  return guarded([&] {
+    if (!line || !out) throw ms::DataError("NULL argument");
+    const ms::RequestDescriptor r = ms::parse_trace_line(line);
+    copy_out(r.request_id, id_buf, id_cap, nullptr);
+    out->request_id = id_buf;
+    out->prompt_tokens = r.prompt_tokens;
+    out->expected_output_tokens = r.expected_output_tokens;
+    out->shared_prefix = r.shared_prefix;
+    out->memory_pressure = r.memory_pressure;
+    out->batch_pressure = r.batch_pressure;
+    out->workload_tag = r.workload_tag ? static_cast<int32_t>(*r.workload_tag) : -1;
+  });
+}
+
+int msw_trace_format_line(const msw_descriptor* d, char* buf, size_t cap,
+                          size_t* needed) {
+  return guarded([&] {
+    if (!d) throw ms::DataError("NULL argument");
+    copy_out(ms::format_trace_line(to_cpp(*d)), buf, cap, needed);
+  });
+}
+
+int msw_trace_generate(const int32_t counts[11], double jitter, uint64_t seed,
+                       int32_t batch_pressure, double batched_fraction,
+                       char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    ms::TraceSpec spec;
+    for (int i = 0; i < ms::kFamilyCount; ++i)
+      if (counts[i] != 0) spec.counts[static_cast<ms::WorkloadFamily>(i)] = counts[i];
+    spec.jitter = jitter;
+    spec.seed = seed;
+    spec.batch_pressure = batch_pressure;
+    spec.batched_fraction = batched_fraction;
+    std::string text;
+    for (const auto& r : ms::generate_trace(spec))
+      text += ms::format_trace_line(r) + "\n";
+    copy_out(text, buf, cap, needed);
+  });
+}
+
+int msw_route_cost(const char* ndjson, int32_t passes, double* mean_stamp_ms,
+                   double* wall_ms_per_decision) {
+  return guarded([&] {
+    const auto trace = parse_ndjson(ndjson);
+    if (trace.empty() || passes < 1) throw ms::ConfigError("nothing to route");
+    const ms::RulePolicy policy;
+    double stamped = 0.0;
+    long n = 0;
+    volatile int sink = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int p = 0; p < passes; ++p)
+      for (const auto& r : trace) {
+        const auto d = policy.route(r);
+        stamped += d.overhead_ms;
+        sink = sink + static_cast<int>(d.mode);
+        ++n;
+      }
+    const double wall = std::chrono::duration<double, std::milli>(
+                            std::chrono::steady_clock::now() - t0)
+                            .count();
+    if (mean_stamp_ms) *mean_stamp_ms = stamped / double(n);
+    if (wall_ms_per_decision) *wall_ms_per_decision = wall / double(n);
+  });
+}
+
+const char* msw_host_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+"""Python handle over the C-ABI mode executor (include/msw_engine.h).
+
+Thin: every call goes straight to libmsw_engine.so; buffers are host numpy
+arrays (the engine does the host<->device copies). No compute happens here
+and there is no fallback if the library or the GPU is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import Request, Result, check_engine, engine_lib
+from .configs import engine_cfg
+
+
+@dataclass
+class RunResult:
+    tokens: np.ndarray
+    logits: np.ndarray | None
+    prefill_ms: float
+    decode_ms: float
+    total_ms: float
+    spec_rounds: int = 0
+    spec_proposed: int = 0
+    spec_accepted: int = 0
+    prefix_hit_tokens: int = 0
+    kernel_launches: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+def _i32p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _f32p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+class Engine:
+    """One per GPU. `cfg` is an EngineCfg (see configs.engine_cfg)."""
+
+    def __init__(self, cfg=None, device: int = 0, **kw):
+        self.cfg = cfg if cfg is not None else engine_cfg(**kw)
+        self.vocab = self.cfg.target.vocab
+        h = C.c_void_p()
+        check_engine(engine_lib().msw_engine_create(device, C.byref(self.cfg), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            engine_lib().msw_engine_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _mk(self, mode, prompt, n_new, want_logits, seq=0):
+        p = np.ascontiguousarray(prompt, dtype=np.int32)
+        out = np.zeros(n_new, dtype=np.int32)
+        lg = np.zeros((n_new, self.vocab), dtype=np.float32) if want_logits else None
+        req = Request(mode=mode, prompt_ids=_i32p(p), prompt_len=len(p), max_new_tokens=n_new,
+                      prefix_group=-1, prefix_len=0, seq=seq)
+        res = Result(out_ids=_i32p(out), logits=_f32p(lg) if lg is not None else None)
+        return p, out, lg, req, res
+
+    @staticmethod
+    def _wrap(out, lg, res) -> RunResult:
+        return RunResult(tokens=out, logits=lg, prefill_ms=res.prefill_ms, decode_ms=res.decode_ms,
+                         total_ms=res.total_ms, spec_rounds=res.spec_rounds,
+                         spec_proposed=res.spec_proposed, spec_accepted=res.spec_accepted,
+                         prefix_hit_tokens=res.prefix_hit_tokens,
+                         kernel_launches=res.kernel_launches)
+
+    def run(self, mode: int, prompt, n_new: int, want_logits: bool = False, seq: int = 0) -> RunResult:
+        p, out, lg, req, res = self._mk(mode, prompt, n_new, want_logits, seq)
+        check_engine(engine_lib().msw_engine_run(self.h, C.byref(req), C.byref(res)))
+        return self._wrap(out, lg, res)
+
+    def run_batch(self, mode: int, prompts, n_new, want_logits: bool = False) -> list[RunResult]:
+        n = len(prompts)
+        n_new = list(n_new) if hasattr(n_new, "__len__") else [n_new] * n
+        keep, reqs, ress = [], (Request * n)(), (Result * n)()
+        outs = []
+        for i, (pr, nn) in enumerate(zip(prompts, n_new)):
+            p, out, lg, req, res = self._mk(mode, pr, nn, want_logits, i)
+            keep.append(p)
+            reqs[i] = req
+            ress[i] = res
+            outs.append((out, lg))
+        check_engine(engine_lib().msw_engine_run_batch(self.h, reqs, n, ress))
+        return [self._wrap(o, l, ress[i]) for i, (o, l) in enumerate(outs)]
+
+    def weight_bytes(self, mode: int) -> int:
+        b = C.c_int64()
+        check_engine(engine_lib().msw_engine_weight_bytes(self.h, mode, C.byref(b)))
+        return b.value
+
+    def reset_prefix_cache(self):
+        check_engine(engine_lib().msw_engine_reset_prefix_cache(self.h))
+
+
+__all__ = ["Engine", "RunResult", "_capi"]

@@ -1,0 +1,122 @@
+"""End-to-end mode parity on the B200 through the C ABI (msw_engine_run /
+msw_engine_run_batch) against the CPU oracle on the same K16 random-init
+weights and synthetic prompts.
+
+Bars:
+  * greedy tokens bit-exact in every mode (FP16, INT8, GPTQ4, spec, GPTQ+PC, INT8+CB);
+  * speculative decoding: tokens == target greedy, and round/proposal/accept
+    counts equal the oracle's (they are a deterministic function of tokens);
+  * logits: max |gpu - oracle| / std(oracle logits) < 2e-3 (FP16, INT8),
+    < 1e-2 (W4: fp16 partial sums) — per generated step.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_23057_b200 import (MODE_FP16, MODE_GPTQ4, MODE_GPTQ_PC, MODE_INT8, MODE_INT8_CB,
+                                   MODE_SPEC, engine_cfg, model_cfg)
+from paper_2605_23057_b200._capi import MswError
+from paper_2605_23057_b200.engine import Engine
+
+pytestmark = pytest.mark.gpu
+
+TOL = {MODE_FP16: 2e-3, MODE_INT8: 2e-3, MODE_GPTQ4: 1e-2, MODE_GPTQ_PC: 1e-2, MODE_INT8_CB: 2e-3,
+       MODE_SPEC: 2e-3}
+ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_GPTQ_PC: 2, MODE_INT8_CB: 1}
+
+
+def prompt(seed, n, vocab):
+    return (np.random.default_rng(seed).integers(0, vocab, size=n)).astype(np.int32)
+
+
+@pytest.fixture(scope="module", params=["tiny", "tiny128"])
+def pair(request, cuda_ok):
+    shape = request.param
+    cfg = engine_cfg(target=shape, draft="tiny_draft", seed=5, kv_blocks=512, max_seq_len=1024)
+    eng = Engine(cfg)
+    orc = O.OracleModel(model_cfg(shape), seed=5, max_ctx=1024)
+    drf = O.OracleModel(model_cfg("tiny_draft"), seed=5, is_draft=True, max_ctx=1024)
+    yield shape, eng, orc, drf
+    eng.close()
+
+
+def _check_logits(gpu, ref, tol):
+    err = np.abs(gpu - ref).max(axis=1) / ref.std(axis=1)
+    assert err.max() < tol, f"logit error {err.max():.3g} >= {tol}"
+
+
+@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4])
+@pytest.mark.parametrize("plen,n_new", [(1, 4), (37, 24), (130, 9)])
+def test_batch1_modes_match_oracle(pair, mode, plen, n_new):
+    _, eng, orc, _ = pair
+    p = prompt(plen * 31 + mode, plen, eng.vocab)
+    r = eng.run(mode, p, n_new, want_logits=True)
+    toks, lg = orc.generate(ORACLE_MODE[mode], p, n_new, want_logits=True)
+    assert np.array_equal(r.tokens, toks)
+    _check_logits(r.logits, lg, TOL[mode])
+
+
+@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4])
+def test_graph_replay_equals_oracle_tokens(pair, mode):
+    _, eng, orc, _ = pair
+    p = prompt(99 + mode, 50, eng.vocab)
+    r = eng.run(mode, p, 40)  # no logits requested -> CUDA-graph decode loop
+    toks, _ = orc.generate(ORACLE_MODE[mode], p, 40)
+    assert np.array_equal(r.tokens, toks)
+    assert r.kernel_launches > 0
+
+
+def test_speculative_matches_target_greedy(pair):
+    _, eng, orc, drf = pair
+    p = prompt(7, 45, eng.vocab)
+    r = eng.run(MODE_SPEC, p, 60, want_logits=True)
+    toks, lg, st = O.spec_generate(orc, drf, 4, p, 60, want_logits=True)
+    assert np.array_equal(r.tokens, toks)
+    assert (r.spec_rounds, r.spec_proposed, r.spec_accepted) == (st["rounds"], st["proposed"], st["accepted"])
+    assert 0 < r.spec_accepted < r.spec_proposed
+    _check_logits(r.logits, lg, TOL[MODE_SPEC])
+    greedy, _ = orc.generate(0, p, 60)
+    assert np.array_equal(r.tokens, greedy)
+
+
+def test_prefix_caching_reuses_blocks_and_keeps_tokens(pair):
+    _, eng, orc, _ = pair
+    eng.reset_prefix_cache()
+    shared = prompt(1234, 96, eng.vocab)
+    outs = []
+    for i in range(3):
+        tail = prompt(2000 + i, 20 + i, eng.vocab)
+        p = np.concatenate([shared, tail])
+        r = eng.run(MODE_GPTQ_PC, p, 12, want_logits=True)
+        toks, lg = orc.generate(2, p, 12, want_logits=True)
+        assert np.array_equal(r.tokens, toks)
+        _check_logits(r.logits, lg, TOL[MODE_GPTQ_PC])
+        outs.append(r.prefix_hit_tokens)
+    assert outs[0] == 0
+    assert outs[1] == 96 and outs[2] == 96  # 6 full shared blocks reused
+
+
+def test_continuous_batching_ragged_cohort(pair):
+    _, eng, orc, _ = pair
+    rng = np.random.default_rng(3)
+    plens = [int(x) for x in rng.integers(5, 90, size=11)]
+    nnew = [int(x) for x in rng.integers(1, 30, size=11)]
+    prompts = [prompt(500 + i, plens[i], eng.vocab) for i in range(11)]
+    res = eng.run_batch(MODE_INT8_CB, prompts, nnew, want_logits=True)
+    for i, r in enumerate(res):
+        toks, lg = orc.generate(1, prompts[i], nnew[i], want_logits=True)
+        assert np.array_equal(r.tokens, toks), i
+        _check_logits(r.logits, lg, TOL[MODE_INT8_CB])
+
+
+def test_error_codes(pair):
+    _, eng, _, _ = pair
+    with pytest.raises(MswError) as e:
+        eng.run(MODE_FP16, np.array([eng.vocab + 5], dtype=np.int32), 2)
+    assert e.value.code == 3
+    with pytest.raises(MswError) as e:
+        eng.run(3, np.array([1, 2, 3], dtype=np.int32), 2)  # AWQ4: not an engine mode
+    assert e.value.code == 2
+    with pytest.raises(MswError) as e:
+        eng.run(MODE_FP16, np.arange(10, dtype=np.int32), 5000)
+    assert e.value.code == 3

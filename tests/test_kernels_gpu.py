@@ -1,0 +1,116 @@
+"""Kernel-level parity on the B200: every sm_100a kernel called through the C
+ABI (device pointers from torch) against the CPU oracle on the same inputs.
+
+Bars: K16 init, W8 and W4 quantisers and the INT8 int32 accumulator are
+BIT-EXACT; FP16 / W4 / W8A8 linears within the stated relative tolerance
+(max |gpu - oracle| / max |oracle|):  FP16 2e-5, W8A8 2e-5 (int32 exact, the
+only fp ops are two scale multiplies), W4 2e-3 (fp16 partial sums of <= 4
+products by contract)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_23057_b200 import _capi
+from paper_2605_23057_b200._capi import check_engine, engine_lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _pack_w4_host(q):
+    """Reference packing of nibble-per-byte q [n,k] into the engine layout
+    (word j = k 8j..8j+7, nibble position p(i) = (i>>1) + 4*(i&1))."""
+    n, k = q.shape
+    qq = q.reshape(n, k // 8, 8).astype(np.uint32)
+    pos = np.array([(i >> 1) + 4 * (i & 1) for i in range(8)], dtype=np.uint32)
+    return (qq << (4 * pos)).sum(axis=2).astype(np.uint32)
+
+
+@pytest.mark.parametrize("rows,cols,tid,shift", [(64, 512, 17, 5), (3, 4096, 1 << 32, 6), (128, 384, 259, 0)])
+def test_fill_fp16_bit_exact(cuda_ok, rows, cols, tid, shift):
+    torch = _torch()
+    d = torch.empty((rows, cols), dtype=torch.int16, device="cuda")
+    check_engine(engine_lib().msw_fill_fp16(d.data_ptr(), rows, cols, 7, tid, shift, None))
+    torch.cuda.synchronize()
+    ref = O.fill_fp16(rows, cols, 7, tid, shift)
+    assert np.array_equal(d.cpu().numpy().view(np.uint16), ref)
+
+
+def test_quantisers_bit_exact(cuda_ok):
+    torch = _torch()
+    n, k = 96, 1024
+    w = O.fill_fp16(n, k, 3, 99, 6)
+    w[5, :] = 0  # all-zero row: scale 0, q = 0 / 8
+    dw = torch.from_numpy(w.view(np.int16)).cuda()
+    q8 = torch.empty((n, k), dtype=torch.int8, device="cuda")
+    s8 = torch.empty(n, dtype=torch.float32, device="cuda")
+    check_engine(engine_lib().msw_quant_int8_rows(dw.data_ptr(), n, k, q8.data_ptr(), s8.data_ptr(), None))
+    q4 = torch.empty((n, k // 8), dtype=torch.int32, device="cuda")
+    s4 = torch.empty((n, k // 128), dtype=torch.int16, device="cuda")
+    check_engine(engine_lib().msw_quant_w4_rows(dw.data_ptr(), n, k, q4.data_ptr(), s4.data_ptr(), None))
+    torch.cuda.synchronize()
+    rq8, rs8 = O.quant_int8_rows(w)
+    rq4, rs4 = O.quant_w4_rows(w)
+    assert np.array_equal(q8.cpu().numpy(), rq8)
+    assert np.array_equal(s8.cpu().numpy().view(np.uint32), rs8.view(np.uint32))
+    assert np.array_equal(q4.cpu().numpy().view(np.uint32), _pack_w4_host(rq4))
+    assert np.array_equal(s4.cpu().numpy().view(np.uint16), rs4)
+
+
+@pytest.mark.parametrize("n,k", [(256, 4096), (130, 14336), (8, 16)])
+def test_int8_accumulators_bit_exact(cuda_ok, n, k):
+    torch = _torch()
+    rng = np.random.default_rng(n + k)
+    w = rng.integers(-127, 128, size=(n, k), dtype=np.int8)
+    x = rng.integers(-127, 128, size=k, dtype=np.int8)
+    w[0, :] = 127
+    x[:] = np.where(np.arange(k) % 2 == 0, 127, x)  # near-extreme sums
+    acc = torch.empty(n, dtype=torch.int32, device="cuda")
+    check_engine(engine_lib().msw_gemv_i8_acc(torch.from_numpy(w).cuda().data_ptr(),
+                                              torch.from_numpy(x).cuda().data_ptr(), n, k,
+                                              acc.data_ptr(), None))
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy(), O.gemv_i8_acc(w, x))
+
+
+def _run_linear(fmt, w_dev, s_dev, n, k, x):
+    torch = _torch()
+    t = x.shape[0]
+    dx = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+    dy = torch.empty((t, n), dtype=torch.float32, device="cuda")
+    check_engine(engine_lib().msw_linear(fmt, w_dev.data_ptr(), s_dev.data_ptr() if s_dev is not None else None,
+                                         n, k, dx.data_ptr(), t, dy.data_ptr(), None))
+    torch.cuda.synchronize()
+    return dy.cpu().numpy()
+
+
+@pytest.mark.parametrize("t", [1, 2, 5, 6, 7, 40])
+@pytest.mark.parametrize("n,k", [(512, 4096), (2048, 512), (256, 14336)])
+def test_linear_formats_vs_oracle(cuda_ok, t, n, k):
+    torch = _torch()
+    rng = np.random.default_rng(t * 1000 + n)
+    w = O.fill_fp16(n, k, 11, 1234 + n, (int(np.ceil(np.log2(k))) + 1) // 2)
+    x = rng.standard_normal((t, k)).astype(np.float32)
+    x[:, 0] = 4.0  # a large activation, as after RMSNorm with outliers
+    # FP16
+    y = _run_linear(_capi.W_FP16, torch.from_numpy(w.view(np.int16)).cuda(), None, n, k, x)
+    ref = O.linear(_capi.W_FP16, w, None, x)
+    assert np.abs(y - ref).max() / np.abs(ref).max() < 2e-5
+    # W8A8
+    q8, s8 = O.quant_int8_rows(w)
+    y = _run_linear(_capi.W_INT8, torch.from_numpy(q8).cuda(), torch.from_numpy(s8).cuda(), n, k, x)
+    ref = O.linear(_capi.W_INT8, q8, s8, x)
+    assert np.abs(y - ref).max() / np.abs(ref).max() < 2e-5
+    # W4 g128
+    q4, s4 = O.quant_w4_rows(w)
+    packed = _pack_w4_host(q4)
+    y = _run_linear(_capi.W_W4, torch.from_numpy(packed.view(np.int32)).cuda(),
+                    torch.from_numpy(s4.view(np.int16)).cuda(), n, k, x)
+    ref = O.linear(_capi.W_W4, q4, s4, x)
+    assert np.abs(y - ref).max() / np.abs(ref).max() < 2e-3
