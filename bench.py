@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark driver (BASELINE.json config 2 by default).
+
+Workload "decode8b": Llama-3.1-8B-shape, K16 random-init weights, batch-1
+greedy decode of one synthetic request (prompt 128 -> 128 new tokens, the
+SyntheticSS nominal prompt) in each resident mode FP16, INT8 (W8A8) and
+GPTQ4 (W4 g128) on every GPU. One step = that request in all three modes,
+issued through the C ABI (msw_engine_run) with HOST prompt/token buffers.
+
+  value  = GPTQ4 decode tokens/s (device time: CUDA events on the engine's
+           stream around the graph-replayed decode loop), summed over ranks;
+  e2e    = GPTQ4 generated tokens / msw_engine_run wall time (H2D prompt,
+           prefill, decode, D2H tokens), summed over ranks;
+  per_mode / speedup_vs_fp16: every mode's decode tok/s and its mean
+           request-latency speedup over FP16 on the same request
+           (reference metric, domain.cpp:118-123);
+  roofline: the dominant kernel, the W4 GEMV (gate_up, 28672 x 4096),
+           timed with CUDA events on torch's stream over rotating weight
+           copies larger than L2, against MEASURED_PEAKS.json hbm_gbs;
+  cpu_baseline: the CPU oracle (port) on a bounded 8B W4 sample.
+
+Multi-GPU: one process per GPU (torchrun), each rank its own replica and its
+own requests (request sharding, no data-path collective); max over ranks.
+
+--impl reference: the reference has no inference path, so the
+reference arm times this repo's C oracle port of the same math on the host
+cores (kind "port"), plus the reference's own RulePolicy::route cost from
+oracle/_ref when present.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODES = [(0, "fp16"), (1, "int8"), (2, "gptq4")]
+PROMPT, NEW = 128, 128
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi style clock / throttle sampling during the timed region (NVML)."""
+
+    def __init__(self, device: int):
+        self.device, self.samples, self._stop = device, [], threading.Event()
+        self.max_mhz, self.reasons = None, set()
+
+    def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.hd = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.hd, nv.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception as ex:  # no NVML: record why
+            self.nv = None
+            self.reasons.add(f"nvml_unavailable:{type(ex).__name__}")
+        return self
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.hd, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.hd)
+                for bit, nm in names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=1)
+
+    def summary(self):
+        busy = [s for s in self.samples if s > 300] or self.samples
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples), "reasons": sorted(self.reasons)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def synth_prompt(seed: int, n: int, vocab: int):
+    import numpy as np
+    return np.random.default_rng(seed).integers(0, vocab, size=n).astype(np.int32)
+
+
+def time_dominant_kernel(iters: int = 50):
+    """W4 GEMV on the 8B gate_up shape (28672 x 4096), rotating over weight
+    copies larger than L2, CUDA events on torch's current stream."""
+    import numpy as np
+    import torch
+    from paper_2605_23057_b200._capi import W_W4, check_engine, engine_lib
+    n, k = 2 * 14336, 4096
+    copies = 5  # 5 x 60.6 MB > 126 MB L2
+    lib = engine_lib()
+    ws, ss = [], []
+    for i in range(copies):
+        w16 = torch.empty((n, k), dtype=torch.int16, device="cuda")
+        check_engine(lib.msw_fill_fp16(w16.data_ptr(), n, k, 99, 4000 + i, 6, None))
+        q = torch.empty((n, k // 8), dtype=torch.int32, device="cuda")
+        s = torch.empty((n, k // 128), dtype=torch.int16, device="cuda")
+        check_engine(lib.msw_quant_w4_rows(w16.data_ptr(), n, k, q.data_ptr(), s.data_ptr(), None))
+        ws.append(q)
+        ss.append(s)
+        del w16
+    x = torch.randn(k, device="cuda", dtype=torch.float32)
+    y = torch.empty(n, device="cuda", dtype=torch.float32)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    for i in range(5):
+        check_engine(lib.msw_linear(W_W4, ws[i % copies].data_ptr(), ss[i % copies].data_ptr(), n, k,
+                                    x.data_ptr(), 1, y.data_ptr(), sp))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(iters):
+        check_engine(lib.msw_linear(W_W4, ws[i % copies].data_ptr(), ss[i % copies].data_ptr(), n, k,
+                                    x.data_ptr(), 1, y.data_ptr(), sp))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    algo_bytes = n * k // 2 + n * (k // 128) * 2 + k * 4 + n * 4  # weights + scales + x + y
+    return {"kernel": "gemv_kernel<W4> gate_up 28672x4096", "ms": ms, "bytes": algo_bytes,
+            "gbs": algo_bytes / (ms * 1e-3) / 1e9}
+
+
+def cpu_baseline_8b(new_tokens: int = 3, prompt_len: int = 4):
+    """CPU oracle (C port, OpenMP over all host cores), 8B shape, W4 mode."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # checker / baseline only
+    from paper_2605_23057_b200.configs import model_cfg
+    t0 = time.perf_counter()
+    m = O.OracleModel(model_cfg("llama8b"), seed=0, modes_mask=1 << 2,
+                      max_ctx=prompt_len + new_tokens + 1)
+    t_init = time.perf_counter() - t0
+    p = synth_prompt(1, prompt_len, 128256)
+    t0 = time.perf_counter()
+    m.generate(2, p, new_tokens)
+    dt = time.perf_counter() - t0
+    m.close()
+    forwards = prompt_len + new_tokens - 1
+    return {"value": forwards / dt, "unit": "tokens/s", "cores": O.lib().orc_threads(),
+            "kind": "port",
+            "sample": f"8B-shape W4 g128 decode, {prompt_len}-token prompt + {new_tokens} new tokens "
+                      f"({forwards} full forwards, {dt:.1f} s; weight init {t_init:.1f} s excluded)"}
+
+
+def ref_route_cost():
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_route_bench")
+    trace = os.path.join(ROOT, "tests", "golden", "balanced_55_seed7.ndjson")
+    if not (os.path.exists(exe) and os.path.exists(trace)):
+        return None
+    try:
+        out = subprocess.run([exe, trace, "200"], capture_output=True, text=True, timeout=120)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return None
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    samples = []
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state worth excluding beyond weight init
+    cb = None
+    for _ in range(args.steps):
+        cb = cpu_baseline_8b(new_tokens=2, prompt_len=2)
+        samples.append(cb["value"])
+    v = statistics.mean(samples)
+    line = {"metric": "decode tokens/s per mode and routed mix (1/2/4/8 B200); mean latency vs FP16 mode",
+            "impl": "reference", "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "w4a16",
+            "data": "synthetic", "config": {"workload": "llama8b batch-1 decode (gptq4 mode)",
+                                            "model": "llama3.1-8b-shape random-init"},
+            "cpu_baseline": dict(cb, value=v),
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_route_cost": ref_route_cost(),
+            "note": "reference has no inference path (SPEC.md:20); arm = C oracle port of the same math"}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2605_23057_b200 import engine_cfg
+    from paper_2605_23057_b200.engine import Engine
+
+    cfg = engine_cfg(target="llama8b", draft=None, modes=[m for m, _ in MODES], seed=0,
+                     kv_blocks=256, max_batch=8, max_seq_len=PROMPT + NEW + 32, use_graphs=True)
+    t0 = time.perf_counter()
+    eng = Engine(cfg, device=local)
+    init_s = time.perf_counter() - t0
+    wbytes = {name: eng.weight_bytes(m) for m, name in MODES}
+    prompts = [synth_prompt(1000 * rank + i, PROMPT, 128256) for i in range(args.warmup + args.steps)]
+
+    def one_step(p):
+        out = {}
+        for m, name in MODES:
+            out[name] = eng.run(m, p, NEW)
+        return out
+
+    for i in range(args.warmup):
+        one_step(prompts[i])
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    agg = {name: {"dec_ms": 0.0, "tot_ms": 0.0, "pre_ms": 0.0, "tokens": 0, "launches": 0} for _, name in MODES}
+    speedups = {name: [] for _, name in MODES}
+    ref_tokens = None
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for i in range(args.steps):
+            res = one_step(prompts[args.warmup + i])
+            for _, name in MODES:
+                r = res[name]
+                a = agg[name]
+                a["dec_ms"] += r.decode_ms
+                a["tot_ms"] += r.total_ms
+                a["pre_ms"] += r.prefill_ms
+                a["tokens"] += len(r.tokens)
+                a["launches"] += r.kernel_launches
+                speedups[name].append(res["fp16"].total_ms / r.total_ms)
+            ref_tokens = res["gptq4"].tokens
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t_wall
+    # max over ranks of the device decode time / e2e time (gptq4 headline)
+    dec = torch.tensor([agg["gptq4"]["dec_ms"], agg["gptq4"]["tot_ms"], wall * 1000.0],
+                       dtype=torch.float64, device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(dec, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.barrier()
+    dec_ms_max, tot_ms_max, wall_max = dec.tolist()
+    if rank != 0:
+        eng.close()
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+    # decode tokens: first token comes from prefill; the decode loop makes NEW-1 tokens per request
+    dec_tokens = (NEW - 1) * args.steps
+    value = ws * dec_tokens / (dec_ms_max / 1000.0)
+    e2e = ws * NEW * args.steps / (tot_ms_max / 1000.0)
+    per_mode = {}
+    for _, name in MODES:
+        a = agg[name]
+        tps = (NEW - 1) * args.steps / (a["dec_ms"] / 1000.0)
+        per_mode[name] = {"decode_tok_s": tps, "ms_per_token": a["dec_ms"] / ((NEW - 1) * args.steps),
+                          "prefill_ms": a["pre_ms"] / args.steps, "request_ms": a["tot_ms"] / args.steps,
+                          "weight_bytes_per_token": wbytes[name],
+                          "hbm_frac_of_measured": wbytes[name] * tps / 1e9 / peaks()[0],
+                          "latency_speedup_vs_fp16": statistics.mean(speedups[name])}
+    kern = time_dominant_kernel()
+    peak, peak_kind = peaks()
+    launches = sum(agg[n]["launches"] for _, n in MODES)
+    cpu = cpu_baseline_8b() if not args.no_cpu_baseline else None
+    line = {
+        "metric": "decode tokens/s per mode and routed mix (1/2/4/8 B200); mean latency vs FP16 mode",
+        "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall_max * 1000.0 / args.steps if wall_max < 1e6 else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "w4a16",
+        "data": "synthetic (K16 random-init weights, hashed prompt ids)",
+        "config": {"workload": "llama8b batch-1 decode, prompt 128 -> 128 tokens; value = gptq4 mode",
+                   "model": "llama3.1-8b-shape", "modes": [n for _, n in MODES],
+                   "parallelism": f"request-sharded replicas x{ws}",
+                   "l2": "weights stream 4.65-15 GB per token >> 126 MB L2 (no flush needed)"},
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": PROMPT * 4 * len(MODES),
+                "d2h_bytes_per_step": NEW * 4 * len(MODES)},
+        "per_mode": per_mode,
+        "roofline": {"bound": "hbm", "achieved": kern["gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": kern["gbs"] / peak, "traffic": None, "kernel": kern["kernel"],
+                     "kernel_ms": kern["ms"], "bytes_per_launch": kern["bytes"],
+                     "peak_source": peak_kind,
+                     "decode_step_frac": per_mode["gptq4"]["hbm_frac_of_measured"]},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "engine_init_s": init_s,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    eng.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

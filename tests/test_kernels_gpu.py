@@ -72,9 +72,9 @@ def test_int8_accumulators_bit_exact(cuda_ok, n, k):
     w[0, :] = 127
     x[:] = np.where(np.arange(k) % 2 == 0, 127, x)  # near-extreme sums
     acc = torch.empty(n, dtype=torch.int32, device="cuda")
-    check_engine(engine_lib().msw_gemv_i8_acc(torch.from_numpy(w).cuda().data_ptr(),
-                                              torch.from_numpy(x).cuda().data_ptr(), n, k,
-                                              acc.data_ptr(), None))
+    dw, dx = torch.from_numpy(w).cuda(), torch.from_numpy(x).cuda()  # keep alive across the call
+    check_engine(engine_lib().msw_gemv_i8_acc(dw.data_ptr(), dx.data_ptr(), n, k, acc.data_ptr(),
+                                              None))
     torch.cuda.synchronize()
     assert np.array_equal(acc.cpu().numpy(), O.gemv_i8_acc(w, x))
 
