@@ -20,6 +20,8 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, const int* __r
                                    const int* __restrict__ slot, const float* __restrict__ inv_freq,
                                    int Hq, int Hk, int D, half* __restrict__ q_out,
                                    half* __restrict__ kc, half* __restrict__ vc) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   const int half_d = D / 2;
   const int width = (Hq + 2 * Hk) * D;
@@ -51,28 +53,80 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, const int* __r
 
 constexpr int kAttnWarps = 4;
 
-template <int D, int G>
+// Positions per split: at least kMinChunk so short contexts use few CTAs.
+constexpr int kMinChunk = 64;
+__device__ __forceinline__ int split_chunk(int ctx, int nsplit) {
+  const int c = (ctx + nsplit - 1) / nsplit;
+  return ((max(c, kMinChunk) + 31) / 32) * 32;
+}
+
+// FUSED (decode / continuous batching: every query token is the newest token
+// of its own sequence): RoPE of q and of the new k happens here from the
+// fp32 qkv row; the split-0 CTA appends k/v to the paged cache, and every CTA
+// uses the fresh k/v from shared memory for the query's own position instead
+// of reading the cache (no cross-CTA ordering needed).
+template <int D, int G, bool FUSED>
 __global__ void __launch_bounds__(kAttnWarps * 32)
-    attention_kernel(const half* __restrict__ q, const int* __restrict__ pos,
-                     const int* __restrict__ seq_of, const int* __restrict__ block_table,
-                     int max_blocks, const half* __restrict__ kc, const half* __restrict__ vc, int Hq,
-                     int Hk, int nsplit, float* __restrict__ part_o, float* __restrict__ part_ml,
+    attention_kernel(const half* __restrict__ q, const float* __restrict__ qkv,
+                     const float* __restrict__ inv_freq, const int* __restrict__ pos,
+                     const int* __restrict__ slot, const int* __restrict__ seq_of,
+                     const int* __restrict__ block_table, int max_blocks, half* __restrict__ kc,
+                     half* __restrict__ vc, int Hq, int Hk, int nsplit,
+                     float* __restrict__ part_o, float* __restrict__ part_ml,
                      float* __restrict__ o) {
   constexpr int DPL = D / 32;  // output dims per lane
   __shared__ float qs[G][D];
+  __shared__ float knew[D], vnew[D];
   __shared__ float wm[kAttnWarps][G], wl[kAttnWarps][G];
   __shared__ float wacc[kAttnWarps][G][D];
   const int t = blockIdx.x, hk = blockIdx.y, sp = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ctx = pos[t] + 1;
-  const int chunk = (ctx + nsplit - 1) / nsplit;
+  pdl_wait();
+  pdl_trigger();
+  const int p_self = pos[t];
+  const int ctx = p_self + 1;
+  const int chunk = split_chunk(ctx, nsplit);
   const int begin = sp * chunk;
+  if (begin >= ctx) return;  // inactive split (combine ignores it)
+  const bool single = chunk >= ctx;
   const int end = min(ctx, begin + chunk);
   const int* bt = block_table + size_t(seq_of[t]) * max_blocks;
   const float scale = 1.0f / sqrtf(float(D));
 
-  for (int i = threadIdx.x; i < G * D; i += blockDim.x)
-    qs[i / D][i % D] = __half2float(q[(size_t(t) * Hq + hk * G + i / D) * D + i % D]);
+  if (FUSED) {
+    const int width = (Hq + 2 * Hk) * D;
+    const float* row = qkv + size_t(t) * width;
+    const float pf = float(p_self);
+    for (int i = threadIdx.x; i < (G + 1) * (D / 2); i += blockDim.x) {
+      const int h = i / (D / 2), j = i % (D / 2);
+      const float* src = h < G ? row + size_t(hk * G + h) * D : row + size_t(Hq + hk) * D;
+      float sn, cs;
+      sincosf(pf * inv_freq[j], &sn, &cs);
+      const float x0 = src[j], x1 = src[j + D / 2];
+      const float y0 = __half2float(__float2half_rn(__fsub_rn(__fmul_rn(x0, cs), __fmul_rn(x1, sn))));
+      const float y1 = __half2float(__float2half_rn(__fadd_rn(__fmul_rn(x1, cs), __fmul_rn(x0, sn))));
+      if (h < G) {
+        qs[h][j] = y0;
+        qs[h][j + D / 2] = y1;
+      } else {
+        knew[j] = y0;
+        knew[j + D / 2] = y1;
+      }
+    }
+    for (int d = threadIdx.x; d < D; d += blockDim.x)
+      vnew[d] = __half2float(__float2half_rn(row[size_t(Hq + Hk + hk) * D + d]));
+    __syncthreads();
+    if (sp == 0) {
+      const size_t off = kv_off(slot[t], hk, Hk, D);
+      for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        kc[off + d] = __float2half_rn(knew[d]);
+        vc[off + d] = __float2half_rn(vnew[d]);
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < G * D; i += blockDim.x)
+      qs[i / D][i % D] = __half2float(q[(size_t(t) * Hq + hk * G + i / D) * D + i % D]);
+  }
   __syncthreads();
 
   float m[G], l[G], acc[G][DPL];
@@ -88,22 +142,29 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     const int p = base + lane;
     float s[G];
     if (p < end) {
-      const int slot = bt[p >> 4] * kKvBlock + (p & 15);
-      const uint4* kr = reinterpret_cast<const uint4*>(kc + kv_off(slot, hk, Hk, D));
       float dot[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) dot[g] = 0.0f;
+      if (FUSED && p == p_self) {
+        for (int d = 0; d < D; ++d) {
+#pragma unroll
+          for (int g = 0; g < G; ++g) dot[g] = fmaf(qs[g][d], knew[d], dot[g]);
+        }
+      } else {
+        const int sl = bt[p >> 4] * kKvBlock + (p & 15);
+        const uint4* kr = reinterpret_cast<const uint4*>(kc + kv_off(sl, hk, Hk, D));
 #pragma unroll 4
-      for (int c = 0; c < D / 8; ++c) {
-        const uint4 kv = kr[c];
-        const half2* kh = reinterpret_cast<const half2*>(&kv);
+        for (int c = 0; c < D / 8; ++c) {
+          const uint4 kv = kr[c];
+          const half2* kh = reinterpret_cast<const half2*>(&kv);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 kf = __half22float2(kh[e]);
+          for (int e = 0; e < 4; ++e) {
+            const float2 kf = __half22float2(kh[e]);
 #pragma unroll
-          for (int g = 0; g < G; ++g) {
-            dot[g] = fmaf(qs[g][c * 8 + 2 * e], kf.x, dot[g]);
-            dot[g] = fmaf(qs[g][c * 8 + 2 * e + 1], kf.y, dot[g]);
+            for (int g = 0; g < G; ++g) {
+              dot[g] = fmaf(qs[g][c * 8 + 2 * e], kf.x, dot[g]);
+              dot[g] = fmaf(qs[g][c * 8 + 2 * e + 1], kf.y, dot[g]);
+            }
           }
         }
       }
@@ -128,10 +189,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     const int n_here = min(32, end - base);
     for (int j = 0; j < n_here; ++j) {
       const int pj = base + j;
-      const int slot = bt[pj >> 4] * kKvBlock + (pj & 15);
-      const half* vr = vc + kv_off(slot, hk, Hk, D) + lane * DPL;
       float vf[DPL];
-      if (DPL == 4) {
+      if (FUSED && pj == p_self) {
+#pragma unroll
+        for (int d = 0; d < DPL; ++d) vf[d] = vnew[lane * DPL + d];
+      } else if (DPL == 4) {
+        const int sl = bt[pj >> 4] * kKvBlock + (pj & 15);
+        const half* vr = vc + kv_off(sl, hk, Hk, D) + lane * DPL;
         const uint2 raw = *reinterpret_cast<const uint2*>(vr);
         const float2 a = __half22float2(*reinterpret_cast<const half2*>(&raw.x));
         const float2 b = __half22float2(*reinterpret_cast<const half2*>(&raw.y));
@@ -140,6 +204,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
         vf[2 % DPL] = b.x;
         vf[3 % DPL] = b.y;
       } else {
+        const int sl = bt[pj >> 4] * kKvBlock + (pj & 15);
+        const half* vr = vc + kv_off(sl, hk, Hk, D) + lane * DPL;
 #pragma unroll
         for (int d = 0; d < DPL; ++d) vf[d] = __half2float(vr[d]);
       }
@@ -176,7 +242,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       }
     }
     const int hq = hk * G + g;
-    if (nsplit == 1) {
+    if (single) {
       o[(size_t(t) * Hq + hq) * D + d] = L > 0.0f ? A / L : 0.0f;
     } else {
       const size_t idx = (size_t(t) * Hq + hq) * nsplit + sp;
@@ -190,15 +256,21 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 }
 
 __global__ void attn_combine_kernel(const float* __restrict__ part_o,
-                                    const float* __restrict__ part_ml, int Hq, int D, int nsplit,
-                                    float* __restrict__ o) {
+                                    const float* __restrict__ part_ml, const int* __restrict__ pos,
+                                    int Hq, int D, int nsplit, float* __restrict__ o) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x, hq = blockIdx.y;
+  const int ctx = pos[t] + 1;
+  const int chunk = split_chunk(ctx, nsplit);
+  if (chunk >= ctx) return;  // single split wrote o directly
+  const int active = (ctx + chunk - 1) / chunk;
   const size_t base = (size_t(t) * Hq + hq) * nsplit;
   float M = -INFINITY;
-  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, part_ml[(base + s) * 2]);
+  for (int s = 0; s < active; ++s) M = fmaxf(M, part_ml[(base + s) * 2]);
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     float L = 0.0f, A = 0.0f;
-    for (int s = 0; s < nsplit; ++s) {
+    for (int s = 0; s < active; ++s) {
       const float ms = part_ml[(base + s) * 2];
       if (ms == -INFINITY) continue;
       const float f = expf(ms - M);
@@ -209,15 +281,16 @@ __global__ void attn_combine_kernel(const float* __restrict__ part_o,
   }
 }
 
-template <int D>
-void attn_d(int G, dim3 grid, const half* q, const int* pos, const int* seq_of, const int* bt,
-            int maxb, const half* kc, const half* vc, int Hq, int Hk, int nsplit, float* po,
-            float* pml, float* o, cudaStream_t st) {
-  const int thr = kAttnWarps * 32;
-#define MSW_ATT(GG)                                                                          \
-  case GG:                                                                                   \
-    attention_kernel<D, GG><<<grid, thr, 0, st>>>(q, pos, seq_of, bt, maxb, kc, vc, Hq, Hk, \
-                                                  nsplit, po, pml, o);                       \
+template <int D, bool FUSED>
+void attn_d(int G, dim3 grid, const half* q, const float* qkv, const float* inv_freq,
+            const int* pos, const int* slot, const int* seq_of, const int* bt, int maxb, half* kc,
+            half* vc, int Hq, int Hk, int nsplit, float* po, float* pml, float* o,
+            cudaStream_t st) {
+  const dim3 thr(kAttnWarps * 32);
+#define MSW_ATT(GG)                                                                              \
+  case GG:                                                                                       \
+    launch_pdl(attention_kernel<D, GG, FUSED>, grid, thr, 0, st, q, qkv, inv_freq, pos, slot,   \
+               seq_of, bt, maxb, kc, vc, Hq, Hk, nsplit, po, pml, o);                            \
     break;
   switch (G) {
     MSW_ATT(1)
@@ -229,35 +302,51 @@ void attn_d(int G, dim3 grid, const half* q, const int* pos, const int* seq_of, 
 #undef MSW_ATT
 }
 
+template <bool FUSED>
+void attention_any(const half* q, const float* qkv, const float* inv_freq, int T, const int* pos,
+                   const int* slot, const int* seq_of, const int* block_table, half* kc, half* vc,
+                   const AttnShape& a, int nsplit, float* part_o, float* part_ml, float* o,
+                   cudaStream_t st) {
+  const int G = a.n_heads / a.n_kv_heads;
+  const dim3 grid(T, a.n_kv_heads, nsplit);
+  if (a.head_dim == 128)
+    attn_d<128, FUSED>(G, grid, q, qkv, inv_freq, pos, slot, seq_of, block_table,
+                       a.max_blocks_per_seq, kc, vc, a.n_heads, a.n_kv_heads, nsplit, part_o,
+                       part_ml, o, st);
+  else if (a.head_dim == 64)
+    attn_d<64, FUSED>(G, grid, q, qkv, inv_freq, pos, slot, seq_of, block_table,
+                      a.max_blocks_per_seq, kc, vc, a.n_heads, a.n_kv_heads, nsplit, part_o,
+                      part_ml, o, st);
+  else
+    throw ConfigErr("attention: head_dim must be 64 or 128");
+  if (nsplit > 1)
+    launch_pdl(attn_combine_kernel, dim3(T, a.n_heads), dim3(128), 0, st, part_o, part_ml, pos,
+               a.n_heads, a.head_dim, nsplit, o);
+}
+
 }  // namespace
 
 void launch_rope_append(const float* qkv, int T, const int* pos, const int* slot,
                         const float* inv_freq, const AttnShape& a, half* q_out, half* kc, half* vc,
                         cudaStream_t st) {
-  rope_append_kernel<<<T, 256, 0, st>>>(qkv, pos, slot, inv_freq, a.n_heads, a.n_kv_heads,
-                                        a.head_dim, q_out, kc, vc);
-  MSW_LAUNCH_CHECK();
+  launch_pdl(rope_append_kernel, dim3(T), dim3(256), 0, st, qkv, pos, slot, inv_freq, a.n_heads,
+             a.n_kv_heads, a.head_dim, q_out, kc, vc);
 }
 
 void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
                       const int* block_table, const half* kc, const half* vc, const AttnShape& a,
                       int nsplit, float* part_o, float* part_ml, float* o, cudaStream_t st) {
-  const int G = a.n_heads / a.n_kv_heads;
-  const dim3 grid(T, a.n_kv_heads, nsplit);
-  if (a.head_dim == 128)
-    attn_d<128>(G, grid, q, pos, seq_of, block_table, a.max_blocks_per_seq, kc, vc, a.n_heads,
-                a.n_kv_heads, nsplit, part_o, part_ml, o, st);
-  else if (a.head_dim == 64)
-    attn_d<64>(G, grid, q, pos, seq_of, block_table, a.max_blocks_per_seq, kc, vc, a.n_heads,
-               a.n_kv_heads, nsplit, part_o, part_ml, o, st);
-  else
-    throw ConfigErr("attention: head_dim must be 64 or 128");
-  MSW_LAUNCH_CHECK();
-  if (nsplit > 1) {
-    attn_combine_kernel<<<dim3(T, a.n_heads), 128, 0, st>>>(part_o, part_ml, a.n_heads,
-                                                           a.head_dim, nsplit, o);
-    MSW_LAUNCH_CHECK();
-  }
+  attention_any<false>(q, nullptr, nullptr, T, pos, nullptr, seq_of, block_table,
+                       const_cast<half*>(kc), const_cast<half*>(vc), a, nsplit, part_o, part_ml, o,
+                       st);
+}
+
+void launch_attention_decode(const float* qkv, const float* inv_freq, int T, const int* pos,
+                             const int* slot, const int* seq_of, const int* block_table, half* kc,
+                             half* vc, const AttnShape& a, int nsplit, float* part_o,
+                             float* part_ml, float* o, cudaStream_t st) {
+  attention_any<true>(nullptr, qkv, inv_freq, T, pos, slot, seq_of, block_table, kc, vc, a, nsplit,
+                      part_o, part_ml, o, st);
 }
 
 }  // namespace msw

@@ -261,8 +261,11 @@ LinearW make_linear(Model& m, int fmt, const half* master, int n, int k, cudaStr
     uint32_t* q = model_alloc<uint32_t>(m, size_t(n) * k / 8);
     half* s = model_alloc<half>(m, size_t(n) * (k / kW4Group));
     launch_quant_w4(master, n, k, q, s, st);
+    uint32_t* qm = model_alloc<uint32_t>(m, size_t(n) * k / 8);
+    launch_repack_w4_mma(q, n, k, qm, st);
     L.w = q;
     L.s = s;
+    L.w_mma = qm;
   }
   return L;
 }
@@ -438,7 +441,8 @@ void alloc_scratch(msw_engine* e) {
 // Runs T tokens (inputs already in sc.tok/pos/slot/seq_of) through model m in
 // format fmt; logits + argmax for the n_logits rows listed in sc.logit_rows
 // (rows == nullptr means rows 0..n_logits-1 == all T rows).
-void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_identity) {
+void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_identity,
+             bool tokens_independent) {
   Scratch& s = e->sc;
   cudaStream_t st = e->st;
   const msw_model_cfg& c = m.c;
@@ -463,10 +467,16 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       launch_gemm(ly.qkv[fmt], kEpiStore, s.xh, s.xq, s.xscale, T, s.qkv, st);
       n += 2;
     }
-    launch_rope_append(s.qkv, T, s.pos, s.slot, m.inv_freq, m.ash, s.q16, kc, vc, st);
-    launch_attention(s.q16, T, s.pos, s.seq_of, m.block_table, kc, vc, m.ash, nsplit, s.part_o,
-                     s.part_ml, s.o, st);
-    n += nsplit > 1 ? 3 : 2;
+    if (tokens_independent) {  // decode / CB: RoPE + KV append fused into attention
+      launch_attention_decode(s.qkv, m.inv_freq, T, s.pos, s.slot, s.seq_of, m.block_table, kc,
+                              vc, m.ash, nsplit, s.part_o, s.part_ml, s.o, st);
+      n += nsplit > 1 ? 2 : 1;
+    } else {
+      launch_rope_append(s.qkv, T, s.pos, s.slot, m.inv_freq, m.ash, s.q16, kc, vc, st);
+      launch_attention(s.q16, T, s.pos, s.seq_of, m.block_table, kc, vc, m.ash, nsplit, s.part_o,
+                       s.part_ml, s.o, st);
+      n += nsplit > 1 ? 3 : 2;
+    }
     if (small) {
       launch_gemv(ly.o[fmt], kProPlain, kEpiResid, s.o, T, nullptr, eps, s.h, st);
       launch_gemv(ly.gu[fmt], kProNorm, kEpiSwiglu, s.h, T, ly.ffn_norm, eps, s.act, st);
@@ -593,7 +603,7 @@ void prefill(msw_engine* e, Model& m, int fmt, int row, const int32_t* prompt, i
       st_rows[0] = T - 1;
       MSW_CUDA(cudaMemcpyAsync(s.logit_rows, st_rows, sizeof(int), cudaMemcpyHostToDevice, e->st));
     }
-    forward(e, m, fmt, T, 1, /*rows_identity=*/T == 1);
+    forward(e, m, fmt, T, 1, /*rows_identity=*/T == 1, /*tokens_independent=*/T == 1);
     MSW_CUDA(cudaStreamSynchronize(e->st));  // staging is reused by the next chunk
   }
 }
@@ -602,7 +612,7 @@ void prefill(msw_engine* e, Model& m, int fmt, int row, const int32_t* prompt, i
 void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph) {
   Scratch& s = e->sc;
   auto body = [&]() {
-    forward(e, m, fmt, 1, 1, true);
+    forward(e, m, fmt, 1, 1, true, true);
     launch_advance(s.next, s.tok, s.pos, s.slot, s.step, s.hist, m.block_table, e->st);
     ++e->launches;
   };
@@ -771,7 +781,7 @@ void run_spec(msw_engine* e, const msw_request& r, msw_result& res) {
           s.stage[4 * T] = T - 1;
           MSW_CUDA(cudaMemcpyAsync(s.logit_rows, s.stage + 4 * T, sizeof(int), cudaMemcpyHostToDevice, e->st));
         }
-        forward(e, dr, kFP16, T, 1, T == 1);
+        forward(e, dr, kFP16, T, 1, T == 1, T == 1);
         MSW_CUDA(cudaStreamSynchronize(e->st));
         dlen = n - 1;
       }
@@ -798,7 +808,7 @@ void run_spec(msw_engine* e, const msw_request& r, msw_result& res) {
       MSW_CUDA(cudaMemcpyAsync(s.pos, s.stage + T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
       MSW_CUDA(cudaMemcpyAsync(s.slot, s.stage + 2 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
       MSW_CUDA(cudaMemcpyAsync(s.seq_of, s.stage + 3 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-      forward(e, tg, kFP16, T, T, true);
+      forward(e, tg, kFP16, T, T, true, false);
       MSW_CUDA(cudaMemcpyAsync(s.stage + 8, s.next, sizeof(int) * T, cudaMemcpyDeviceToHost, e->st));
       MSW_CUDA(cudaStreamSynchronize(e->st));
       for (int i = 0; i < T; ++i) g[i] = s.stage[8 + i];
@@ -917,7 +927,7 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
       MSW_CUDA(cudaMemcpyAsync(s.pos, s.stage + T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
       MSW_CUDA(cudaMemcpyAsync(s.slot, s.stage + 2 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
       MSW_CUDA(cudaMemcpyAsync(s.seq_of, s.stage + 3 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-      forward(e, m, fmt, T, T, true);
+      forward(e, m, fmt, T, T, true, true);
       MSW_CUDA(cudaMemcpyAsync(s.stage + 4 * T, s.next, sizeof(int) * T, cudaMemcpyDeviceToHost, e->st));
       for (int i = 0; i < T; ++i) {
         msw_result& rr = res[live[i].req];
@@ -1084,7 +1094,17 @@ int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n, int3
     W.s = scales;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (t <= kGemvMaxTokens) {
+      uint32_t* qm = nullptr;
+      if (wtype == kW4) {  // test entry: weights arrive row-packed; build the decode layout
+        qm = dalloc<uint32_t>(size_t(n) * k / 8);
+        launch_repack_w4_mma(static_cast<const uint32_t*>(w), n, k, qm, st);
+        W.w_mma = qm;
+      }
       launch_gemv(W, kProPlain, kEpiStore, x, t, nullptr, 1e-5f, y, st);
+      if (qm) {
+        MSW_CUDA(cudaStreamSynchronize(st));
+        cudaFree(qm);
+      }
     } else {
       half* xh = dalloc<half>(size_t(t) * k);
       int8_t* xq = dalloc<int8_t>(size_t(t) * k);

@@ -1,0 +1,380 @@
+// Blackwell tensor-core linear for T > kGemvMaxTokens tokens (prefill,
+// continuous-batching steps): tcgen05.mma with the accumulator in TMEM.
+//
+// Swap-AB: the WEIGHT tile is the MMA's M=128 operand (128 output features,
+// K-major, exactly the row-major [n, k] storage) and the activation tile is the
+// N operand (BN tokens, K-major [t, k]); D[n, t] accumulates in TMEM (lane =
+// feature, column = token). This keeps M at 128 for any token count, so small
+// continuous-batching steps (T = 16..64) still run full-width UMMAs.
+//
+// Per CTA (one 128 x BN output tile):
+//   warp 0 (one lane) : TMA producer, 4-stage smem ring (SWIZZLE_128B tiles)
+//   warp 1 (one lane) : MMA issuer (tcgen05.mma, commit -> empty barrier)
+//   warp 2            : TMEM allocation owner
+//   warps 0-3         : epilogue, tcgen05.ld 32x32b, fused store / residual
+//                       add / SwiGLU / W8A8 rescale
+//   warps 4-7 (W4)    : dequantisers: packed uint4b8 + fp16 group scale ->
+//                       fp16 (q-8)*s written in the SW128 K-major layout the
+//                       UMMA descriptor reads (no int4 UMMA on sm_100a)
+// kind::f16 for FP16 and W4, kind::i8 (int32 accumulate, exact) for W8A8.
+#include <cuda.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "kernels.cuh"
+
+namespace msw {
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kTileM = 128;     // weight rows per CTA (UMMA M)
+constexpr int kTileKBytes = 128;  // one SW128 row per k-tile
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "MSW_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra MSW_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B canonical layout
+// (8-row x 128-byte atoms, SBO = 1024 B between atoms along M/N, LBO = 16 B).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = uint64_t((saddr & 0x3FFFF) >> 4);
+  d |= uint64_t(1) << 16;           // LBO (16 B; unused for swizzled K-major)
+  d |= uint64_t(1024 >> 4) << 32;   // SBO
+  d |= uint64_t(1) << 46;           // descriptor version (sm_100)
+  d |= uint64_t(2) << 61;           // SWIZZLE_128B
+  return d;
+}
+
+template <int FMT, int BN>
+__device__ __forceinline__ constexpr uint32_t instr_desc() {
+  // c_format bits 4-5 (F32=1, S32=2); a/b format bits 7-9 / 10-12 (F16=0; INT8 signed=1);
+  // K-major A and B; N>>3 at bits 17-22; M>>4 at bits 24-28.
+  return (FMT == kINT8 ? (2u << 4) | (1u << 7) | (1u << 10) : (1u << 4)) |
+         (uint32_t(BN >> 3) << 17) | (uint32_t(kTileM >> 4) << 24);
+}
+
+template <int FMT>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                     uint32_t accumulate) {
+  if (FMT == kINT8) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  }
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+template <int FMT, int BN>
+struct TcCfg {
+  static constexpr bool kIsW4 = FMT == kW4;
+  static constexpr int kElt = FMT == kINT8 ? 1 : 2;
+  static constexpr int kTileK = kTileKBytes / kElt;           // elements per k-tile
+  static constexpr int kUmmaK = FMT == kINT8 ? 32 : 16;       // elements per UMMA
+  static constexpr int kABytes = kTileM * kTileKBytes;        // 16 KB
+  static constexpr int kBBytes = BN * kTileKBytes;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kThreads = kIsW4 ? 256 : 128;
+  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int FMT, int BN, int EPI>
+__global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int N, int K, int T, const void* __restrict__ wscale,
+                   const float* __restrict__ xscale, const uint32_t* __restrict__ w4,
+                   float* __restrict__ y) {
+  using C = TcCfg<FMT, BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* done = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * kTileM, t0 = blockIdx.y * BN;
+  const int nk = K / C::kTileK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], C::kIsW4 ? 1 + 4 : 1);  // TMA arrive (+ 4 dequant warps)
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    if (!C::kIsW4) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_expect_tx(&full[s], C::kIsW4 ? C::kBBytes : C::kStageBytes);
+      if (!C::kIsW4) tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * C::kTileK, n0);
+      tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * C::kTileK, t0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    constexpr uint32_t idesc = instr_desc<FMT, BN>();
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(sA + s * C::kABytes);
+      const uint32_t b0 = smem_u32(sB + s * C::kBBytes);
+#pragma unroll
+      for (int k = 0; k < C::kTileK / C::kUmmaK; ++k) {
+        const uint32_t off = k * C::kUmmaK * C::kElt;  // bytes along the swizzled row
+        umma<FMT>(tmem, sw128_desc(a0 + off), sw128_desc(b0 + off), idesc, (kb | k) != 0);
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(done);
+  } else if (C::kIsW4 && warp >= 4) {
+    // ---- W4 dequantisers: thread r (0..127) owns weight row n0 + r of every k-tile
+    const int r = threadIdx.x - 128;
+    const uint32_t* wrow = w4 + size_t(n0 + r) * (K / 8);
+    const half* srow = static_cast<const half*>(wscale) + size_t(n0 + r) * (K / kW4Group);
+    const half2 k1032 = __float2half2_rn(1032.0f);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      // 64 k per tile = 8 packed words; one group scale covers it (128 | 64)
+      const uint4 p0 = ld_stream(wrow + kb * 8);
+      const uint4 p1 = ld_stream(wrow + kb * 8 + 4);
+      const half2 s2 = __half2half2(srow[(kb * 64) / kW4Group]);
+      mbar_wait(&empty[s], ph ^ 1);
+      uint8_t* rowp = sA + s * C::kABytes + r * 128;
+      const uint32_t words[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {  // chunk c = k 8c..8c+7 = packed word c
+        uint32_t out[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t u = lop3_and_or(words[c] >> (4 * i), 0x000F000Fu, 0x64006400u);
+          const half2 q = __hsub2(*reinterpret_cast<const half2*>(&u), k1032);
+          const half2 wv = __hmul2(q, s2);
+          out[i] = *reinterpret_cast<const uint32_t*>(&wv);
+        }
+        *reinterpret_cast<uint4*>(rowp + ((c ^ (r & 7)) << 4)) = make_uint4(out[0], out[1], out[2], out[3]);
+      }
+      fence_async_smem();  // generic-proxy stores -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  }
+
+  // ---- epilogue (warps 0-3): TMEM lane = weight row, column = token
+  __syncwarp();  // reconverge the producer / MMA lanes before .sync.aligned TMEM loads
+  if (warp < 4) {
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int n = n0 + warp * 32 + lane;
+    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+    float ws = 1.0f;
+    if (FMT == kINT8) ws = static_cast<const float*>(wscale)[n];
+#pragma unroll 1
+    for (int j0 = 0; j0 < BN; j0 += 16) {
+      uint32_t r[16];
+      tmem_ld16(trow + j0, r);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int t = t0 + j0 + j;
+        float v;
+        if (FMT == kINT8) {
+          v = (float(int(r[j])) * (t < T ? xscale[t] : 0.0f)) * ws;
+        } else {
+          v = __uint_as_float(r[j]);
+        }
+        if (EPI == kEpiSwiglu) {
+          const float up = __shfl_xor_sync(0xffffffffu, v, 1);
+          if (t < T && (lane & 1) == 0) y[size_t(t) * (N / 2) + (n >> 1)] = silu(v) * up;
+        } else if (t < T) {
+          if (EPI == kEpiStore) y[size_t(t) * N + n] = v;
+          else y[size_t(t) * N + n] += v;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(C::kTmemCols));
+  }
+}
+
+// ---- host side: tensor maps through the driver entry point (no -lcuda)
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    fn = reinterpret_cast<EncodeFn>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D K-major tile map: rows x k elements, box = box_rows x 128 bytes, SWIZZLE_128B.
+CUtensorMap make_map(const void* base, int elt_bytes, uint64_t rows, uint64_t k, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {k, rows};
+  const cuuint64_t strides[1] = {k * elt_bytes};
+  const cuuint32_t box[2] = {cuuint32_t(kTileKBytes / elt_bytes), cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, elt_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                                 2, const_cast<void*>(base), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
+template <int FMT, int BN, int EPI>
+void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, float* y,
+               cudaStream_t st) {
+  using C = TcCfg<FMT, BN>;
+  static bool attr = false;
+  if (!attr) {
+    MSW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<FMT, BN, EPI>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    attr = true;
+  }
+  const int elt = C::kElt;
+  CUtensorMap ta{};
+  if (FMT != kW4) ta = make_map(W.w, elt, W.n, W.k, kTileM);
+  const CUtensorMap tb = make_map(xact, elt, T, W.k, BN);
+  const dim3 grid(W.n / kTileM, (T + BN - 1) / BN);
+  gemm_tc_kernel<FMT, BN, EPI><<<grid, C::kThreads, C::kSmem, st>>>(
+      ta, tb, W.n, W.k, T, W.s, xscale, static_cast<const uint32_t*>(W.w), y);
+  MSW_LAUNCH_CHECK();
+}
+
+template <int FMT, int EPI>
+void launch_fmt_epi(const LinearW& W, const void* x, const float* xs, int T, float* y,
+                    cudaStream_t st) {
+  if (T <= 16) return launch_bn<FMT, 16, EPI>(W, x, xs, T, y, st);
+  if (T <= 32) return launch_bn<FMT, 32, EPI>(W, x, xs, T, y, st);
+  if (T <= 64) return launch_bn<FMT, 64, EPI>(W, x, xs, T, y, st);
+  return launch_bn<FMT, 128, EPI>(W, x, xs, T, y, st);
+}
+
+template <int FMT>
+void launch_fmt(const LinearW& W, int epi, const void* x, const float* xs, int T, float* y,
+                cudaStream_t st) {
+  if (epi == kEpiStore) return launch_fmt_epi<FMT, kEpiStore>(W, x, xs, T, y, st);
+  if (epi == kEpiResid) return launch_fmt_epi<FMT, kEpiResid>(W, x, xs, T, y, st);
+  return launch_fmt_epi<FMT, kEpiSwiglu>(W, x, xs, T, y, st);
+}
+
+}  // namespace
+
+bool gemm_tc_supported(const LinearW& W) {
+  return W.n % kTileM == 0 && W.k % 128 == 0 && W.n > 0;
+}
+
+void launch_gemm_tc(const LinearW& W, int epi, const half* xh, const int8_t* xq,
+                    const float* xscale, int T, float* y, cudaStream_t st) {
+  if (!gemm_tc_supported(W)) throw ConfigErr("gemm_tc: n must be a multiple of 128, k of 128");
+  switch (W.fmt) {
+    case kFP16: return launch_fmt<kFP16>(W, epi, xh, xscale, T, y, st);
+    case kINT8: return launch_fmt<kINT8>(W, epi, xq, xscale, T, y, st);
+    case kW4: return launch_fmt<kW4>(W, epi, xh, xscale, T, y, st);
+    default: throw ConfigErr("gemm_tc: bad format");
+  }
+}
+
+}  // namespace msw

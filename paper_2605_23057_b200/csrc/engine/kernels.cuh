@@ -17,6 +17,7 @@ struct LinearW {
   int n = 0, k = 0;
   const void* w = nullptr;
   const void* s = nullptr;
+  const void* w_mma = nullptr;  // kW4 only: the same weights in mma.sync fragment order (decode)
   size_t bytes() const {
     const size_t nk = size_t(n) * size_t(k);
     if (fmt == kFP16) return nk * 2;
@@ -49,6 +50,8 @@ constexpr int kGemvMaxTokens = 6;
 void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
                  float eps, float* y, cudaStream_t st);
 void launch_gemv_i8_acc(const int8_t* w, const int8_t* x, int n, int k, int* acc, cudaStream_t st);
+// row-packed W4 -> mma.sync fragment order used by the decode GEMV
+void launch_repack_w4_mma(const uint32_t* packed, int n, int k, uint32_t* mma4, cudaStream_t st);
 
 // ---- gemm.cu: T > 1 tokens (prefill / verify / continuous batching) -----------
 // prep: per token row, optional RMSNorm, then fp16 rounding (xh) or int8
@@ -57,6 +60,11 @@ void launch_prep_act(int fmt, const float* x, int T, int K, const half* gamma, f
                      half* xh, int8_t* xq, float* xscale, cudaStream_t st);
 void launch_gemm(const LinearW& W, int epi, const half* xh, const int8_t* xq, const float* xscale,
                  int T, float* y, cudaStream_t st);
+
+// ---- gemm_tc.cu: tcgen05/TMEM/TMA tensor-core path (n % 128 == 0, k % 128 == 0)
+bool gemm_tc_supported(const LinearW& W);
+void launch_gemm_tc(const LinearW& W, int epi, const half* xh, const int8_t* xq,
+                    const float* xscale, int T, float* y, cudaStream_t st);
 
 // ---- attention.cu -----------------------------------------------------------
 struct AttnShape {
@@ -73,6 +81,13 @@ void launch_rope_append(const float* qkv, int T, const int* pos, const int* slot
 void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
                       const int* block_table, const half* kc, const half* vc, const AttnShape& a,
                       int nsplit, float* part_o, float* part_ml, float* o, cudaStream_t st);
+
+// Decode / continuous batching (each token is the newest of its own sequence):
+// RoPE + KV append fused into the attention kernel; reads fp32 qkv directly.
+void launch_attention_decode(const float* qkv, const float* inv_freq, int T, const int* pos,
+                             const int* slot, const int* seq_of, const int* block_table, half* kc,
+                             half* vc, const AttnShape& a, int nsplit, float* part_o,
+                             float* part_ml, float* o, cudaStream_t st);
 
 // ---- misc.cu ------------------------------------------------------------------
 void launch_embed(const half* emb, const int* tok, int T, int H, float* h, cudaStream_t st);

@@ -7,6 +7,8 @@ namespace {
 
 __global__ void embed_kernel(const half* __restrict__ emb, const int* __restrict__ tok, int H,
                              float* __restrict__ h) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   const half* row = emb + size_t(tok[t]) * H;
   for (int i = threadIdx.x; i < H; i += blockDim.x) h[size_t(t) * H + i] = __half2float(row[i]);
@@ -23,6 +25,8 @@ __device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int* __restrict__ out) {
   __shared__ float sv[32];
   __shared__ int si[32];
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   const float* row = logits + size_t(t) * V;
   float bv = -INFINITY;
@@ -56,6 +60,8 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int* __re
 
 __global__ void gather_rows_kernel(const float* __restrict__ src, const int* __restrict__ rows,
                                    int width, float* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const float* s = src + size_t(rows[r]) * width;
   for (int i = threadIdx.x; i < width; i += blockDim.x) dst[size_t(r) * width + i] = s[i];
@@ -66,6 +72,8 @@ __global__ void gather_rows_kernel(const float* __restrict__ src, const int* __r
 // through block-table row 0.
 __global__ void advance_kernel(const int* next, int* tok, int* pos, int* slot, int* step,
                                int* history, const int* block_table) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x != 0) return;
   const int s = step[0];
   const int t = next[0];
@@ -80,25 +88,22 @@ __global__ void advance_kernel(const int* next, int* tok, int* pos, int* slot, i
 }  // namespace
 
 void launch_embed(const half* emb, const int* tok, int T, int H, float* h, cudaStream_t st) {
-  embed_kernel<<<T, 256, 0, st>>>(emb, tok, H, h);
-  MSW_LAUNCH_CHECK();
+  launch_pdl(embed_kernel, dim3(T), dim3(256), 0, st, emb, tok, H, h);
 }
 
 void launch_argmax(const float* logits, int T, int V, int* out, cudaStream_t st) {
-  argmax_kernel<<<T, 1024, 0, st>>>(logits, V, out);
-  MSW_LAUNCH_CHECK();
+  launch_pdl(argmax_kernel, dim3(T), dim3(1024), 0, st, logits, V, out);
 }
 
 void launch_gather_rows(const float* src, const int* rows, int n, int width, float* dst,
                         cudaStream_t st) {
-  gather_rows_kernel<<<n, 256, 0, st>>>(src, rows, width, dst);
-  MSW_LAUNCH_CHECK();
+  launch_pdl(gather_rows_kernel, dim3(n), dim3(256), 0, st, src, rows, width, dst);
 }
 
 void launch_advance(const int* next, int* tok, int* pos, int* slot, int* step, int* history,
                     const int* block_table, cudaStream_t st) {
-  advance_kernel<<<1, 32, 0, st>>>(next, tok, pos, slot, step, history, block_table);
-  MSW_LAUNCH_CHECK();
+  launch_pdl(advance_kernel, dim3(1), dim3(32), 0, st, next, tok, pos, slot, step, history,
+             block_table);
 }
 
 }  // namespace msw

@@ -2,7 +2,9 @@
 ABI (device pointers from torch) against the CPU oracle on the same inputs.
 
 Bars: K16 init, W8 and W4 quantisers and the INT8 int32 accumulator are
-BIT-EXACT; FP16 / W4 / W8A8 linears within the stated relative tolerance
+BIT-EXACT; FP16 / W4 / W8A8 linears (decode GEMV for t <= 6, tcgen05 GEMM
+for t > 6 and n % 128 == 0, CUDA-core tile GEMM otherwise) within the stated
+relative tolerance
 (max |gpu - oracle| / max |oracle|):  FP16 2e-5, W8A8 2e-5 (int32 exact, the
 only fp ops are two scale multiplies), W4 2e-3 (fp16 partial sums of <= 4
 products by contract)."""
@@ -90,8 +92,8 @@ def _run_linear(fmt, w_dev, s_dev, n, k, x):
     return dy.cpu().numpy()
 
 
-@pytest.mark.parametrize("t", [1, 2, 5, 6, 7, 40])
-@pytest.mark.parametrize("n,k", [(512, 4096), (2048, 512), (256, 14336)])
+@pytest.mark.parametrize("t", [1, 2, 5, 6, 7, 40, 129, 300])
+@pytest.mark.parametrize("n,k", [(512, 4096), (2048, 512), (256, 14336), (96, 256)])
 def test_linear_formats_vs_oracle(cuda_ok, t, n, k):
     torch = _torch()
     rng = np.random.default_rng(t * 1000 + n)
