@@ -131,6 +131,12 @@ int msw_engine_reset_prefix_cache(msw_engine* e);
 int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n,
                int32_t k, const float* x, int32_t t, float* y, void* stream);
 
+/* Decode GEMV on the engine's W4 decode layout (see msw_repack_w4_mma). */
+int msw_linear_w4_decode(const uint32_t* w_mma, const uint16_t* scales, int32_t n, int32_t k,
+                         const float* x, int32_t t, float* y, void* stream);
+/* Row-packed W4 ([n][k/8] words) -> mma.sync fragment order used by decode. */
+int msw_repack_w4_mma(const uint32_t* packed, int32_t n, int32_t k, uint32_t* out, void* stream);
+
 /* INT8 core on identical operands: acc[n] = sum_k w[n,k]*x[k] (int32 exact). */
 int msw_gemv_i8_acc(const int8_t* w, const int8_t* x, int32_t n, int32_t k,
                     int32_t* acc, void* stream);

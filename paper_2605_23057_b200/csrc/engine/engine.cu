@@ -1119,6 +1119,23 @@ int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n, int3
   });
 }
 
+int msw_linear_w4_decode(const uint32_t* w_mma, const uint16_t* scales, int32_t n, int32_t k,
+                         const float* x, int32_t t, float* y, void* stream) {
+  return guarded([&] {
+    LinearW W;
+    W.fmt = kW4;
+    W.n = n;
+    W.k = k;
+    W.s = scales;
+    W.w_mma = w_mma;
+    launch_gemv(W, kProPlain, kEpiStore, x, t, nullptr, 1e-5f, y, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int msw_repack_w4_mma(const uint32_t* packed, int32_t n, int32_t k, uint32_t* out, void* stream) {
+  return guarded([&] { launch_repack_w4_mma(packed, n, k, out, static_cast<cudaStream_t>(stream)); });
+}
+
 int msw_gemv_i8_acc(const int8_t* w, const int8_t* x, int32_t n, int32_t k, int32_t* acc,
                     void* stream) {
   return guarded([&] { launch_gemv_i8_acc(w, x, n, k, acc, static_cast<cudaStream_t>(stream)); });
