@@ -134,7 +134,7 @@ def time_dominant_kernel(iters: int = 50):
         s = torch.empty((n, k // 128), dtype=torch.int16, device="cuda")
         check_engine(lib.msw_quant_w4_rows(w16.data_ptr(), n, k, q.data_ptr(), s.data_ptr(), None))
         qm = torch.empty_like(q)
-        check_engine(lib.msw_repack_w4_mma(q.data_ptr(), n, k, qm.data_ptr(), None))
+        check_engine(lib.msw_repack_decode(2, q.data_ptr(), n, k, qm.data_ptr(), None))
         ws.append(qm)
         del q
         ss.append(s)
@@ -144,19 +144,19 @@ def time_dominant_kernel(iters: int = 50):
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     for i in range(5):
-        check_engine(lib.msw_linear_w4_decode(ws[i % copies].data_ptr(), ss[i % copies].data_ptr(), n,
-                                              k, x.data_ptr(), 1, y.data_ptr(), sp))
+        check_engine(lib.msw_linear_decode(2, ws[i % copies].data_ptr(), ss[i % copies].data_ptr(), n,
+                                           k, x.data_ptr(), 1, y.data_ptr(), sp))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(iters):
-        check_engine(lib.msw_linear_w4_decode(ws[i % copies].data_ptr(), ss[i % copies].data_ptr(), n,
-                                              k, x.data_ptr(), 1, y.data_ptr(), sp))
+        check_engine(lib.msw_linear_decode(2, ws[i % copies].data_ptr(), ss[i % copies].data_ptr(), n,
+                                           k, x.data_ptr(), 1, y.data_ptr(), sp))
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
     algo_bytes = n * k // 2 + n * (k // 128) * 2 + k * 4 + n * 4  # weights + scales + x + y
-    return {"kernel": "gemv_w4_kernel (mma.sync) gate_up 28672x4096, batch 1", "ms": ms, "bytes": algo_bytes,
+    return {"kernel": "gemv_tf_kernel<W4> (TMA bulk ring + mma.sync) gate_up 28672x4096, batch 1", "ms": ms, "bytes": algo_bytes,
             "gbs": algo_bytes / (ms * 1e-3) / 1e9}
 
 

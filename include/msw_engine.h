@@ -127,15 +127,18 @@ int msw_engine_reset_prefix_cache(msw_engine* e);
 
 /* y[T,N] = x[T,K] . W^T for one weight format. x is fp32 [T,K]; y fp32.
  * INT8: x is quantised per token inside the kernel (absmax/127, RNE).
- * W4: w = fp16((q-8)*s), q packed per msw_pack_w4 layout. */
+ * W4: w = (q-8)*s_g, q row-packed (word j = k 8j..8j+7, nibble position
+ * (i>>1) + 4*(i&1) for element i). */
 int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n,
                int32_t k, const float* x, int32_t t, float* y, void* stream);
 
-/* Decode GEMV on the engine's W4 decode layout (see msw_repack_w4_mma). */
-int msw_linear_w4_decode(const uint32_t* w_mma, const uint16_t* scales, int32_t n, int32_t k,
-                         const float* x, int32_t t, float* y, void* stream);
-/* Row-packed W4 ([n][k/8] words) -> mma.sync fragment order used by decode. */
-int msw_repack_w4_mma(const uint32_t* packed, int32_t n, int32_t k, uint32_t* out, void* stream);
+/* Decode GEMV (t <= 6 tokens) on weights already in the engine's decode
+ * (tile-fragment) layout, see msw_repack_decode. */
+int msw_linear_decode(int32_t wtype, const void* w_tf, const void* scales, int32_t n, int32_t k,
+                      const float* x, int32_t t, float* y, void* stream);
+/* Row-major weights (fp16 / int8 / W4 row-packed) -> the decode layout:
+ * 16-row tiles of 512-byte mma.sync A-fragment chunks; same byte count. */
+int msw_repack_decode(int32_t wtype, const void* w, int32_t n, int32_t k, void* out, void* stream);
 
 /* INT8 core on identical operands: acc[n] = sum_k w[n,k]*x[k] (int32 exact). */
 int msw_gemv_i8_acc(const int8_t* w, const int8_t* x, int32_t n, int32_t k,

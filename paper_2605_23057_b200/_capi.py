@@ -105,8 +105,8 @@ def engine_lib() -> C.CDLL:
         lib.msw_engine_reset_prefix_cache.argtypes = [vp]
         lib.msw_linear.argtypes = [i32, vp, vp, i32, i32, vp, i32, vp, vp]
         lib.msw_gemv_i8_acc.argtypes = [vp, vp, i32, i32, vp, vp]
-        lib.msw_linear_w4_decode.argtypes = [vp, vp, i32, i32, vp, i32, vp, vp]
-        lib.msw_repack_w4_mma.argtypes = [vp, i32, i32, vp, vp]
+        lib.msw_linear_decode.argtypes = [i32, vp, vp, i32, i32, vp, i32, vp, vp]
+        lib.msw_repack_decode.argtypes = [i32, vp, i32, i32, vp, vp]
         lib.msw_fill_fp16.argtypes = [vp, i64, i64, C.c_uint64, C.c_uint64, i32, vp]
         lib.msw_quant_int8_rows.argtypes = [vp, i32, i32, vp, vp, vp]
         lib.msw_quant_w4_rows.argtypes = [vp, i32, i32, vp, vp, vp]

@@ -187,33 +187,36 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
     }
     const int n_here = min(32, end - base);
-    for (int j = 0; j < n_here; ++j) {
-      const int pj = base + j;
-      float vf[DPL];
-      if (FUSED && pj == p_self) {
+    for (int j0 = 0; j0 < n_here; j0 += 8) {
+      float vf[8][DPL];
 #pragma unroll
-        for (int d = 0; d < DPL; ++d) vf[d] = vnew[lane * DPL + d];
-      } else if (DPL == 4) {
-        const int sl = bt[pj >> 4] * kKvBlock + (pj & 15);
-        const half* vr = vc + kv_off(sl, hk, Hk, D) + lane * DPL;
-        const uint2 raw = *reinterpret_cast<const uint2*>(vr);
-        const float2 a = __half22float2(*reinterpret_cast<const half2*>(&raw.x));
-        const float2 b = __half22float2(*reinterpret_cast<const half2*>(&raw.y));
-        vf[0] = a.x;
-        vf[1] = a.y;
-        vf[2 % DPL] = b.x;
-        vf[3 % DPL] = b.y;
-      } else {
-        const int sl = bt[pj >> 4] * kKvBlock + (pj & 15);
-        const half* vr = vc + kv_off(sl, hk, Hk, D) + lane * DPL;
+      for (int jj = 0; jj < 8; ++jj) {  // issue up to 8 row loads before consuming any
+        const int pj = base + j0 + jj;
+        if (j0 + jj >= n_here) {
 #pragma unroll
-        for (int d = 0; d < DPL; ++d) vf[d] = __half2float(vr[d]);
+          for (int d = 0; d < DPL; ++d) vf[jj][d] = 0.0f;
+        } else if (FUSED && pj == p_self) {
+#pragma unroll
+          for (int d = 0; d < DPL; ++d) vf[jj][d] = vnew[lane * DPL + d];
+        } else {
+          const int sl = bt[pj >> 4] * kKvBlock + (pj & 15);
+          const half* vr = vc + kv_off(sl, hk, Hk, D) + lane * DPL;
+#pragma unroll
+          for (int d = 0; d < DPL; d += 2) {
+            const float2 f = __half22float2(*reinterpret_cast<const half2*>(vr + d));
+            vf[jj][d] = f.x;
+            vf[jj][d + 1] = f.y;
+          }
+        }
       }
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float w = __shfl_sync(0xffffffffu, e[g], j);
+      for (int jj = 0; jj < 8; ++jj) {
 #pragma unroll
-        for (int d = 0; d < DPL; ++d) acc[g][d] = fmaf(w, vf[d], acc[g][d]);
+        for (int g = 0; g < G; ++g) {
+          const float w = __shfl_sync(0xffffffffu, e[g], (j0 + jj) & 31);
+#pragma unroll
+          for (int d = 0; d < DPL; ++d) acc[g][d] = fmaf(w, vf[jj][d], acc[g][d]);
+        }
       }
     }
   }
@@ -252,6 +255,254 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
         part_ml[idx * 2 + 1] = L;
       }
     }
+  }
+}
+
+// Decode / continuous-batching attention (each query token is the newest
+// token of its own sequence). Per CTA: one (token, kv head, split).
+//  * before griddepcontrol.wait: the K rows and V slices of the first tile of
+//    this split's range are loaded (positions < pos[t] are immutable history;
+//    pos / slot / block table were written by kernels that completed before
+//    the previous one), so the cache reads overlap the QKV GEMV's tail;
+//  * after the wait: RoPE of q and the new k from the fp32 qkv row; the
+//    split-0 CTA appends k / v to the paged cache; the query's own position
+//    uses the fresh k / v from shared memory;
+//  * splits are merged in-kernel: every split writes (m, l, acc) partials and
+//    the last CTA to finish (atomic counter) combines them, so there is no
+//    separate combine launch.
+template <int D>
+struct VSlice;
+template <>
+struct VSlice<128> {
+  using T = uint2;  // 4 halves per lane
+};
+template <>
+struct VSlice<64> {
+  using T = uint32_t;  // 2 halves per lane
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(kAttnWarps * 32)
+    attn_decode_kernel(const float* __restrict__ qkv, const float* __restrict__ inv_freq,
+                       const int* __restrict__ pos, const int* __restrict__ slot,
+                       const int* __restrict__ seq_of, const int* __restrict__ block_table,
+                       int max_blocks, half* __restrict__ kc, half* __restrict__ vc, int Hq, int Hk,
+                       int nsplit, float* __restrict__ part_o, float* __restrict__ part_ml,
+                       int* __restrict__ counters, float* __restrict__ o) {
+  constexpr int DPL = D / 32;
+  constexpr int KC = D / 8;
+  using VT = typename VSlice<D>::T;
+  __shared__ float qs[G][D];
+  __shared__ float knew[D], vnew[D];
+  __shared__ float wm[kAttnWarps][G], wl[kAttnWarps][G];
+  __shared__ float wacc[kAttnWarps][G][D];
+  __shared__ int is_last;
+  const int t = blockIdx.x, hk = blockIdx.y, sp = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p_self = pos[t];
+  const int ctx = p_self + 1;
+  const int chunk = split_chunk(ctx, nsplit);
+  const int begin = sp * chunk;
+  if (begin >= ctx) {
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
+  const int end = min(ctx, begin + chunk);
+  const int active = (ctx + chunk - 1) / chunk;
+  const int* bt = block_table + size_t(seq_of[t]) * max_blocks;
+
+  uint4 kreg[KC];
+  VT vreg[32];
+  auto load_tile = [&](int base) {
+    const int p = base + lane;
+    if (p < end && p != p_self) {
+      const int sl = bt[p >> 4] * kKvBlock + (p & 15);
+      const uint4* kr = reinterpret_cast<const uint4*>(kc + kv_off(sl, hk, Hk, D));
+#pragma unroll
+      for (int c = 0; c < KC; ++c) kreg[c] = kr[c];
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int pj = base + j;
+      if (pj < end && pj != p_self) {
+        const int sl = bt[pj >> 4] * kKvBlock + (pj & 15);
+        vreg[j] = *reinterpret_cast<const VT*>(vc + kv_off(sl, hk, Hk, D) + lane * DPL);
+      }
+    }
+  };
+  const int first = begin + warp * 32;
+  if (first < end) load_tile(first);  // history only: safe before the wait
+
+  pdl_wait();
+  pdl_trigger();
+  {
+    const int width = (Hq + 2 * Hk) * D;
+    const float* row = qkv + size_t(t) * width;
+    const float pf = float(p_self);
+    for (int i = threadIdx.x; i < (G + 1) * (D / 2); i += blockDim.x) {
+      const int h = i / (D / 2), j = i % (D / 2);
+      const float* src = h < G ? row + size_t(hk * G + h) * D : row + size_t(Hq + hk) * D;
+      float sn, cs;
+      sincosf(pf * inv_freq[j], &sn, &cs);
+      const float x0 = src[j], x1 = src[j + D / 2];
+      const float y0 = __half2float(__float2half_rn(__fsub_rn(__fmul_rn(x0, cs), __fmul_rn(x1, sn))));
+      const float y1 = __half2float(__float2half_rn(__fadd_rn(__fmul_rn(x1, cs), __fmul_rn(x0, sn))));
+      if (h < G) {
+        qs[h][j] = y0;
+        qs[h][j + D / 2] = y1;
+      } else {
+        knew[j] = y0;
+        knew[j + D / 2] = y1;
+      }
+    }
+    for (int d = threadIdx.x; d < D; d += blockDim.x)
+      vnew[d] = __half2float(__float2half_rn(row[size_t(Hq + Hk + hk) * D + d]));
+  }
+  __syncthreads();
+  if (sp == 0) {
+    const size_t off = kv_off(slot[t], hk, Hk, D);
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+      kc[off + d] = __float2half_rn(knew[d]);
+      vc[off + d] = __float2half_rn(vnew[d]);
+    }
+  }
+  const float scale = 1.0f / sqrtf(float(D));
+  float m[G], l[G], acc[G][DPL];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.0f;
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) acc[g][d] = 0.0f;
+  }
+  for (int base = first; base < end; base += kAttnWarps * 32) {
+    if (base != first) load_tile(base);
+    const int p = base + lane;
+    float s[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) s[g] = 0.0f;
+    if (p < end) {
+      if (p == p_self) {
+        for (int d = 0; d < D; ++d) {
+#pragma unroll
+          for (int g = 0; g < G; ++g) s[g] = fmaf(qs[g][d], knew[d], s[g]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          const half2* kh = reinterpret_cast<const half2*>(&kreg[c]);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float4 q0 = *reinterpret_cast<const float4*>(&qs[g][c * 8]);
+            const float4 q1 = *reinterpret_cast<const float4*>(&qs[g][c * 8 + 4]);
+            const float2 k0 = __half22float2(kh[0]), k1 = __half22float2(kh[1]);
+            const float2 k2 = __half22float2(kh[2]), k3 = __half22float2(kh[3]);
+            s[g] = fmaf(q0.x, k0.x, fmaf(q0.y, k0.y, fmaf(q0.z, k1.x, fmaf(q0.w, k1.y, s[g]))));
+            s[g] = fmaf(q1.x, k2.x, fmaf(q1.y, k2.y, fmaf(q1.z, k3.x, fmaf(q1.w, k3.y, s[g]))));
+          }
+        }
+      }
+    }
+    float e[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float sv = p < end ? s[g] * scale : -INFINITY;
+      const float mn = fmaxf(m[g], warp_max(sv));
+      const float corr = expf(m[g] - mn);
+      e[g] = p < end ? expf(sv - mn) : 0.0f;
+      l[g] = l[g] * corr + warp_sum(e[g]);
+      m[g] = mn;
+#pragma unroll
+      for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
+    }
+    const int n_here = min(32, end - base);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < n_here) {
+        const int pj = base + j;
+        float vf[DPL];
+        if (pj == p_self) {
+#pragma unroll
+          for (int d = 0; d < DPL; ++d) vf[d] = vnew[lane * DPL + d];
+        } else {
+          const half2* vh = reinterpret_cast<const half2*>(&vreg[j]);
+#pragma unroll
+          for (int d = 0; d < DPL / 2; ++d) {
+            const float2 f = __half22float2(vh[d]);
+            vf[2 * d] = f.x;
+            vf[2 * d + 1] = f.y;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float w = __shfl_sync(0xffffffffu, e[g], j);
+#pragma unroll
+          for (int d = 0; d < DPL; ++d) acc[g][d] = fmaf(w, vf[d], acc[g][d]);
+        }
+      }
+    }
+  }
+  // merge the warps of this CTA
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (lane == 0) {
+      wm[warp][g] = m[g];
+      wl[warp][g] = l[g];
+    }
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) wacc[warp][g][lane * DPL + d] = acc[g][d];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const int g = i / D, d = i % D;
+    float M = -INFINITY;
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, wm[w][g]);
+    float L = 0.0f, A = 0.0f;
+    if (M != -INFINITY)
+      for (int w = 0; w < kAttnWarps; ++w) {
+        const float f = expf(wm[w][g] - M);
+        L += wl[w][g] * f;
+        A += wacc[w][g][d] * f;
+      }
+    const int hq = hk * G + g;
+    if (active == 1) {
+      o[(size_t(t) * Hq + hq) * D + d] = L > 0.0f ? A / L : 0.0f;
+    } else {
+      const size_t idx = (size_t(t) * Hq + hq) * nsplit + sp;
+      part_o[idx * D + d] = A;
+      if (d == 0) {
+        part_ml[idx * 2] = M;
+        part_ml[idx * 2 + 1] = L;
+      }
+    }
+  }
+  if (active == 1) return;
+  // last split to finish merges all partials of this (token, kv head)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int done = atomicAdd(&counters[t * Hk + hk], 1);
+    is_last = done == active - 1;
+    if (is_last) counters[t * Hk + hk] = 0;  // reset for the next step
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    const int g = i / D, d = i % D;
+    const size_t base = (size_t(t) * Hq + hk * G + g) * nsplit;
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < active; ++s2) M = fmaxf(M, __ldcg(&part_ml[(base + s2) * 2]));
+    float L = 0.0f, A = 0.0f;
+    for (int s2 = 0; s2 < active; ++s2) {
+      const float ms = __ldcg(&part_ml[(base + s2) * 2]);
+      if (ms == -INFINITY) continue;
+      const float f = expf(ms - M);
+      L += __ldcg(&part_ml[(base + s2) * 2 + 1]) * f;
+      A += __ldcg(&part_o[(base + s2) * D + d]) * f;
+    }
+    o[(size_t(t) * Hq + hk * G + g) * D + d] = L > 0.0f ? A / L : 0.0f;
   }
 }
 
@@ -344,9 +595,24 @@ void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
 void launch_attention_decode(const float* qkv, const float* inv_freq, int T, const int* pos,
                              const int* slot, const int* seq_of, const int* block_table, half* kc,
                              half* vc, const AttnShape& a, int nsplit, float* part_o,
-                             float* part_ml, float* o, cudaStream_t st) {
-  attention_any<true>(nullptr, qkv, inv_freq, T, pos, slot, seq_of, block_table, kc, vc, a, nsplit,
-                      part_o, part_ml, o, st);
+                             float* part_ml, int* counters, float* o, cudaStream_t st) {
+  const int G = a.n_heads / a.n_kv_heads;
+  const dim3 grid(T, a.n_kv_heads, nsplit), thr(kAttnWarps * 32);
+#define MSW_DEC(DD, GG)                                                                       \
+  if (a.head_dim == DD && G == GG)                                                            \
+    return launch_pdl(attn_decode_kernel<DD, GG>, grid, thr, 0, st, qkv, inv_freq, pos, slot, \
+                      seq_of, block_table, a.max_blocks_per_seq, kc, vc, a.n_heads,           \
+                      a.n_kv_heads, nsplit, part_o, part_ml, counters, o);
+  MSW_DEC(128, 1)
+  MSW_DEC(128, 2)
+  MSW_DEC(128, 4)
+  MSW_DEC(128, 8)
+  MSW_DEC(64, 1)
+  MSW_DEC(64, 2)
+  MSW_DEC(64, 4)
+  MSW_DEC(64, 8)
+#undef MSW_DEC
+  throw ConfigErr("attention: unsupported head_dim / GQA group");
 }
 
 }  // namespace msw

@@ -152,6 +152,7 @@ struct Model {
   bool fmt_on[3] = {false, false, false};
   half* embed = nullptr;
   half* lm_head = nullptr;
+  half* lm_head_tf = nullptr;  // decode (tile-fragment) copy
   half* final_norm = nullptr;
   float* inv_freq = nullptr;
   std::vector<Layer> layers;
@@ -196,6 +197,7 @@ struct Scratch {
   int* slot = nullptr;
   int* seq_of = nullptr;
   int* logit_rows = nullptr;
+  int* split_cnt = nullptr;  // attention split-merge counters [tokens, kv heads], self-resetting
   int* next = nullptr;
   int* step = nullptr;
   int* hist = nullptr;
@@ -261,12 +263,13 @@ LinearW make_linear(Model& m, int fmt, const half* master, int n, int k, cudaStr
     uint32_t* q = model_alloc<uint32_t>(m, size_t(n) * k / 8);
     half* s = model_alloc<half>(m, size_t(n) * (k / kW4Group));
     launch_quant_w4(master, n, k, q, s, st);
-    uint32_t* qm = model_alloc<uint32_t>(m, size_t(n) * k / 8);
-    launch_repack_w4_mma(q, n, k, qm, st);
     L.w = q;
     L.s = s;
-    L.w_mma = qm;
   }
+  // decode copy in tile-fragment order (prefill keeps the row-major copy for TMA)
+  uint8_t* tf = model_alloc<uint8_t>(m, tf_bytes(fmt, n, k));
+  launch_repack_tf(fmt, L.w, n, k, tf, st);
+  L.w_tf = tf;
   return L;
 }
 
@@ -292,6 +295,8 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
     MSW_CUDA(cudaMemcpy(d_agree, agree.data(), V, cudaMemcpyHostToDevice));
     m.lm_head = model_alloc<half>(m, size_t(V) * H);
     launch_lm_head(m.embed, d_pred, d_agree, is_draft ? 1 : 0, V, H, m.lm_head, st);
+    m.lm_head_tf = model_alloc<half>(m, size_t(V) * H);
+    launch_repack_tf(kFP16, m.lm_head, V, H, m.lm_head_tf, st);
     MSW_CUDA(cudaStreamSynchronize(st));
     cudaFree(d_pred);
     cudaFree(d_agree);
@@ -424,6 +429,8 @@ void alloc_scratch(msw_engine* e) {
   s.slot = dalloc<int>(T);
   s.seq_of = dalloc<int>(T);
   s.logit_rows = dalloc<int>(kMaxLogitRows);
+  s.split_cnt = dalloc<int>(tsplit * 64);
+  MSW_CUDA(cudaMemset(s.split_cnt, 0, sizeof(int) * tsplit * 64));
   s.next = dalloc<int>(kMaxLogitRows);
   s.step = dalloc<int>(1);
   s.hist = dalloc<int>(size_t(e->cfg.max_seq_len) + 64);
@@ -433,7 +440,8 @@ void alloc_scratch(msw_engine* e) {
   for (void* p : {(void*)s.h, (void*)s.qkv, (void*)s.q16, (void*)s.o, (void*)s.act, (void*)s.xh,
                   (void*)s.xq, (void*)s.xscale, (void*)s.hsel, (void*)s.logits, (void*)s.part_o,
                   (void*)s.part_ml, (void*)s.tok, (void*)s.pos, (void*)s.slot, (void*)s.seq_of,
-                  (void*)s.logit_rows, (void*)s.next, (void*)s.step, (void*)s.hist})
+                  (void*)s.logit_rows, (void*)s.split_cnt, (void*)s.next, (void*)s.step,
+                  (void*)s.hist})
     e->owned.push_back(p);
 }
 
@@ -469,8 +477,8 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
     }
     if (tokens_independent) {  // decode / CB: RoPE + KV append fused into attention
       launch_attention_decode(s.qkv, m.inv_freq, T, s.pos, s.slot, s.seq_of, m.block_table, kc,
-                              vc, m.ash, nsplit, s.part_o, s.part_ml, s.o, st);
-      n += nsplit > 1 ? 2 : 1;
+                              vc, m.ash, nsplit, s.part_o, s.part_ml, s.split_cnt, s.o, st);
+      n += 1;
     } else {
       launch_rope_append(s.qkv, T, s.pos, s.slot, m.inv_freq, m.ash, s.q16, kc, vc, st);
       launch_attention(s.q16, T, s.pos, s.seq_of, m.block_table, kc, vc, m.ash, nsplit, s.part_o,
@@ -505,6 +513,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
   head.n = c.vocab;
   head.k = H;
   head.w = m.lm_head;
+  head.w_tf = m.lm_head_tf;
   if (n_logits <= kGemvMaxTokens) {
     launch_gemv(head, kProNorm, kEpiStore, hrows, n_logits, m.final_norm, eps, s.logits, st);
     ++n;
@@ -1094,17 +1103,13 @@ int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n, int3
     W.s = scales;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (t <= kGemvMaxTokens) {
-      uint32_t* qm = nullptr;
-      if (wtype == kW4) {  // test entry: weights arrive row-packed; build the decode layout
-        qm = dalloc<uint32_t>(size_t(n) * k / 8);
-        launch_repack_w4_mma(static_cast<const uint32_t*>(w), n, k, qm, st);
-        W.w_mma = qm;
-      }
+      // test entry: weights arrive row-major; build the decode layout first
+      uint8_t* tf = dalloc<uint8_t>(tf_bytes(wtype, n, k));
+      launch_repack_tf(wtype, w, n, k, tf, st);
+      W.w_tf = tf;
       launch_gemv(W, kProPlain, kEpiStore, x, t, nullptr, 1e-5f, y, st);
-      if (qm) {
-        MSW_CUDA(cudaStreamSynchronize(st));
-        cudaFree(qm);
-      }
+      MSW_CUDA(cudaStreamSynchronize(st));
+      cudaFree(tf);
     } else {
       half* xh = dalloc<half>(size_t(t) * k);
       int8_t* xq = dalloc<int8_t>(size_t(t) * k);
@@ -1119,21 +1124,21 @@ int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n, int3
   });
 }
 
-int msw_linear_w4_decode(const uint32_t* w_mma, const uint16_t* scales, int32_t n, int32_t k,
-                         const float* x, int32_t t, float* y, void* stream) {
+int msw_linear_decode(int32_t wtype, const void* w_tf, const void* scales, int32_t n, int32_t k,
+                      const float* x, int32_t t, float* y, void* stream) {
   return guarded([&] {
     LinearW W;
-    W.fmt = kW4;
+    W.fmt = wtype;
     W.n = n;
     W.k = k;
     W.s = scales;
-    W.w_mma = w_mma;
+    W.w_tf = w_tf;
     launch_gemv(W, kProPlain, kEpiStore, x, t, nullptr, 1e-5f, y, static_cast<cudaStream_t>(stream));
   });
 }
 
-int msw_repack_w4_mma(const uint32_t* packed, int32_t n, int32_t k, uint32_t* out, void* stream) {
-  return guarded([&] { launch_repack_w4_mma(packed, n, k, out, static_cast<cudaStream_t>(stream)); });
+int msw_repack_decode(int32_t wtype, const void* w, int32_t n, int32_t k, void* out, void* stream) {
+  return guarded([&] { launch_repack_tf(wtype, w, n, k, out, static_cast<cudaStream_t>(stream)); });
 }
 
 int msw_gemv_i8_acc(const int8_t* w, const int8_t* x, int32_t n, int32_t k, int32_t* acc,

@@ -1,33 +1,33 @@
-// Decode GEMV (1..6 tokens) for the three weight formats.
+// Decode GEMV (1..6 tokens) for the three weight formats, TMA-fed, on the
+// tensor cores.
 //
-// HBM-bound: every weight byte is read once per step with 128-bit
-// ld.global.nc.L1::no_allocate loads, coalesced across the warp.
+// HBM-bound: every weight byte is read once per step. Decode weights are
+// stored "tile-fragment" (TF): 16-row tiles, each a contiguous run of 512-byte
+// chunks, a chunk being one 16-byte mma.sync A fragment per lane:
+//   FP16 : m16n8k16 f16 -> f32, chunk = 16 rows x 16 k
+//   INT8 : m16n8k32 s8 -> s32 (exact), chunk = 16 rows x 32 k
+//   W4   : m16n8k16 f16 on lop3/hsub2-dequantised (q-8), chunk = 16 rows x 64 k
+//          (4 k16 steps), group scale applied in fp32 per 128 k
+// The 8 MMA columns carry up to 8 tokens (verify / tiny batches) at no cost.
 //
-//  * FP16 / W8A8 (CUDA cores): one warp owns a PAIR of output rows (so the
-//    SwiGLU epilogue combines gate/up, interleaved rows 2i / 2i+1, in
-//    registers), lanes stride 16-byte chunks along K, warp-shuffle reduction;
-//    W8A8 uses dp4a with exact int32 accumulation.
-//  * W4 g128 (tensor cores, mma.sync m16n8k16): weights are stored in the
-//    fragment order of the A operand, so one 16-byte load per lane is four
-//    k16 steps of a 16-row tile; dequant is lop3 (nibble -> fp16 1024+q) and
-//    one hsub2 -> (q-8) exact; the group scale is applied in fp32 per 128-k
-//    group. The 8 MMA columns are up to 8 tokens (verify / tiny batches) for
-//    free. K is split across the 8 warps of a CTA and reduced in smem.
-//
-// Grids are persistent (<= 2 CTAs per SM), so the activation prologue
-// (RMSNorm + fp16 rounding or per-token int8 quantisation, into smem) runs
-// once per CTA, and every kernel is launched with programmatic dependent
-// launch: the first weight loads are issued BEFORE griddepcontrol.wait, so
-// they overlap the previous kernel's tail.
+// Per CTA (persistent, one per SM, a contiguous tile range): a producer warp
+// streams the CTA's weights through an smem ring with cp.async.bulk (<= 16 KB
+// stages, mbarrier full/empty) and starts BEFORE griddepcontrol.wait, so the
+// ring fills while the previous kernel finishes (PDL); 8 consumer warps each
+// take a slice of every stage, run the MMAs, and reduce the 16 x 8 tile across
+// warps in smem at tile boundaries. The activation prologue (RMSNorm, fp16
+// rounding / per-token int8 quantisation) runs once per CTA into smem.
 #include "kernels.cuh"
 
 namespace msw {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kUnroll = 4;      // 16-byte chunks per lane per row in flight (CUDA-core path)
-constexpr int kCtasPerSm = 2;
+constexpr int kConsumers = 8;
+constexpr int kThreads = (kConsumers + 1) * 32;  // + producer warp
+constexpr int kConsThreads = kConsumers * 32;
+constexpr int kChunkBytes = 512;
+constexpr int kMaxStages = 8;
+constexpr int kSmemBudget = 200 * 1024;
 
 __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -37,18 +37,68 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t
 __device__ __forceinline__ half2 u2h2(uint32_t u) { return *reinterpret_cast<half2*>(&u); }
 __device__ __forceinline__ uint32_t h22u(half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
-// ---------------------------------------------------------------- prologue
+__device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                       uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int FMT>
+struct TF {
+  static constexpr int kChunkK = FMT == kFP16 ? 16 : (FMT == kINT8 ? 32 : 64);
+  static constexpr int kMinChunksPerWarp = FMT == kW4 ? 2 : 1;  // a W4 scale group is 2 chunks
+};
+
+// Stage size in chunks: the largest power of two <= 32 dividing a tile's chunks.
+__host__ __device__ inline int stage_chunks(int chunks_per_tile) {
+  int s = 32;
+  while (s > 1 && chunks_per_tile % s) s >>= 1;
+  return s;
+}
+
+// Consumer-only block reductions (named barrier 1 over the consumer warps).
+__device__ __forceinline__ float cons_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  named_sync(1, kConsThreads);
+  if (lane == 0) red[warp] = v;
+  named_sync(1, kConsThreads);
+  const float t = lane < kConsumers ? red[lane] : 0.0f;
+  return warp_sum(t);
+}
+__device__ __forceinline__ float cons_max(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_max(v);
+  named_sync(1, kConsThreads);
+  if (lane == 0) red[warp] = v;
+  named_sync(1, kConsThreads);
+  const float t = lane < kConsumers ? red[lane] : -3.402823466e38f;
+  return warp_max(t);
+}
+
 // x fp32 [T, k] -> smem: fp16 [NT][k] (FP16 / W4) or int8 [NT][k] + scale.
 template <int FMT, int PRO, int NT>
 __device__ __forceinline__ void prologue(const float* __restrict__ x, const half* __restrict__ gamma,
-                                         float eps, int k, int T, uint8_t* smem, float* red,
+                                         float eps, int k, int T, uint8_t* xs, float* red,
                                          float* xscale) {
+  const int tid = threadIdx.x;
   for (int t = 0; t < NT; ++t) {
-    if (t >= T) {  // padding token
-      const int bytes = FMT == kINT8 ? k : 2 * k;
-      for (int i = threadIdx.x; i < bytes / 16; i += kThreads)
-        reinterpret_cast<uint4*>(smem + size_t(t) * bytes)[i] = make_uint4(0, 0, 0, 0);
-      if (threadIdx.x == 0) xscale[t] = 0.0f;
+    const int bytes = FMT == kINT8 ? k : 2 * k;
+    if (t >= T) {
+      for (int i = tid; i < bytes / 16; i += kConsThreads)
+        reinterpret_cast<uint4*>(xs + size_t(t) * bytes)[i] = make_uint4(0, 0, 0, 0);
+      if (tid == 0) xscale[t] = 0.0f;
       continue;
     }
     const float4* xt = reinterpret_cast<const float4*>(x + size_t(t) * k);
@@ -56,18 +106,18 @@ __device__ __forceinline__ void prologue(const float* __restrict__ x, const half
     float r = 1.0f;
     if (PRO == kProNorm) {
       float ss = 0.0f;
-      for (int i = threadIdx.x; i < k4; i += kThreads) {
+      for (int i = tid; i < k4; i += kConsThreads) {
         const float4 v = xt[i];
         ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
       }
-      ss = block_sum(ss, red);
+      ss = cons_sum(ss, red);
       r = 1.0f / sqrtf(ss / float(k) + eps);
     }
     auto act4 = [&](int i) -> float4 {
       float4 v = xt[i];
       if (PRO == kProNorm) {
-        const half2* g = reinterpret_cast<const half2*>(gamma) + 2 * i;
-        const float2 g0 = __half22float2(g[0]), g1 = __half22float2(g[1]);
+        const half2* gm = reinterpret_cast<const half2*>(gamma) + 2 * i;
+        const float2 g0 = __half22float2(gm[0]), g1 = __half22float2(gm[1]);
         v.x = (v.x * r) * g0.x;
         v.y = (v.y * r) * g0.y;
         v.z = (v.z * r) * g1.x;
@@ -77,38 +127,36 @@ __device__ __forceinline__ void prologue(const float* __restrict__ x, const half
     };
     if (FMT == kINT8) {
       float amax = 0.0f;
-      for (int i = threadIdx.x; i < k4; i += kThreads) {
+      for (int i = tid; i < k4; i += kConsThreads) {
         const float4 v = act4(i);
         amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
       }
-      amax = block_max(amax, red);
+      amax = cons_max(amax, red);
       const float s = amax / 127.0f;
-      char4* xq = reinterpret_cast<char4*>(smem + size_t(t) * k);
+      char4* xq = reinterpret_cast<char4*>(xs + size_t(t) * k);
       auto q = [&](float v) -> signed char {
         const float u = amax > 0.0f ? rintf(v / s) : 0.0f;
         return static_cast<signed char>(fminf(fmaxf(u, -127.0f), 127.0f));
       };
-      for (int i = threadIdx.x; i < k4; i += kThreads) {
+      for (int i = tid; i < k4; i += kConsThreads) {
         const float4 v = act4(i);
         xq[i] = make_char4(q(v.x), q(v.y), q(v.z), q(v.w));
       }
-      if (threadIdx.x == 0) xscale[t] = s;
+      if (tid == 0) xscale[t] = s;
     } else {
-      half2* xh = reinterpret_cast<half2*>(smem + size_t(t) * 2 * k);
-      for (int i = threadIdx.x; i < k4; i += kThreads) {
+      half2* xh = reinterpret_cast<half2*>(xs + size_t(t) * 2 * k);
+      for (int i = tid; i < k4; i += kConsThreads) {
         const float4 v = act4(i);
         xh[2 * i] = __floats2half2_rn(v.x, v.y);
         xh[2 * i + 1] = __floats2half2_rn(v.z, v.w);
       }
     }
-    __syncthreads();
+    named_sync(1, kConsThreads);
   }
-  __syncthreads();
 }
 
 template <int EPI>
-__device__ __forceinline__ void store_out(float* y, int n, int t, int row, float v0, float v1) {
-  // rows (row, row+1): STORE / RESID write both; SWIGLU writes silu(v0) * v1 at row/2
+__device__ __forceinline__ void store_pair(float* y, int n, int t, int row, float v0, float v1) {
   if (EPI == kEpiStore) {
     y[size_t(t) * n + row] = v0;
     y[size_t(t) * n + row + 1] = v1;
@@ -116,197 +164,133 @@ __device__ __forceinline__ void store_out(float* y, int n, int t, int row, float
     y[size_t(t) * n + row] += v0;
     y[size_t(t) * n + row + 1] += v1;
   } else {
-    y[size_t(t) * (n / 2) + row / 2] = silu(v0) * v1;
+    y[size_t(t) * (n / 2) + row / 2] = silu(v0) * v1;  // rows (2i, 2i+1) = (gate_i, up_i)
   }
 }
 
-// ------------------------------------------------- FP16 / W8A8 (CUDA cores)
 template <int FMT, int PRO, int EPI, int NT>
-__global__ void __launch_bounds__(kThreads) gemv_cc_kernel(const uint8_t* __restrict__ w,
-                                                           const void* __restrict__ ws, int n, int k,
-                                                           const float* __restrict__ x, int T,
-                                                           const half* __restrict__ gamma,
-                                                           float eps, float* __restrict__ y) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ float red[32];
-  __shared__ float xscale[NT];
+__global__ void __launch_bounds__(kThreads, 1)
+    gemv_tf_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
+                   const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
+                   float* __restrict__ y, int n_stages) {
   using Acc = typename std::conditional<FMT == kINT8, int, float>::type;
-  constexpr int E = FMT == kINT8 ? 16 : 8;  // elements per 16-byte chunk
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nch = k / E;
-  const size_t row_bytes = size_t(nch) * 16;
-  const int tok16 = (FMT == kINT8 ? k : 2 * k) / 16;  // uint4 per token in smem
-  const int npairs = n >> 1;
-  const int groups = (nch + 32 * kUnroll - 1) / (32 * kUnroll);
-  const int pair_stride = gridDim.x * kWarps;
-  int pair = blockIdx.x * kWarps + warp;
-
-  uint4 buf[2][kUnroll];
-  auto load = [&](int p, int g, uint4 (&b)[2][kUnroll]) {
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const uint8_t* row = w + size_t(2 * p + r) * row_bytes;
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int c = (g * kUnroll + u) * 32 + lane;
-        b[r][u] = c < nch ? ld_stream(row + size_t(c) * 16) : make_uint4(0, 0, 0, 0);
-      }
-    }
-  };
-  if (pair < npairs) load(pair, 0, buf);  // weights only: safe before the dependency wait
-  pdl_wait();
-  pdl_trigger();
-  prologue<FMT, PRO, NT>(x, gamma, eps, k, T, smem, red, xscale);
-  const uint4* xs = reinterpret_cast<const uint4*>(smem);
-
-  for (; pair < npairs; pair += pair_stride) {
-    Acc acc0[NT], acc1[NT];
-#pragma unroll
-    for (int t = 0; t < NT; ++t) acc0[t] = acc1[t] = 0;
-    for (int g = 0; g < groups; ++g) {
-      uint4 nxt[2][kUnroll];
-      if (g + 1 < groups) load(pair, g + 1, nxt);
-      else if (pair + pair_stride < npairs) load(pair + pair_stride, 0, nxt);
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int c = (g * kUnroll + u) * 32 + lane;
-        if (c < nch) {
-#pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            const uint4 xv = xs[t * tok16 + c];  // one smem load serves both rows
-            if (FMT == kINT8) {
-              acc0[t] = __dp4a(int(buf[0][u].x), int(xv.x), acc0[t]);
-              acc0[t] = __dp4a(int(buf[0][u].y), int(xv.y), acc0[t]);
-              acc0[t] = __dp4a(int(buf[0][u].z), int(xv.z), acc0[t]);
-              acc0[t] = __dp4a(int(buf[0][u].w), int(xv.w), acc0[t]);
-              acc1[t] = __dp4a(int(buf[1][u].x), int(xv.x), acc1[t]);
-              acc1[t] = __dp4a(int(buf[1][u].y), int(xv.y), acc1[t]);
-              acc1[t] = __dp4a(int(buf[1][u].z), int(xv.z), acc1[t]);
-              acc1[t] = __dp4a(int(buf[1][u].w), int(xv.w), acc1[t]);
-            } else {
-              const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
-              const uint32_t w0[4] = {buf[0][u].x, buf[0][u].y, buf[0][u].z, buf[0][u].w};
-              const uint32_t w1[4] = {buf[1][u].x, buf[1][u].y, buf[1][u].z, buf[1][u].w};
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float2 b = __half22float2(u2h2(xw[i]));
-                const float2 a0 = __half22float2(u2h2(w0[i]));
-                const float2 a1 = __half22float2(u2h2(w1[i]));
-                acc0[t] = fmaf(a0.x, b.x, fmaf(a0.y, b.y, acc0[t]));
-                acc1[t] = fmaf(a1.x, b.x, fmaf(a1.y, b.y, acc1[t]));
-              }
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) buf[r][u] = nxt[r][u];
-    }
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      float v0, v1;
-      if (FMT == kINT8) {
-        const int a0 = warp_sum_i(int(acc0[t])), a1 = warp_sum_i(int(acc1[t]));
-        const float* sw = static_cast<const float*>(ws);
-        v0 = (float(a0) * xscale[t]) * sw[2 * pair];
-        v1 = (float(a1) * xscale[t]) * sw[2 * pair + 1];
-      } else {
-        v0 = warp_sum(float(acc0[t]));
-        v1 = warp_sum(float(acc1[t]));
-      }
-      if (lane == 0 && t < T) store_out<EPI>(y, n, t, 2 * pair, v0, v1);
-    }
-  }
-}
-
-// ------------------------------------------------------- W4 (mma.sync path)
-// Layout "mma4": [n/16 row tiles][k/64 chunks][32 lanes][4 words]; word j =
-// k16 step j of the chunk; its 8 nibbles (position (i>>1) + 4*(i&1) for
-// element i) are the A fragment a0..a3 of lane (g = lane/4, t = lane%4):
-// a0 = (row g, k 2t..2t+1), a1 = (row g+8, k 2t..), a2 = (row g, k 2t+8..),
-// a3 = (row g+8, k 2t+8..).
-constexpr int kW4Unroll = 8;  // chunks (512 B per warp) in flight per warp
-
-__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
-                                         uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-template <int PRO, int EPI, int NT>
-__global__ void __launch_bounds__(kThreads) gemv_w4_kernel(const uint4* __restrict__ wq,
-                                                           const half* __restrict__ ws, int n, int k,
-                                                           const float* __restrict__ x, int T,
-                                                           const half* __restrict__ gamma,
-                                                           float eps, float* __restrict__ y) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int CK = TF<FMT>::kChunkK;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ float red[32];
   __shared__ float xscale[NT];
-  __shared__ float part[kWarps][16][8];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, tq = lane & 3;
-  const int nchunks = k / 64;
-  // K slice of this warp, in chunks; even so a 128-k scale group never straddles warps
-  const int per_warp = (((nchunks + kWarps - 1) / kWarps) + 1) & ~1;
-  const int c_begin = warp * per_warp;
-  const int c_end = min(nchunks, c_begin + per_warp);
-  const int ntiles = n / 16;
-  const int groups_k = k / kW4Group;
-  int tile = blockIdx.x;
+  __shared__ uint32_t part[kConsumers][16][8];  // raw 32-bit partials (f32 or s32)
 
-  uint4 cur[kW4Unroll];
-  auto load = [&](int tl, int c0, uint4 (&b)[kW4Unroll]) {
-    const uint4* base = wq + (size_t(tl) * nchunks) * 32 + lane;
-#pragma unroll
-    for (int u = 0; u < kW4Unroll; ++u) {
-      const int c = c0 + u;
-      b[u] = c < c_end ? ld_stream(base + size_t(c) * 32) : make_uint4(0, 0, 0, 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunks_tile = k / CK;
+  const int S = stage_chunks(chunks_tile);  // chunks per stage
+  const int cpw = max(S / kConsumers, TF<FMT>::kMinChunksPerWarp);
+  const int active_warps = S / cpw;
+  const int ntiles = n / 16;
+  const int per_cta = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int tile_begin = blockIdx.x * per_cta;
+  const int tile_end = min(ntiles, tile_begin + per_cta);
+  const int stages_tile = chunks_tile / S;
+  const int total_stages = tile_end > tile_begin ? (tile_end - tile_begin) * stages_tile : 0;
+  const int stage_bytes = S * kChunkBytes;
+  const int xbytes = NT * (FMT == kINT8 ? k : 2 * k);
+  uint8_t* xs = smem;
+  uint8_t* ring = smem + ((xbytes + 127) & ~127);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], active_warps);
     }
-  };
-  if (tile < ntiles) load(tile, c_begin, cur);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumers) {
+    // producer: stream this CTA's contiguous weight range. Weights only, so it
+    // runs ahead of griddepcontrol.wait and fills the ring during the
+    // previous kernel.
+    if (lane == 0) {
+      const uint8_t* src = wtf + size_t(tile_begin) * chunks_tile * kChunkBytes;
+      for (int st = 0; st < total_stages; ++st) {
+        const int s = st % n_stages;
+        mbar_wait(&empty[s], ((st / n_stages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], stage_bytes);
+        bulk_g2s(ring + size_t(s) * stage_bytes, src + size_t(st) * stage_bytes, stage_bytes,
+                 &full[s]);
+      }
+    }
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
+
+  // consumers
   pdl_wait();
   pdl_trigger();
-  prologue<kW4, PRO, NT>(x, gamma, eps, k, T, smem, red, xscale);
-  const half* xs = reinterpret_cast<const half*>(smem);
+  prologue<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red, xscale);
+  const int g = lane >> 2, tq = lane & 3;
+  const bool has_tok = g < T;  // this lane's MMA column is a real token
+  const int groups_k = k / kW4Group;
   const half2 k1032 = __float2half2_rn(1032.0f);
-  const bool has_tok = g < NT && g < T;
 
-  for (; tile < ntiles; tile += gridDim.x) {
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    float cg[4] = {0.f, 0.f, 0.f, 0.f};
-    const half* s_lo = ws + size_t(tile * 16 + g) * groups_k;
-    const half* s_hi = ws + size_t(tile * 16 + g + 8) * groups_k;
-    for (int c0 = c_begin; c0 < c_end; c0 += kW4Unroll) {
-      uint4 nxt[kW4Unroll];
-      if (c0 + kW4Unroll < c_end) load(tile, c0 + kW4Unroll, nxt);
-      else if (tile + int(gridDim.x) < ntiles) load(tile + gridDim.x, c_begin, nxt);
+  Acc acc[4] = {0, 0, 0, 0};
+  float cg[4] = {0.f, 0.f, 0.f, 0.f};  // W4: current 128-k group
+  for (int st = 0; st < total_stages; ++st) {
+    const int s = st % n_stages;
+    const int tile = tile_begin + st / stages_tile;
+    const int c_tile0 = (st % stages_tile) * S;  // first chunk (within the tile) of the stage
+    mbar_wait(&full[s], (st / n_stages) & 1);
+    if (warp < active_warps) {
+      const uint4* stage = reinterpret_cast<const uint4*>(ring + size_t(s) * stage_bytes);
+#pragma unroll 2
+      for (int j = 0; j < cpw; ++j) {
+        const int c_local = warp * cpw + j;
+        const int c = c_tile0 + c_local;  // chunk index within the tile
+        const uint4 a4 = stage[c_local * 32 + lane];
+        if (FMT == kFP16) {
+          const int kk = c * 16 + 2 * tq;
+          uint32_t b0 = 0, b1 = 0;
+          if (has_tok) {
+            const half* xr = reinterpret_cast<const half*>(xs) + size_t(g) * k;
+            b0 = *reinterpret_cast<const uint32_t*>(xr + kk);
+            b1 = *reinterpret_cast<const uint32_t*>(xr + kk + 8);
+          }
+          const uint32_t a[4] = {a4.x, a4.y, a4.z, a4.w};
+          mma_f16(reinterpret_cast<float(&)[4]>(acc), a, b0, b1);
+        } else if (FMT == kINT8) {
+          const int kk = c * 32 + 4 * tq;
+          uint32_t b0 = 0, b1 = 0;
+          if (has_tok) {
+            const int8_t* xr = reinterpret_cast<const int8_t*>(xs) + size_t(g) * k;
+            b0 = *reinterpret_cast<const uint32_t*>(xr + kk);
+            b1 = *reinterpret_cast<const uint32_t*>(xr + kk + 16);
+          }
+          const uint32_t a[4] = {a4.x, a4.y, a4.z, a4.w};
+          mma_s8(reinterpret_cast<int(&)[4]>(acc), a, b0, b1);
+        } else {
+          const uint32_t wv[4] = {a4.x, a4.y, a4.z, a4.w};
+          const half* xr = reinterpret_cast<const half*>(xs) + size_t(g) * k;
 #pragma unroll
-      for (int u = 0; u < kW4Unroll; ++u) {
-        const int c = c0 + u;
-        if (c < c_end) {
-          const uint32_t wv[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int kk = c * 64 + j * 16 + 2 * tq;
+          for (int jj = 0; jj < 4; ++jj) {
+            const int kk = c * 64 + jj * 16 + 2 * tq;
             uint32_t b0 = 0, b1 = 0;
             if (has_tok) {
-              b0 = *reinterpret_cast<const uint32_t*>(xs + size_t(g) * k + kk);
-              b1 = *reinterpret_cast<const uint32_t*>(xs + size_t(g) * k + kk + 8);
+              b0 = *reinterpret_cast<const uint32_t*>(xr + kk);
+              b1 = *reinterpret_cast<const uint32_t*>(xr + kk + 8);
             }
             uint32_t a[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              a[i] = h22u(__hsub2(u2h2(lop3_and_or(wv[j] >> (4 * i), 0x000F000Fu, 0x64006400u)), k1032));
-            mma16816(cg, a, b0, b1);
+              a[i] = h22u(__hsub2(u2h2(lop3_and_or(wv[jj] >> (4 * i), 0x000F000Fu, 0x64006400u)),
+                                  k1032));
+            mma_f16(cg, a, b0, b1);
           }
-          if (c & 1) {  // end of a 128-k group: apply the fp32 group scale
+          if (c & 1) {  // end of a 128-k group: fp32 group scale per row
+            const half* sc = static_cast<const half*>(ws);
             const int grp = c >> 1;
-            const float slo = __half2float(s_lo[grp]), shi = __half2float(s_hi[grp]);
+            const float slo = __half2float(sc[size_t(tile * 16 + g) * groups_k + grp]);
+            const float shi = __half2float(sc[size_t(tile * 16 + g + 8) * groups_k + grp]);
             acc[0] = fmaf(slo, cg[0], acc[0]);
             acc[1] = fmaf(slo, cg[1], acc[1]);
             acc[2] = fmaf(shi, cg[2], acc[2]);
@@ -315,68 +299,123 @@ __global__ void __launch_bounds__(kThreads) gemv_w4_kernel(const uint4* __restri
           }
         }
       }
-#pragma unroll
-      for (int u = 0; u < kW4Unroll; ++u) cur[u] = nxt[u];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // cross-warp K reduction: lane holds (row g, cols 2tq, 2tq+1) and (row g+8, ...)
-    part[warp][g][2 * tq] = acc[0];
-    part[warp][g][2 * tq + 1] = acc[1];
-    part[warp][g + 8][2 * tq] = acc[2];
-    part[warp][g + 8][2 * tq + 1] = acc[3];
-    __syncthreads();
-    if (threadIdx.x < 128) {
-      const int row = threadIdx.x >> 3, col = threadIdx.x & 7;
-      float v = 0.f;
+    if ((st + 1) % stages_tile == 0) {
+      // tile complete: reduce the 16 x 8 partials of all warps, fused epilogue
+      uint32_t raw[4];
 #pragma unroll
-      for (int w2 = 0; w2 < kWarps; ++w2) v += part[w2][row][col];
-      const float v_next = __shfl_down_sync(0xffffffffu, v, 8);  // row + 1, same column
-      if ((row & 1) == 0 && col < T) store_out<EPI>(y, n, col, tile * 16 + row, v, v_next);
+      for (int i = 0; i < 4; ++i) {
+        if (FMT == kINT8) raw[i] = warp < active_warps ? uint32_t(int(acc[i])) : 0u;
+        else raw[i] = __float_as_uint(warp < active_warps ? float(acc[i]) : 0.0f);
+      }
+      part[warp][g][2 * tq] = raw[0];
+      part[warp][g][2 * tq + 1] = raw[1];
+      part[warp][g + 8][2 * tq] = raw[2];
+      part[warp][g + 8][2 * tq + 1] = raw[3];
+      named_sync(1, kConsThreads);
+      if (threadIdx.x < 128) {
+        const int row = threadIdx.x >> 3, col = threadIdx.x & 7;
+        float v;
+        if (FMT == kINT8) {
+          int iv = 0;  // exact int32 across warps
+#pragma unroll
+          for (int w2 = 0; w2 < kConsumers; ++w2) iv += int(part[w2][row][col]);
+          v = float(iv);
+        } else {
+          v = 0.f;
+#pragma unroll
+          for (int w2 = 0; w2 < kConsumers; ++w2) v += __uint_as_float(part[w2][row][col]);
+        }
+        const float vn = __shfl_down_sync(0xffffffffu, v, 8);  // row + 1, same column
+        if ((row & 1) == 0 && col < T) {
+          float v0 = v, v1 = vn;
+          if (FMT == kINT8) {
+            const float* sw = static_cast<const float*>(ws);
+            v0 = (v0 * xscale[col]) * sw[tile * 16 + row];
+            v1 = (v1 * xscale[col]) * sw[tile * 16 + row + 1];
+          }
+          store_pair<EPI>(y, n, col, tile * 16 + row, v0, v1);
+        }
+      }
+      named_sync(1, kConsThreads);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = 0;
     }
-    __syncthreads();
   }
 }
 
-// ------------------------------------------------------------- launchers
+// --------------------------------------------------------------- repacking
+// Row-major source -> tile-fragment layout. Source formats:
+//   FP16: half [n][k]; INT8: int8 [n][k]; W4: row-packed words [n][k/8]
+//   (nibble position (i>>1) + 4*(i&1) for element i of a word).
+__global__ void repack_tf_kernel(int fmt, const uint8_t* __restrict__ src, int n, int k,
+                                 uint8_t* __restrict__ dst) {
+  const int ck = fmt == kFP16 ? 16 : (fmt == kINT8 ? 32 : 64);
+  const int chunks_tile = k / ck;
+  const long long words = (long long)(n / 16) * chunks_tile * 32 * 4;  // 32-bit words
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < words;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int reg = int(i & 3);  // A fragment register a0..a3 (W4: k16 step)
+    const int lane = int((i >> 2) & 31);
+    const long long tc = i >> 7;
+    const int c = int(tc % chunks_tile);
+    const int tile = int(tc / chunks_tile);
+    const int g = lane >> 2, tq = lane & 3;
+    uint32_t word = 0;
+    if (fmt == kFP16) {
+      const int row = tile * 16 + g + ((reg & 1) ? 8 : 0);
+      const int kk = c * 16 + 2 * tq + ((reg & 2) ? 8 : 0);
+      word = *reinterpret_cast<const uint32_t*>(src + (size_t(row) * k + kk) * 2);
+    } else if (fmt == kINT8) {
+      const int row = tile * 16 + g + ((reg & 1) ? 8 : 0);
+      const int kk = c * 32 + 4 * tq + ((reg & 2) ? 16 : 0);
+      word = *reinterpret_cast<const uint32_t*>(src + size_t(row) * k + kk);
+    } else {
+      // element e of the k16 step: pair e>>1 -> a0..a3, e&1 -> first/second k
+      const uint32_t* sw = reinterpret_cast<const uint32_t*>(src);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int pr = e >> 1, hi = e & 1;
+        const int row = tile * 16 + g + ((pr & 1) ? 8 : 0);
+        const int kk = c * 64 + reg * 16 + 2 * tq + ((pr & 2) ? 8 : 0) + hi;
+        const uint32_t w = sw[size_t(row) * (k / 8) + kk / 8];
+        const int si = kk & 7;
+        const uint32_t q = (w >> (4 * ((si >> 1) + 4 * (si & 1)))) & 0xF;
+        word |= q << (4 * ((e >> 1) + 4 * (e & 1)));
+      }
+    }
+    reinterpret_cast<uint32_t*>(dst)[i] = word;
+  }
+}
+
 template <int FMT, int PRO, int EPI, int NT>
-void launch_cc(const LinearW& W, const float* x, int T, const half* gamma, float eps, float* y,
+void launch_tf(const LinearW& W, const float* x, int T, const half* gamma, float eps, float* y,
                cudaStream_t st) {
-  const int npairs = W.n / 2;
-  const int grid = std::max(1, std::min(ceil_div(npairs, kWarps), kNumSMs * kCtasPerSm));
-  const size_t smem = size_t(NT) * (FMT == kINT8 ? size_t(W.k) : size_t(W.k) * 2);
+  const int ntiles = W.n / 16;
+  const int grid = std::max(1, std::min(ntiles, kNumSMs));
+  const int chunks_tile = W.k / TF<FMT>::kChunkK;
+  const int stage_bytes = stage_chunks(chunks_tile) * kChunkBytes;
+  const size_t xbytes = (size_t(NT) * (FMT == kINT8 ? W.k : 2 * W.k) + 127) & ~size_t(127);
+  int stages = int((kSmemBudget - std::min<size_t>(xbytes, kSmemBudget - 2 * stage_bytes)) / stage_bytes);
+  stages = std::max(2, std::min(kMaxStages, stages));
+  const size_t smem = xbytes + size_t(stages) * stage_bytes;
   static bool attr_done = false;
   if (!attr_done) {
-    MSW_CUDA(cudaFuncSetAttribute(gemv_cc_kernel<FMT, PRO, EPI, NT>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    MSW_CUDA(cudaFuncSetAttribute(gemv_tf_kernel<FMT, PRO, EPI, NT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_done = true;
   }
-  launch_pdl(gemv_cc_kernel<FMT, PRO, EPI, NT>, dim3(grid), dim3(kThreads), smem, st,
-             static_cast<const uint8_t*>(W.w), W.s, W.n, W.k, x, T, gamma, eps, y);
-}
-
-template <int PRO, int EPI, int NT>
-void launch_w4(const LinearW& W, const float* x, int T, const half* gamma, float eps, float* y,
-               cudaStream_t st) {
-  const int grid = std::max(1, std::min(W.n / 16, kNumSMs * kCtasPerSm));
-  const size_t smem = size_t(NT) * size_t(W.k) * 2;
-  static bool attr_done = false;
-  if (!attr_done) {
-    MSW_CUDA(cudaFuncSetAttribute(gemv_w4_kernel<PRO, EPI, NT>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_done = true;
-  }
-  launch_pdl(gemv_w4_kernel<PRO, EPI, NT>, dim3(grid), dim3(kThreads), smem, st,
-             static_cast<const uint4*>(W.w_mma), static_cast<const half*>(W.s), W.n, W.k, x, T,
-             gamma, eps, y);
+  launch_pdl(gemv_tf_kernel<FMT, PRO, EPI, NT>, dim3(grid), dim3(kThreads), smem, st,
+             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages);
 }
 
 template <int FMT, int NT>
 void dispatch_nt(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
                  float eps, float* y, cudaStream_t st) {
-#define MSW_GEMV_CASE(P, E)                                                  \
-  if (pro == P && epi == E) {                                                \
-    if (FMT == kW4) return launch_w4<P, E, NT>(W, x, T, gamma, eps, y, st);  \
-    return launch_cc<FMT == kW4 ? kFP16 : FMT, P, E, NT>(W, x, T, gamma, eps, y, st); \
-  }
+#define MSW_GEMV_CASE(P, E) \
+  if (pro == P && epi == E) return launch_tf<FMT, P, E, NT>(W, x, T, gamma, eps, y, st);
   MSW_GEMV_CASE(kProPlain, kEpiStore)
   MSW_GEMV_CASE(kProPlain, kEpiResid)
   MSW_GEMV_CASE(kProPlain, kEpiSwiglu)
@@ -399,7 +438,7 @@ void dispatch_fmt(const LinearW& W, int pro, int epi, const float* x, int T, con
 __global__ void gemv_i8_acc_kernel(const int8_t* __restrict__ w, const int8_t* __restrict__ x,
                                    int n, int k, int* __restrict__ acc) {
   const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= n) return;
   const int nch = k / 16;
   int a = 0;
@@ -415,59 +454,35 @@ __global__ void gemv_i8_acc_kernel(const int8_t* __restrict__ w, const int8_t* _
   if (lane == 0) acc[row] = a;
 }
 
-// row-packed W4 ([n][k/8] words, nibble position (i>>1)+4(i&1)) -> mma4 layout
-__global__ void repack_w4_mma_kernel(const uint32_t* __restrict__ src, int n, int k,
-                                     uint32_t* __restrict__ dst) {
-  const int nchunks = k / 64;
-  const long long total = (long long)(n / 16) * nchunks * 32 * 4;  // words
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int j = int(i & 3);
-    const int lane = int((i >> 2) & 31);
-    const long long tc = i >> 7;
-    const int c = int(tc % nchunks);
-    const int tile = int(tc / nchunks);
-    const int g = lane >> 2, tq = lane & 3;
-    uint32_t word = 0;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {  // element e of the A fragment
-      const int pair = e >> 1, hi = e & 1;
-      const int row = tile * 16 + g + ((pair & 1) ? 8 : 0);
-      const int kk = c * 64 + j * 16 + 2 * tq + ((pair & 2) ? 8 : 0) + hi;
-      const uint32_t sw = src[size_t(row) * (k / 8) + kk / 8];
-      const int si = kk & 7;
-      const uint32_t q = (sw >> (4 * ((si >> 1) + 4 * (si & 1)))) & 0xF;
-      word |= q << (4 * ((e >> 1) + 4 * (e & 1)));
-    }
-    dst[i] = word;
-  }
-}
-
 }  // namespace
 
 void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
                  float eps, float* y, cudaStream_t st) {
   if (W.n % 16 != 0 || W.k % 128 != 0) throw ConfigErr("gemv: n % 16, k % 128 required");
   if (T < 1 || T > kGemvMaxTokens) throw ConfigErr("gemv: 1..6 tokens");
+  if (!W.w_tf) throw ConfigErr("gemv: decode (tile-fragment) weight layout missing");
   switch (W.fmt) {
     case kFP16: return dispatch_fmt<kFP16>(W, pro, epi, x, T, gamma, eps, y, st);
     case kINT8: return dispatch_fmt<kINT8>(W, pro, epi, x, T, gamma, eps, y, st);
-    case kW4:
-      if (!W.w_mma) throw ConfigErr("gemv: W4 needs the mma4 layout");
-      return dispatch_fmt<kW4>(W, pro, epi, x, T, gamma, eps, y, st);
+    case kW4: return dispatch_fmt<kW4>(W, pro, epi, x, T, gamma, eps, y, st);
     default: throw ConfigErr("gemv: bad weight format");
   }
 }
 
-void launch_repack_w4_mma(const uint32_t* packed, int n, int k, uint32_t* mma4, cudaStream_t st) {
-  if (n % 16 || k % 128) throw ConfigErr("repack_w4: n % 16, k % 128 required");
-  repack_w4_mma_kernel<<<kNumSMs * 8, 256, 0, st>>>(packed, n, k, mma4);
+size_t tf_bytes(int fmt, int n, int k) {
+  return fmt == kFP16 ? size_t(n) * k * 2 : (fmt == kINT8 ? size_t(n) * k : size_t(n) * k / 2);
+}
+
+void launch_repack_tf(int fmt, const void* src, int n, int k, void* dst, cudaStream_t st) {
+  if (n % 16 || k % 128) throw ConfigErr("repack_tf: n % 16, k % 128 required");
+  repack_tf_kernel<<<kNumSMs * 8, 256, 0, st>>>(fmt, static_cast<const uint8_t*>(src), n, k,
+                                                static_cast<uint8_t*>(dst));
   MSW_LAUNCH_CHECK();
 }
 
 void launch_gemv_i8_acc(const int8_t* w, const int8_t* x, int n, int k, int* acc, cudaStream_t st) {
   if (k % 16 != 0) throw ConfigErr("gemv_i8_acc: k must be a multiple of 16");
-  gemv_i8_acc_kernel<<<ceil_div(n, kWarps), kThreads, 0, st>>>(w, x, n, k, acc);
+  gemv_i8_acc_kernel<<<ceil_div(n, 8), 256, 0, st>>>(w, x, n, k, acc);
   MSW_LAUNCH_CHECK();
 }
 

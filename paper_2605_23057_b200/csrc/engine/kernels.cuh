@@ -17,7 +17,7 @@ struct LinearW {
   int n = 0, k = 0;
   const void* w = nullptr;
   const void* s = nullptr;
-  const void* w_mma = nullptr;  // kW4 only: the same weights in mma.sync fragment order (decode)
+  const void* w_tf = nullptr;  // the same weights in tile-fragment order (decode GEMV)
   size_t bytes() const {
     const size_t nk = size_t(n) * size_t(k);
     if (fmt == kFP16) return nk * 2;
@@ -50,8 +50,10 @@ constexpr int kGemvMaxTokens = 6;
 void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
                  float eps, float* y, cudaStream_t st);
 void launch_gemv_i8_acc(const int8_t* w, const int8_t* x, int n, int k, int* acc, cudaStream_t st);
-// row-packed W4 -> mma.sync fragment order used by the decode GEMV
-void launch_repack_w4_mma(const uint32_t* packed, int n, int k, uint32_t* mma4, cudaStream_t st);
+// row-major weights (FP16 half / INT8 int8 / W4 row-packed words) -> the
+// tile-fragment layout the decode GEMV streams (same byte count)
+size_t tf_bytes(int fmt, int n, int k);
+void launch_repack_tf(int fmt, const void* src, int n, int k, void* dst, cudaStream_t st);
 
 // ---- gemm.cu: T > 1 tokens (prefill / verify / continuous batching) -----------
 // prep: per token row, optional RMSNorm, then fp16 rounding (xh) or int8
@@ -87,7 +89,7 @@ void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
 void launch_attention_decode(const float* qkv, const float* inv_freq, int T, const int* pos,
                              const int* slot, const int* seq_of, const int* block_table, half* kc,
                              half* vc, const AttnShape& a, int nsplit, float* part_o,
-                             float* part_ml, float* o, cudaStream_t st);
+                             float* part_ml, int* counters, float* o, cudaStream_t st);
 
 // ---- misc.cu ------------------------------------------------------------------
 void launch_embed(const half* emb, const int* tok, int T, int H, float* h, cudaStream_t st);

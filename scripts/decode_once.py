@@ -16,12 +16,15 @@ ap.add_argument("--prompt", type=int, default=128)
 ap.add_argument("--new", type=int, default=4)
 ap.add_argument("--target", default="llama8b")
 ap.add_argument("--graphs", type=int, default=1)
+ap.add_argument("--reps", type=int, default=1)
 a = ap.parse_args()
 modes = [a.mode] if a.mode != 4 else [0, 4]
 eng = Engine(engine_cfg(target=a.target, draft="llama1b" if a.mode == 4 else None, modes=modes,
                         kv_blocks=128, max_seq_len=a.prompt + a.new + 32, use_graphs=bool(a.graphs)))
 p = np.random.default_rng(0).integers(0, eng.vocab, size=a.prompt).astype(np.int32)
-r = eng.run(a.mode, p, a.new)
-print("tokens", r.tokens[:8], "decode_ms", r.decode_ms, "prefill_ms", r.prefill_ms,
-      "launches", r.kernel_launches)
+for rep in range(a.reps):
+    r = eng.run(a.mode, p, a.new)
+    print("tokens", r.tokens[:4], "decode_ms", round(r.decode_ms, 3), "per_token_ms",
+          round(r.decode_ms / max(1, a.new - 1), 4), "prefill_ms", round(r.prefill_ms, 3),
+          "launches", r.kernel_launches, flush=True)
 eng.close()
