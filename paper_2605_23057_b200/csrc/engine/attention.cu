@@ -16,8 +16,19 @@ __device__ __forceinline__ size_t kv_off(int slot, int hk, int Hk, int D) {
   return ((size_t(slot >> 4) * Hk + hk) * kKvBlock + (slot & 15)) * size_t(D);
 }
 
+__global__ void rope_table_kernel(const float* __restrict__ inv_freq, int half_d, int max_pos,
+                                  float2* __restrict__ table) {
+  const int total = max_pos * half_d;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int p = i / half_d, j = i % half_d;
+    float sn, cs;
+    sincosf(float(p) * inv_freq[j], &sn, &cs);  // fp32 angle, as the oracle
+    table[i] = make_float2(cs, sn);
+  }
+}
+
 __global__ void rope_append_kernel(const float* __restrict__ qkv, const int* __restrict__ pos,
-                                   const int* __restrict__ slot, const float* __restrict__ inv_freq,
+                                   const int* __restrict__ slot, const float2* __restrict__ rope,
                                    int Hq, int Hk, int D, half* __restrict__ q_out,
                                    half* __restrict__ kc, half* __restrict__ vc) {
   pdl_wait();
@@ -26,12 +37,12 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, const int* __r
   const int half_d = D / 2;
   const int width = (Hq + 2 * Hk) * D;
   const float* row = qkv + size_t(t) * width;
-  const float p = float(pos[t]);
+  const int pi = pos[t];
   const int s = slot[t];
   for (int i = threadIdx.x; i < (Hq + Hk) * half_d; i += blockDim.x) {
     const int h = i / half_d, j = i % half_d;
-    float sn, cs;
-    sincosf(p * inv_freq[j], &sn, &cs);
+    const float2 r = rope[size_t(pi) * half_d + j];
+    const float cs = r.x, sn = r.y;
     const float x0 = row[h * D + j], x1 = row[h * D + j + half_d];
     const float y0 = __fsub_rn(__fmul_rn(x0, cs), __fmul_rn(x1, sn));
     const float y1 = __fadd_rn(__fmul_rn(x1, cs), __fmul_rn(x0, sn));
@@ -270,29 +281,28 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 //  * splits are merged in-kernel: every split writes (m, l, acc) partials and
 //    the last CTA to finish (atomic counter) combines them, so there is no
 //    separate combine launch.
-template <int D>
-struct VSlice;
-template <>
-struct VSlice<128> {
-  using T = uint2;  // 4 halves per lane
-};
-template <>
-struct VSlice<64> {
-  using T = uint32_t;  // 2 halves per lane
-};
+constexpr int kKvPad = 8;  // halves of padding per staged K/V row (bank-conflict free LDS.128)
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
 
 template <int D, int G>
 __global__ void __launch_bounds__(kAttnWarps * 32)
-    attn_decode_kernel(const float* __restrict__ qkv, const float* __restrict__ inv_freq,
+    attn_decode_kernel(const float* __restrict__ qkv, const float2* __restrict__ rope,
                        const int* __restrict__ pos, const int* __restrict__ slot,
                        const int* __restrict__ seq_of, const int* __restrict__ block_table,
                        int max_blocks, half* __restrict__ kc, half* __restrict__ vc, int Hq, int Hk,
                        int nsplit, float* __restrict__ part_o, float* __restrict__ part_ml,
                        int* __restrict__ counters, float* __restrict__ o) {
   constexpr int DPL = D / 32;
-  constexpr int KC = D / 8;
-  using VT = typename VSlice<D>::T;
-  __shared__ float qs[G][D];
+  constexpr int RS = D + kKvPad;  // staged row stride (halves)
+  extern __shared__ __align__(16) half kv_smem[];  // [warp][K|V][32][RS]
+  __shared__ __align__(16) float qs[G][D];
   __shared__ float knew[D], vnew[D];
   __shared__ float wm[kAttnWarps][G], wl[kAttnWarps][G];
   __shared__ float wacc[kAttnWarps][G][D];
@@ -311,40 +321,37 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   const int end = min(ctx, begin + chunk);
   const int active = (ctx + chunk - 1) / chunk;
   const int* bt = block_table + size_t(seq_of[t]) * max_blocks;
+  half* sK = kv_smem + size_t(warp) * 2 * 32 * RS;
+  half* sV = sK + 32 * RS;
 
-  uint4 kreg[KC];
-  VT vreg[32];
-  auto load_tile = [&](int base) {
+  // stage one 32-position tile of K and V rows (lane = position) into smem
+  auto stage_tile = [&](int base) {
     const int p = base + lane;
     if (p < end && p != p_self) {
       const int sl = bt[p >> 4] * kKvBlock + (p & 15);
-      const uint4* kr = reinterpret_cast<const uint4*>(kc + kv_off(sl, hk, Hk, D));
+      const half* kr = kc + kv_off(sl, hk, Hk, D);
+      const half* vr = vc + kv_off(sl, hk, Hk, D);
 #pragma unroll
-      for (int c = 0; c < KC; ++c) kreg[c] = kr[c];
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int pj = base + j;
-      if (pj < end && pj != p_self) {
-        const int sl = bt[pj >> 4] * kKvBlock + (pj & 15);
-        vreg[j] = *reinterpret_cast<const VT*>(vc + kv_off(sl, hk, Hk, D) + lane * DPL);
+      for (int c = 0; c < D / 8; ++c) {
+        cp_async16(sK + lane * RS + c * 8, kr + c * 8);
+        cp_async16(sV + lane * RS + c * 8, vr + c * 8);
       }
     }
   };
   const int first = begin + warp * 32;
-  if (first < end) load_tile(first);  // history only: safe before the wait
+  if (first < end) stage_tile(first);  // cache history only: safe before the wait
 
   pdl_wait();
   pdl_trigger();
   {
     const int width = (Hq + 2 * Hk) * D;
     const float* row = qkv + size_t(t) * width;
-    const float pf = float(p_self);
+    const float2* rp = rope + size_t(p_self) * (D / 2);
     for (int i = threadIdx.x; i < (G + 1) * (D / 2); i += blockDim.x) {
       const int h = i / (D / 2), j = i % (D / 2);
       const float* src = h < G ? row + size_t(hk * G + h) * D : row + size_t(Hq + hk) * D;
-      float sn, cs;
-      sincosf(pf * inv_freq[j], &sn, &cs);
+      const float2 r = rp[j];
+      const float cs = r.x, sn = r.y;
       const float x0 = src[j], x1 = src[j + D / 2];
       const float y0 = __half2float(__float2half_rn(__fsub_rn(__fmul_rn(x0, cs), __fmul_rn(x1, sn))));
       const float y1 = __half2float(__float2half_rn(__fadd_rn(__fmul_rn(x1, cs), __fmul_rn(x0, sn))));
@@ -377,27 +384,34 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     for (int d = 0; d < DPL; ++d) acc[g][d] = 0.0f;
   }
   for (int base = first; base < end; base += kAttnWarps * 32) {
-    if (base != first) load_tile(base);
+    if (base != first) {
+      __syncwarp();
+      stage_tile(base);
+    }
+    cp_async_wait_all();
+    __syncwarp();
     const int p = base + lane;
     float s[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) s[g] = 0.0f;
     if (p < end) {
       if (p == p_self) {
-        for (int d = 0; d < D; ++d) {
+#pragma unroll 4
+        for (int d = 0; d < D; ++d)
 #pragma unroll
           for (int g = 0; g < G; ++g) s[g] = fmaf(qs[g][d], knew[d], s[g]);
-        }
       } else {
-#pragma unroll
-        for (int c = 0; c < KC; ++c) {
-          const half2* kh = reinterpret_cast<const half2*>(&kreg[c]);
+        const half* kr = sK + lane * RS;
+#pragma unroll 2
+        for (int c = 0; c < D / 8; ++c) {
+          const uint4 kv = *reinterpret_cast<const uint4*>(kr + c * 8);
+          const half2* kh = reinterpret_cast<const half2*>(&kv);
+          const float2 k0 = __half22float2(kh[0]), k1 = __half22float2(kh[1]);
+          const float2 k2 = __half22float2(kh[2]), k3 = __half22float2(kh[3]);
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const float4 q0 = *reinterpret_cast<const float4*>(&qs[g][c * 8]);
             const float4 q1 = *reinterpret_cast<const float4*>(&qs[g][c * 8 + 4]);
-            const float2 k0 = __half22float2(kh[0]), k1 = __half22float2(kh[1]);
-            const float2 k2 = __half22float2(kh[2]), k3 = __half22float2(kh[3]);
             s[g] = fmaf(q0.x, k0.x, fmaf(q0.y, k0.y, fmaf(q0.z, k1.x, fmaf(q0.w, k1.y, s[g]))));
             s[g] = fmaf(q1.x, k2.x, fmaf(q1.y, k2.y, fmaf(q1.z, k3.x, fmaf(q1.w, k3.y, s[g]))));
           }
@@ -417,29 +431,26 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
     }
     const int n_here = min(32, end - base);
+#pragma unroll 2
+    for (int j = 0; j < n_here; ++j) {
+      float vf[DPL];
+      if (base + j == p_self) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j < n_here) {
-        const int pj = base + j;
-        float vf[DPL];
-        if (pj == p_self) {
+        for (int d = 0; d < DPL; ++d) vf[d] = vnew[lane * DPL + d];
+      } else {
+        const half2* vh = reinterpret_cast<const half2*>(sV + j * RS + lane * DPL);
 #pragma unroll
-          for (int d = 0; d < DPL; ++d) vf[d] = vnew[lane * DPL + d];
-        } else {
-          const half2* vh = reinterpret_cast<const half2*>(&vreg[j]);
-#pragma unroll
-          for (int d = 0; d < DPL / 2; ++d) {
-            const float2 f = __half22float2(vh[d]);
-            vf[2 * d] = f.x;
-            vf[2 * d + 1] = f.y;
-          }
+        for (int d = 0; d < DPL / 2; ++d) {
+          const float2 f = __half22float2(vh[d]);
+          vf[2 * d] = f.x;
+          vf[2 * d + 1] = f.y;
         }
+      }
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float w = __shfl_sync(0xffffffffu, e[g], j);
+      for (int g = 0; g < G; ++g) {
+        const float w = __shfl_sync(0xffffffffu, e[g], j);
 #pragma unroll
-          for (int d = 0; d < DPL; ++d) acc[g][d] = fmaf(w, vf[d], acc[g][d]);
-        }
+        for (int d = 0; d < DPL; ++d) acc[g][d] = fmaf(w, vf[d], acc[g][d]);
       }
     }
   }
@@ -478,13 +489,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     }
   }
   if (active == 1) return;
-  // last split to finish merges all partials of this (token, kv head)
+  // the last split to finish merges all partials of this (token, kv head)
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const int done = atomicAdd(&counters[t * Hk + hk], 1);
     is_last = done == active - 1;
-    if (is_last) counters[t * Hk + hk] = 0;  // reset for the next step
+    if (is_last) counters[t * Hk + hk] = 0;  // self-reset for the next step
   }
   __syncthreads();
   if (!is_last) return;
@@ -577,10 +588,16 @@ void attention_any(const half* q, const float* qkv, const float* inv_freq, int T
 
 }  // namespace
 
+void launch_rope_table(const float* inv_freq, int head_dim, int max_pos, float2* table,
+                       cudaStream_t st) {
+  rope_table_kernel<<<kNumSMs * 4, 256, 0, st>>>(inv_freq, head_dim / 2, max_pos, table);
+  MSW_LAUNCH_CHECK();
+}
+
 void launch_rope_append(const float* qkv, int T, const int* pos, const int* slot,
-                        const float* inv_freq, const AttnShape& a, half* q_out, half* kc, half* vc,
+                        const float2* rope, const AttnShape& a, half* q_out, half* kc, half* vc,
                         cudaStream_t st) {
-  launch_pdl(rope_append_kernel, dim3(T), dim3(256), 0, st, qkv, pos, slot, inv_freq, a.n_heads,
+  launch_pdl(rope_append_kernel, dim3(T), dim3(256), 0, st, qkv, pos, slot, rope, a.n_heads,
              a.n_kv_heads, a.head_dim, q_out, kc, vc);
 }
 
@@ -592,17 +609,25 @@ void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
                        st);
 }
 
-void launch_attention_decode(const float* qkv, const float* inv_freq, int T, const int* pos,
+void launch_attention_decode(const float* qkv, const float2* rope, int T, const int* pos,
                              const int* slot, const int* seq_of, const int* block_table, half* kc,
                              half* vc, const AttnShape& a, int nsplit, float* part_o,
                              float* part_ml, int* counters, float* o, cudaStream_t st) {
   const int G = a.n_heads / a.n_kv_heads;
   const dim3 grid(T, a.n_kv_heads, nsplit), thr(kAttnWarps * 32);
 #define MSW_DEC(DD, GG)                                                                       \
-  if (a.head_dim == DD && G == GG)                                                            \
-    return launch_pdl(attn_decode_kernel<DD, GG>, grid, thr, 0, st, qkv, inv_freq, pos, slot, \
-                      seq_of, block_table, a.max_blocks_per_seq, kc, vc, a.n_heads,           \
-                      a.n_kv_heads, nsplit, part_o, part_ml, counters, o);
+  if (a.head_dim == DD && G == GG) {                                                          \
+    const size_t smem = size_t(kAttnWarps) * 2 * 32 * (DD + kKvPad) * sizeof(half);           \
+    static bool attr = false;                                                                 \
+    if (!attr) {                                                                              \
+      MSW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<DD, GG>,                               \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
+      attr = true;                                                                            \
+    }                                                                                         \
+    return launch_pdl(attn_decode_kernel<DD, GG>, grid, thr, smem, st, qkv, rope, pos,        \
+                      slot, seq_of, block_table, a.max_blocks_per_seq, kc, vc, a.n_heads,     \
+                      a.n_kv_heads, nsplit, part_o, part_ml, counters, o);                    \
+  }
   MSW_DEC(128, 1)
   MSW_DEC(128, 2)
   MSW_DEC(128, 4)

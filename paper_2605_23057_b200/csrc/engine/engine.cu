@@ -155,6 +155,7 @@ struct Model {
   half* lm_head_tf = nullptr;  // decode (tile-fragment) copy
   half* final_norm = nullptr;
   float* inv_freq = nullptr;
+  float2* rope = nullptr;  // [max_seq_len + 64][head_dim/2] (cos, sin)
   std::vector<Layer> layers;
   half* kc = nullptr;
   half* vc = nullptr;
@@ -372,6 +373,8 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
   }
   m.inv_freq = model_alloc<float>(m, D / 2);
   MSW_CUDA(cudaMemcpy(m.inv_freq, inv.data(), sizeof(float) * inv.size(), cudaMemcpyHostToDevice));
+  m.rope = model_alloc<float2>(m, size_t(cfg.max_seq_len + 64) * (D / 2));
+  launch_rope_table(m.inv_freq, D, cfg.max_seq_len + 64, m.rope, st);
 
   // paged KV pool
   m.nblk = cfg.kv_blocks;
@@ -476,11 +479,11 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       n += 2;
     }
     if (tokens_independent) {  // decode / CB: RoPE + KV append fused into attention
-      launch_attention_decode(s.qkv, m.inv_freq, T, s.pos, s.slot, s.seq_of, m.block_table, kc,
+      launch_attention_decode(s.qkv, m.rope, T, s.pos, s.slot, s.seq_of, m.block_table, kc,
                               vc, m.ash, nsplit, s.part_o, s.part_ml, s.split_cnt, s.o, st);
       n += 1;
     } else {
-      launch_rope_append(s.qkv, T, s.pos, s.slot, m.inv_freq, m.ash, s.q16, kc, vc, st);
+      launch_rope_append(s.qkv, T, s.pos, s.slot, m.rope, m.ash, s.q16, kc, vc, st);
       launch_attention(s.q16, T, s.pos, s.seq_of, m.block_table, kc, vc, m.ash, nsplit, s.part_o,
                        s.part_ml, s.o, st);
       n += nsplit > 1 ? 3 : 2;

@@ -6,8 +6,12 @@
 // chunks, a chunk being one 16-byte mma.sync A fragment per lane:
 //   FP16 : m16n8k16 f16 -> f32, chunk = 16 rows x 16 k
 //   INT8 : m16n8k32 s8 -> s32 (exact), chunk = 16 rows x 32 k
-//   W4   : m16n8k16 f16 on lop3/hsub2-dequantised (q-8), chunk = 16 rows x 64 k
-//          (4 k16 steps), group scale applied in fp32 per 128 k
+//   W4   : m16n8k16 f16, chunk = 16 rows x 64 k (4 k16 steps). Dequant is ONE
+//          lop3 per fp16 pair and no subtraction: even k16 steps feed (1024 + q)
+//          against x, odd steps feed (1024 + 16 q) against x/16 (so one shift
+//          serves four lop3s); the per-group offset 1032*Sx_even + 72*Sx_odd
+//          (activation sums from the prologue) is removed in fp32 before the
+//          group scale: sum_k (q-8) x = D_even + D_odd - C_group.
 // The 8 MMA columns carry up to 8 tokens (verify / tiny batches) at no cost.
 //
 // Per CTA (persistent, one per SM, a contiguous tile range): a producer warp
@@ -22,12 +26,12 @@
 namespace msw {
 namespace {
 
-constexpr int kConsumers = 8;
-constexpr int kThreads = (kConsumers + 1) * 32;  // + producer warp
+constexpr int kConsumers = 16;
+constexpr int kThreads = (kConsumers + 2) * 32;  // + producer warp + epilogue warp
 constexpr int kConsThreads = kConsumers * 32;
 constexpr int kChunkBytes = 512;
 constexpr int kMaxStages = 8;
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 190 * 1024;
 
 __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -60,13 +64,6 @@ struct TF {
   static constexpr int kMinChunksPerWarp = FMT == kW4 ? 2 : 1;  // a W4 scale group is 2 chunks
 };
 
-// Stage size in chunks: the largest power of two <= 32 dividing a tile's chunks.
-__host__ __device__ inline int stage_chunks(int chunks_per_tile) {
-  int s = 32;
-  while (s > 1 && chunks_per_tile % s) s >>= 1;
-  return s;
-}
-
 // Consumer-only block reductions (named barrier 1 over the consumer warps).
 __device__ __forceinline__ float cons_sum(float v, float* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -87,6 +84,19 @@ __device__ __forceinline__ float cons_max(float v, float* red) {
   return warp_max(t);
 }
 
+// Activations are stored permuted so that lane (g, tq) fetches both B-fragment
+// registers of an MMA with one 8-byte LDS:
+//   fp16, per 16-k block: [0,1,8,9 | 2,3,10,11 | 4,5,12,13 | 6,7,14,15]
+//   int8, per 32-k block: [0..3,16..19 | 4..7,20..23 | 8..11,24..27 | 12..15,28..31]
+__device__ __forceinline__ int perm_f16(int k) {  // pairs (k, k+1), k even, stay adjacent
+  const int w = k & 15;
+  return (k & ~15) + ((w & 7) >> 1) * 4 + (w >> 3) * 2 + (w & 1);
+}
+__device__ __forceinline__ int perm_i8(int k) {  // quads (k..k+3), k % 4 == 0, stay adjacent
+  const int w = k & 31;
+  return (k & ~31) + ((w & 15) >> 2) * 8 + (w >> 4) * 4 + (w & 3);
+}
+
 // x fp32 [T, k] -> smem: fp16 [NT][k] (FP16 / W4) or int8 [NT][k] + scale.
 template <int FMT, int PRO, int NT>
 __device__ __forceinline__ void prologue(const float* __restrict__ x, const half* __restrict__ gamma,
@@ -95,7 +105,7 @@ __device__ __forceinline__ void prologue(const float* __restrict__ x, const half
   const int tid = threadIdx.x;
   for (int t = 0; t < NT; ++t) {
     const int bytes = FMT == kINT8 ? k : 2 * k;
-    if (t >= T) {
+    if (t >= T) {  // padding token columns: never stored, but keep them finite
       for (int i = tid; i < bytes / 16; i += kConsThreads)
         reinterpret_cast<uint4*>(xs + size_t(t) * bytes)[i] = make_uint4(0, 0, 0, 0);
       if (tid == 0) xscale[t] = 0.0f;
@@ -133,22 +143,51 @@ __device__ __forceinline__ void prologue(const float* __restrict__ x, const half
       }
       amax = cons_max(amax, red);
       const float s = amax / 127.0f;
-      char4* xq = reinterpret_cast<char4*>(xs + size_t(t) * k);
-      auto q = [&](float v) -> signed char {
+      int8_t* xq = reinterpret_cast<int8_t*>(xs + size_t(t) * k);
+      auto q = [&](float v) -> int8_t {
         const float u = amax > 0.0f ? rintf(v / s) : 0.0f;
-        return static_cast<signed char>(fminf(fmaxf(u, -127.0f), 127.0f));
+        return static_cast<int8_t>(fminf(fmaxf(u, -127.0f), 127.0f));
       };
       for (int i = tid; i < k4; i += kConsThreads) {
         const float4 v = act4(i);
-        xq[i] = make_char4(q(v.x), q(v.y), q(v.z), q(v.w));
+        // 4 consecutive k stay together: one char4 at its permuted slot
+        *reinterpret_cast<char4*>(xq + perm_i8(4 * i)) = make_char4(q(v.x), q(v.y), q(v.z), q(v.w));
       }
       if (tid == 0) xscale[t] = s;
     } else {
-      half2* xh = reinterpret_cast<half2*>(xs + size_t(t) * 2 * k);
+      half* xh = reinterpret_cast<half*>(xs + size_t(t) * 2 * k);
+      half* xh16 = reinterpret_cast<half*>(xs + size_t(NT) * 2 * k + size_t(t) * 2 * k);
       for (int i = tid; i < k4; i += kConsThreads) {
         const float4 v = act4(i);
-        xh[2 * i] = __floats2half2_rn(v.x, v.y);
-        xh[2 * i + 1] = __floats2half2_rn(v.z, v.w);
+        const half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
+        // pairs (k, k+1) stay together at their permuted slot
+        *reinterpret_cast<half2*>(xh + perm_f16(4 * i)) = lo;
+        *reinterpret_cast<half2*>(xh + perm_f16(4 * i + 2)) = hi;
+        if (FMT == kW4) {  // x/16 copy (exact power-of-two scaling) for the odd k16 steps
+          *reinterpret_cast<half2*>(xh16 + perm_f16(4 * i)) = __hmul2(lo, __float2half2_rn(0.0625f));
+          *reinterpret_cast<half2*>(xh16 + perm_f16(4 * i + 2)) = __hmul2(hi, __float2half2_rn(0.0625f));
+        }
+      }
+      if (FMT == kW4) {
+        named_sync(1, kConsThreads);
+        // per-group offsets C = 1032 * sum(x | even k16 steps) + 72 * sum(x | odd k16 steps)
+        const int groups = k / kW4Group;
+        float* corr = reinterpret_cast<float*>(xs + size_t(NT) * 4 * k) + size_t(t) * groups;
+        const int lane = tid & 31, warp = tid >> 5;
+        for (int grp = warp; grp < groups; grp += kConsumers) {
+          double se = 0.0, so = 0.0;
+          for (int i = lane; i < kW4Group; i += 32) {
+            const double v = __half2float(xh[perm_f16(grp * kW4Group + i)]);
+            if ((i & 31) < 16) se += v;
+            else so += v;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            se += __shfl_xor_sync(0xffffffffu, se, o);
+            so += __shfl_xor_sync(0xffffffffu, so, o);
+          }
+          if (lane == 0) corr[grp] = float(1032.0 * se + 72.0 * so);
+        }
       }
     }
     named_sync(1, kConsThreads);
@@ -168,60 +207,143 @@ __device__ __forceinline__ void store_pair(float* y, int n, int t, int row, floa
   }
 }
 
-template <int FMT, int PRO, int EPI, int NT>
+// Warp roles (one CTA per SM, a contiguous range of 16-row tiles):
+//   warps 0..kConsumers-1 : consumers. Every contiguous 16 KB ring stage holds
+//                           S chunks of one tile; warp w takes CPW of them.
+//                           At a tile end each warp red.shared-adds its 16 x 8
+//                           partial into one of two tile accumulators and
+//                           arrives on that buffer's mbarrier (no CTA barrier).
+//   warp kConsumers       : producer (cp.async.bulk ring, ahead of the PDL wait)
+//   warp kConsumers + 1   : epilogue: waits for a tile's accumulator, applies
+//                           the scales / SwiGLU / residual store, zeroes the
+//                           buffer and hands it back.
+template <int FMT, int PRO, int EPI, int NT, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_tf_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
                    const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
                    float* __restrict__ y, int n_stages) {
   using Acc = typename std::conditional<FMT == kINT8, int, float>::type;
   constexpr int CK = TF<FMT>::kChunkK;
+  constexpr int CPW = (S / kConsumers) > TF<FMT>::kMinChunksPerWarp ? (S / kConsumers)
+                                                                     : TF<FMT>::kMinChunksPerWarp;
+  constexpr int ACTIVE = S / CPW;
+  constexpr int STAGE_BYTES = S * kChunkBytes;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], sbar;
+  __shared__ uint64_t tile_full[2], tile_free[2];
   __shared__ float red[32];
   __shared__ float xscale[NT];
-  __shared__ uint32_t part[kConsumers][16][8];  // raw 32-bit partials (f32 or s32)
+  __shared__ __align__(16) uint32_t part[2][kConsumers][16][8];  // per-warp tile partials
+  __shared__ __align__(16) uint8_t zero_b[64];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunks_tile = k / CK;
-  const int S = stage_chunks(chunks_tile);  // chunks per stage
-  const int cpw = max(S / kConsumers, TF<FMT>::kMinChunksPerWarp);
-  const int active_warps = S / cpw;
   const int ntiles = n / 16;
   const int per_cta = (ntiles + gridDim.x - 1) / gridDim.x;
   const int tile_begin = blockIdx.x * per_cta;
   const int tile_end = min(ntiles, tile_begin + per_cta);
+  const int ntile_cta = max(0, tile_end - tile_begin);
   const int stages_tile = chunks_tile / S;
-  const int total_stages = tile_end > tile_begin ? (tile_end - tile_begin) * stages_tile : 0;
-  const int stage_bytes = S * kChunkBytes;
-  const int xbytes = NT * (FMT == kINT8 ? k : 2 * k);
+  const int total_stages = ntile_cta * stages_tile;
+  const int groups_k = k / kW4Group;
+  const int rows = ntile_cta * 16;
+  const int xbytes = FMT == kINT8 ? NT * k
+                                  : (FMT == kW4 ? NT * 4 * k + NT * (k / kW4Group) * 4 : NT * 2 * k);
+  const int sbytes = FMT == kW4 ? rows * groups_k * 2 : (FMT == kINT8 ? rows * 4 : 0);
   uint8_t* xs = smem;
-  uint8_t* ring = smem + ((xbytes + 127) & ~127);
+  uint8_t* sc_smem = smem + ((xbytes + 127) & ~127);
+  uint8_t* ring = sc_smem + ((sbytes + 127) & ~127);
 
+  if (threadIdx.x < 64) zero_b[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < n_stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], active_warps);
+      mbar_init(&empty[s], ACTIVE);
+    }
+    mbar_init(&sbar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tile_full[b], ACTIVE);
+      mbar_init(&tile_free[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   if (warp == kConsumers) {
-    // producer: stream this CTA's contiguous weight range. Weights only, so it
-    // runs ahead of griddepcontrol.wait and fills the ring during the
-    // previous kernel.
-    if (lane == 0) {
+    // producer: weights only, so it runs ahead of griddepcontrol.wait
+    if (lane == 0 && total_stages > 0) {
+      if (sbytes > 0) {
+        const uint8_t* ssrc = static_cast<const uint8_t*>(ws) +
+                              size_t(tile_begin) * 16 * (FMT == kW4 ? groups_k * 2 : 4);
+        mbar_expect_tx(&sbar, sbytes);
+        bulk_g2s(sc_smem, ssrc, sbytes, &sbar);
+      }
       const uint8_t* src = wtf + size_t(tile_begin) * chunks_tile * kChunkBytes;
+      int s = 0;
+      uint32_t phase = 0;
       for (int st = 0; st < total_stages; ++st) {
-        const int s = st % n_stages;
-        mbar_wait(&empty[s], ((st / n_stages) & 1) ^ 1);
-        mbar_expect_tx(&full[s], stage_bytes);
-        bulk_g2s(ring + size_t(s) * stage_bytes, src + size_t(st) * stage_bytes, stage_bytes,
-                 &full[s]);
+        mbar_wait(&empty[s], phase ^ 1);
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        bulk_g2s(ring + size_t(s) * STAGE_BYTES, src + size_t(st) * STAGE_BYTES, STAGE_BYTES, &full[s]);
+        if (++s == n_stages) {
+          s = 0;
+          phase ^= 1;
+        }
       }
     }
     pdl_wait();
     pdl_trigger();
+    return;
+  }
+  if (warp == kConsumers + 1) {
+    // epilogue warp: tile accumulators -> y (scales, SwiGLU pairing, residual)
+    pdl_wait();
+    pdl_trigger();
+    if (sbytes > 0 && total_stages > 0) mbar_wait(&sbar, 0);
+    named_sync(3, kConsThreads + 32);  // prologue (xscale) is complete
+    const float* sc_f = reinterpret_cast<const float*>(sc_smem);
+    for (int i = 0; i < ntile_cta; ++i) {
+      const int b = i & 1;
+      mbar_wait(&tile_full[b], (i >> 1) & 1);
+      const int tile = tile_begin + i;
+      // 128 (row, col) values; lane handles rows 2*(lane>>3)+{0,1} (a pair), col lane & 7,
+      // for row pairs lane>>3 in {0..3} and +4 in a second pass
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+        const int rp = (lane >> 3) + pass * 4;  // row pair 0..7
+        const int col = lane & 7;
+        const int row = 2 * rp;
+        float v0, v1;
+        if (FMT == kINT8) {  // exact int32 across warps
+          int i0 = 0, i1 = 0;
+#pragma unroll 4
+          for (int w2 = 0; w2 < ACTIVE; ++w2) {
+            i0 += int(part[b][w2][row][col]);
+            i1 += int(part[b][w2][row + 1][col]);
+          }
+          v0 = float(i0);
+          v1 = float(i1);
+        } else {
+          v0 = 0.f;
+          v1 = 0.f;
+#pragma unroll 4
+          for (int w2 = 0; w2 < ACTIVE; ++w2) {
+            v0 += __uint_as_float(part[b][w2][row][col]);
+            v1 += __uint_as_float(part[b][w2][row + 1][col]);
+          }
+        }
+        if (col < T) {
+          if (FMT == kINT8) {
+            const int lrr = i * 16 + row;
+            v0 = (v0 * xscale[col]) * sc_f[lrr];
+            v1 = (v1 * xscale[col]) * sc_f[lrr + 1];
+          }
+          store_pair<EPI>(y, n, col, tile * 16 + row, v0, v1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_free[b]);
+    }
     return;
   }
 
@@ -229,119 +351,113 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait();
   pdl_trigger();
   prologue<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red, xscale);
+  named_sync(3, kConsThreads + 32);  // release the epilogue warp (xscale ready)
   const int g = lane >> 2, tq = lane & 3;
   const bool has_tok = g < T;  // this lane's MMA column is a real token
-  const int groups_k = k / kW4Group;
-  const half2 k1032 = __float2half2_rn(1032.0f);
+  if (sbytes > 0 && total_stages > 0) mbar_wait(&sbar, 0);
+  const half* sc_h = reinterpret_cast<const half*>(sc_smem);   // W4 [rows][groups_k]
+  const float* corr = reinterpret_cast<const float*>(xs + size_t(NT) * 4 * k);
+  // B-fragment rows. MMA column g only feeds output column g, and columns >= T
+  // are never stored, so lanes without a token read token 0's row (finite)
+  // instead of a zero slot: loop-invariant bases, no per-load masking.
+  const int brow = has_tok ? g : 0;
+  const uint8_t* xrow = xs + size_t(brow) * (FMT == kINT8 ? k : 2 * k) + tq * 8;
+  const uint8_t* xrow16 = xs + size_t(NT) * 2 * k + size_t(brow) * 2 * k + tq * 8;
 
   Acc acc[4] = {0, 0, 0, 0};
-  float cg[4] = {0.f, 0.f, 0.f, 0.f};  // W4: current 128-k group
+  Acc acc2[4] = {0, 0, 0, 0};
+  float cg[2][4] = {};
+  int s = 0;
+  uint32_t phase = 0;
+  int c_tile0 = 0, ti = 0;  // chunk offset within the tile, tile index within the CTA
+  const int my_c0 = warp * CPW;
   for (int st = 0; st < total_stages; ++st) {
-    const int s = st % n_stages;
-    const int tile = tile_begin + st / stages_tile;
-    const int c_tile0 = (st % stages_tile) * S;  // first chunk (within the tile) of the stage
-    mbar_wait(&full[s], (st / n_stages) & 1);
-    if (warp < active_warps) {
-      const uint4* stage = reinterpret_cast<const uint4*>(ring + size_t(s) * stage_bytes);
-#pragma unroll 2
-      for (int j = 0; j < cpw; ++j) {
-        const int c_local = warp * cpw + j;
-        const int c = c_tile0 + c_local;  // chunk index within the tile
-        const uint4 a4 = stage[c_local * 32 + lane];
+    mbar_wait(&full[s], phase);
+    if (warp < ACTIVE) {
+      const uint4* stage = reinterpret_cast<const uint4*>(ring + size_t(s) * STAGE_BYTES) +
+                           my_c0 * 32 + lane;
+      const int cbase = c_tile0 + my_c0;
+      const int lr = ti * 16 + g;
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) {
+        const uint4 a4 = stage[j * 32];
+        const int c = cbase + j;
         if (FMT == kFP16) {
-          const int kk = c * 16 + 2 * tq;
-          uint32_t b0 = 0, b1 = 0;
-          if (has_tok) {
-            const half* xr = reinterpret_cast<const half*>(xs) + size_t(g) * k;
-            b0 = *reinterpret_cast<const uint32_t*>(xr + kk);
-            b1 = *reinterpret_cast<const uint32_t*>(xr + kk + 8);
-          }
+          const uint2 b = *reinterpret_cast<const uint2*>(xrow + c * 32);
           const uint32_t a[4] = {a4.x, a4.y, a4.z, a4.w};
-          mma_f16(reinterpret_cast<float(&)[4]>(acc), a, b0, b1);
+          if (j & 1) mma_f16(reinterpret_cast<float(&)[4]>(acc2), a, b.x, b.y);
+          else mma_f16(reinterpret_cast<float(&)[4]>(acc), a, b.x, b.y);
         } else if (FMT == kINT8) {
-          const int kk = c * 32 + 4 * tq;
-          uint32_t b0 = 0, b1 = 0;
-          if (has_tok) {
-            const int8_t* xr = reinterpret_cast<const int8_t*>(xs) + size_t(g) * k;
-            b0 = *reinterpret_cast<const uint32_t*>(xr + kk);
-            b1 = *reinterpret_cast<const uint32_t*>(xr + kk + 16);
-          }
+          const uint2 b = *reinterpret_cast<const uint2*>(xrow + c * 32);
           const uint32_t a[4] = {a4.x, a4.y, a4.z, a4.w};
-          mma_s8(reinterpret_cast<int(&)[4]>(acc), a, b0, b1);
+          if (j & 1) mma_s8(reinterpret_cast<int(&)[4]>(acc2), a, b.x, b.y);
+          else mma_s8(reinterpret_cast<int(&)[4]>(acc), a, b.x, b.y);
         } else {
           const uint32_t wv[4] = {a4.x, a4.y, a4.z, a4.w};
-          const half* xr = reinterpret_cast<const half*>(xs) + size_t(g) * k;
+          float (&cgr)[4] = cg[(j >> 1) & 1];  // group accumulator (compile-time index: j is unrolled)
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int kk = c * 64 + jj * 16 + 2 * tq;
-            uint32_t b0 = 0, b1 = 0;
-            if (has_tok) {
-              b0 = *reinterpret_cast<const uint32_t*>(xr + kk);
-              b1 = *reinterpret_cast<const uint32_t*>(xr + kk + 8);
-            }
-            uint32_t a[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              a[i] = h22u(__hsub2(u2h2(lop3_and_or(wv[jj] >> (4 * i), 0x000F000Fu, 0x64006400u)),
-                                  k1032));
-            mma_f16(cg, a, b0, b1);
+          for (int p = 0; p < 2; ++p) {  // step 2p: (1024+q) vs x; step 2p+1: (1024+16q) vs x/16
+            const uint32_t w0 = wv[2 * p], w1 = wv[2 * p + 1];
+            const uint32_t w0s = w0 >> 8, w1s = w1 >> 8;
+            const uint32_t a_lo[4] = {lop3_and_or(w0, 0x000F000Fu, 0x64006400u),
+                                      lop3_and_or(w0s, 0x000F000Fu, 0x64006400u),
+                                      lop3_and_or(w1, 0x000F000Fu, 0x64006400u),
+                                      lop3_and_or(w1s, 0x000F000Fu, 0x64006400u)};
+            const uint32_t a_hi[4] = {lop3_and_or(w0, 0x00F000F0u, 0x64006400u),
+                                      lop3_and_or(w0s, 0x00F000F0u, 0x64006400u),
+                                      lop3_and_or(w1, 0x00F000F0u, 0x64006400u),
+                                      lop3_and_or(w1s, 0x00F000F0u, 0x64006400u)};
+            const int kb = (c * 64 + p * 32) * 2;  // byte offset of the even step's 16-k block
+            const uint2 be = *reinterpret_cast<const uint2*>(xrow + kb);
+            const uint2 bo = *reinterpret_cast<const uint2*>(xrow16 + kb + 32);
+            mma_f16(cgr, a_lo, be.x, be.y);
+            mma_f16(cgr, a_hi, bo.x, bo.y);
           }
-          if (c & 1) {  // end of a 128-k group: fp32 group scale per row
-            const half* sc = static_cast<const half*>(ws);
+          if (j & 1) {  // end of a 128-k group (my_c0 and CPW are even)
             const int grp = c >> 1;
-            const float slo = __half2float(sc[size_t(tile * 16 + g) * groups_k + grp]);
-            const float shi = __half2float(sc[size_t(tile * 16 + g + 8) * groups_k + grp]);
-            acc[0] = fmaf(slo, cg[0], acc[0]);
-            acc[1] = fmaf(slo, cg[1], acc[1]);
-            acc[2] = fmaf(shi, cg[2], acc[2]);
-            acc[3] = fmaf(shi, cg[3], acc[3]);
-            cg[0] = cg[1] = cg[2] = cg[3] = 0.f;
+            const float slo = __half2float(sc_h[lr * groups_k + grp]);
+            const float shi = __half2float(sc_h[(lr + 8) * groups_k + grp]);
+            const float c0 = corr[(2 * tq < NT ? 2 * tq : 0) * groups_k + grp];
+            const float c1 = corr[(2 * tq + 1 < NT ? 2 * tq + 1 : 0) * groups_k + grp];
+            acc[0] = fmaf(slo, cgr[0] - c0, acc[0]);
+            acc[1] = fmaf(slo, cgr[1] - c1, acc[1]);
+            acc[2] = fmaf(shi, cgr[2] - c0, acc[2]);
+            acc[3] = fmaf(shi, cgr[3] - c1, acc[3]);
+            cgr[0] = cgr[1] = cgr[2] = cgr[3] = 0.f;
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if ((st + 1) % stages_tile == 0) {
-      // tile complete: reduce the 16 x 8 partials of all warps, fused epilogue
-      uint32_t raw[4];
+    if (++s == n_stages) {
+      s = 0;
+      phase ^= 1;
+    }
+    c_tile0 += S;
+    if (c_tile0 == chunks_tile) {
+      // tile complete: add this warp's partial into the tile accumulator (async)
+      c_tile0 = 0;
+      if (warp < ACTIVE) {
+        const int b = ti & 1;
+        if (ti >= 2) mbar_wait(&tile_free[b], ((ti >> 1) - 1) & 1);  // epilogue drained it
+        uint32_t* pw = &part[b][warp][0][0];
+        uint32_t r4[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (FMT == kINT8) raw[i] = warp < active_warps ? uint32_t(int(acc[i])) : 0u;
-        else raw[i] = __float_as_uint(warp < active_warps ? float(acc[i]) : 0.0f);
-      }
-      part[warp][g][2 * tq] = raw[0];
-      part[warp][g][2 * tq + 1] = raw[1];
-      part[warp][g + 8][2 * tq] = raw[2];
-      part[warp][g + 8][2 * tq + 1] = raw[3];
-      named_sync(1, kConsThreads);
-      if (threadIdx.x < 128) {
-        const int row = threadIdx.x >> 3, col = threadIdx.x & 7;
-        float v;
-        if (FMT == kINT8) {
-          int iv = 0;  // exact int32 across warps
-#pragma unroll
-          for (int w2 = 0; w2 < kConsumers; ++w2) iv += int(part[w2][row][col]);
-          v = float(iv);
-        } else {
-          v = 0.f;
-#pragma unroll
-          for (int w2 = 0; w2 < kConsumers; ++w2) v += __uint_as_float(part[w2][row][col]);
+        for (int i = 0; i < 4; ++i) {
+          const Acc tot = acc[i] + acc2[i];
+          r4[i] = FMT == kINT8 ? uint32_t(int(tot)) : __float_as_uint(float(tot));
         }
-        const float vn = __shfl_down_sync(0xffffffffu, v, 8);  // row + 1, same column
-        if ((row & 1) == 0 && col < T) {
-          float v0 = v, v1 = vn;
-          if (FMT == kINT8) {
-            const float* sw = static_cast<const float*>(ws);
-            v0 = (v0 * xscale[col]) * sw[tile * 16 + row];
-            v1 = (v1 * xscale[col]) * sw[tile * 16 + row + 1];
-          }
-          store_pair<EPI>(y, n, col, tile * 16 + row, v0, v1);
-        }
+        pw[g * 8 + 2 * tq] = r4[0];
+        pw[g * 8 + 2 * tq + 1] = r4[1];
+        pw[(g + 8) * 8 + 2 * tq] = r4[2];
+        pw[(g + 8) * 8 + 2 * tq + 1] = r4[3];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tile_full[b]);
       }
-      named_sync(1, kConsThreads);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] = 0;
+      for (int i = 0; i < 4; ++i) acc[i] = acc2[i] = 0;
+      ++ti;
     }
   }
 }
@@ -373,42 +489,64 @@ __global__ void repack_tf_kernel(int fmt, const uint8_t* __restrict__ src, int n
       const int kk = c * 32 + 4 * tq + ((reg & 2) ? 16 : 0);
       word = *reinterpret_cast<const uint32_t*>(src + size_t(row) * k + kk);
     } else {
-      // element e of the k16 step: pair e>>1 -> a0..a3, e&1 -> first/second k
+      // word `reg` = 2p + h of the chunk (p: step pair (2p, 2p+1); h: 0 -> fragment
+      // regs a0/a1 (k base 2tq), 1 -> a2/a3 (k base 2tq + 8)). Nibble position ->
+      // (step, fragment reg, lo/hi):
+      //   pos0/pos4: step 2p,   row g,   k, k+1      pos2/pos6: step 2p,   row g+8, k, k+1
+      //   pos1/pos5: step 2p+1, row g,   k, k+1      pos3/pos7: step 2p+1, row g+8, k, k+1
       const uint32_t* sw = reinterpret_cast<const uint32_t*>(src);
+      const int p = reg >> 1, h = reg & 1;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int pr = e >> 1, hi = e & 1;
-        const int row = tile * 16 + g + ((pr & 1) ? 8 : 0);
-        const int kk = c * 64 + reg * 16 + 2 * tq + ((pr & 2) ? 8 : 0) + hi;
+      for (int pos = 0; pos < 8; ++pos) {
+        const int step = 2 * p + (pos & 1);
+        const int row = tile * 16 + g + ((pos & 2) ? 8 : 0);
+        const int kk = c * 64 + step * 16 + 2 * tq + (h ? 8 : 0) + (pos >> 2);
         const uint32_t w = sw[size_t(row) * (k / 8) + kk / 8];
         const int si = kk & 7;
         const uint32_t q = (w >> (4 * ((si >> 1) + 4 * (si & 1)))) & 0xF;
-        word |= q << (4 * ((e >> 1) + 4 * (e & 1)));
+        word |= q << (4 * pos);
       }
     }
     reinterpret_cast<uint32_t*>(dst)[i] = word;
   }
 }
 
+template <int FMT, int PRO, int EPI, int NT, int S>
+void launch_tf_s(const LinearW& W, const float* x, int T, const half* gamma, float eps, float* y,
+                 cudaStream_t st) {
+  const int ntiles = W.n / 16;
+  const int grid = std::max(1, std::min(ntiles, kNumSMs));
+  const int stage_bytes = S * kChunkBytes;
+  const size_t xraw = FMT == kINT8 ? size_t(NT) * W.k
+                                   : (FMT == kW4 ? size_t(NT) * 4 * W.k + size_t(NT) * (W.k / kW4Group) * 4
+                                                 : size_t(NT) * 2 * W.k);
+  const size_t xbytes = (xraw + 127) & ~size_t(127);
+  const int per_cta = (ntiles + grid - 1) / grid;
+  const size_t sbytes = FMT == kW4 ? size_t(per_cta) * 16 * (W.k / kW4Group) * 2
+                                   : (FMT == kINT8 ? size_t(per_cta) * 16 * 4 : 0);
+  const size_t fixed = xbytes + ((sbytes + 127) & ~size_t(127));
+  int stages = int((kSmemBudget - std::min<size_t>(fixed, kSmemBudget - 2 * stage_bytes)) / stage_bytes);
+  stages = std::max(2, std::min(kMaxStages, stages));
+  const size_t smem = fixed + size_t(stages) * stage_bytes;
+  if (smem > 200 * 1024) throw ConfigErr("gemv: shared memory budget exceeded");
+  static bool attr_done = false;
+  if (!attr_done) {
+    MSW_CUDA(cudaFuncSetAttribute(gemv_tf_kernel<FMT, PRO, EPI, NT, S>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_done = true;
+  }
+  launch_pdl(gemv_tf_kernel<FMT, PRO, EPI, NT, S>, dim3(grid), dim3(kThreads), smem, st,
+             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages);
+}
+
 template <int FMT, int PRO, int EPI, int NT>
 void launch_tf(const LinearW& W, const float* x, int T, const half* gamma, float eps, float* y,
                cudaStream_t st) {
-  const int ntiles = W.n / 16;
-  const int grid = std::max(1, std::min(ntiles, kNumSMs));
   const int chunks_tile = W.k / TF<FMT>::kChunkK;
-  const int stage_bytes = stage_chunks(chunks_tile) * kChunkBytes;
-  const size_t xbytes = (size_t(NT) * (FMT == kINT8 ? W.k : 2 * W.k) + 127) & ~size_t(127);
-  int stages = int((kSmemBudget - std::min<size_t>(xbytes, kSmemBudget - 2 * stage_bytes)) / stage_bytes);
-  stages = std::max(2, std::min(kMaxStages, stages));
-  const size_t smem = xbytes + size_t(stages) * stage_bytes;
-  static bool attr_done = false;
-  if (!attr_done) {
-    MSW_CUDA(cudaFuncSetAttribute(gemv_tf_kernel<FMT, PRO, EPI, NT>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_done = true;
-  }
-  launch_pdl(gemv_tf_kernel<FMT, PRO, EPI, NT>, dim3(grid), dim3(kThreads), smem, st,
-             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages);
+  if (chunks_tile % 32 == 0) return launch_tf_s<FMT, PRO, EPI, NT, 32>(W, x, T, gamma, eps, y, st);
+  if (chunks_tile % 8 == 0) return launch_tf_s<FMT, PRO, EPI, NT, 8>(W, x, T, gamma, eps, y, st);
+  if (chunks_tile % 4 == 0) return launch_tf_s<FMT, PRO, EPI, NT, 4>(W, x, T, gamma, eps, y, st);
+  throw ConfigErr("gemv: unsupported K for the decode layout");
 }
 
 template <int FMT, int NT>
@@ -464,7 +602,16 @@ void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, cons
   switch (W.fmt) {
     case kFP16: return dispatch_fmt<kFP16>(W, pro, epi, x, T, gamma, eps, y, st);
     case kINT8: return dispatch_fmt<kINT8>(W, pro, epi, x, T, gamma, eps, y, st);
-    case kW4: return dispatch_fmt<kW4>(W, pro, epi, x, T, gamma, eps, y, st);
+    case kW4:
+      if (T > 1 && size_t(kGemvMaxTokens) * 4 * W.k > 120 * 1024) {
+        // large-K multi-token W4 (not on any engine path: GPTQ modes are batch-1):
+        // one launch per token keeps the x staging within shared memory
+        for (int t = 0; t < T; ++t)
+          dispatch_fmt<kW4>(W, pro, epi, x + size_t(t) * W.k, 1, gamma, eps,
+                            y + size_t(t) * (epi == kEpiSwiglu ? W.n / 2 : W.n), st);
+        return;
+      }
+      return dispatch_fmt<kW4>(W, pro, epi, x, T, gamma, eps, y, st);
     default: throw ConfigErr("gemv: bad weight format");
   }
 }

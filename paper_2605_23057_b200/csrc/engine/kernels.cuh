@@ -75,8 +75,11 @@ struct AttnShape {
 };
 // qkv fp32 [T, (Hq+2Hk)*D] -> RoPE on q,k -> q fp16 [T,Hq,D]; k,v fp16 into the
 // paged cache at slot[t] (= block*16 + offset) of this layer.
+// RoPE cos/sin table [max_pos][head_dim/2] (fp32 angle pos * inv_freq, as the oracle)
+void launch_rope_table(const float* inv_freq, int head_dim, int max_pos, float2* table,
+                       cudaStream_t st);
 void launch_rope_append(const float* qkv, int T, const int* pos, const int* slot,
-                        const float* inv_freq, const AttnShape& a, half* q_out, half* kc, half* vc,
+                        const float2* rope, const AttnShape& a, half* q_out, half* kc, half* vc,
                         cudaStream_t st);
 // o fp32 [T, Hq, D]: token t (sequence seq_of[t], position pos[t]) attends to
 // positions [0, pos[t]] of its sequence through block_table[seq_of[t]].
@@ -86,7 +89,7 @@ void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
 
 // Decode / continuous batching (each token is the newest of its own sequence):
 // RoPE + KV append fused into the attention kernel; reads fp32 qkv directly.
-void launch_attention_decode(const float* qkv, const float* inv_freq, int T, const int* pos,
+void launch_attention_decode(const float* qkv, const float2* rope, int T, const int* pos,
                              const int* slot, const int* seq_of, const int* block_table, half* kc,
                              half* vc, const AttnShape& a, int nsplit, float* part_o,
                              float* part_ml, int* counters, float* o, cudaStream_t st);
