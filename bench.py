@@ -194,24 +194,40 @@ def ref_route_cost():
 
 
 def run_reference(args):
+    """Reference arm: the reference has no inference path, so the
+    C oracle port of the same W4 decode math runs on all host cores; one step
+    = one 8B-shape decode token. Rank 0 only."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    samples = []
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm-up state worth excluding beyond weight init
-    cb = None
-    for _ in range(args.steps):
-        cb = cpu_baseline_8b(new_tokens=2, prompt_len=2)
-        samples.append(cb["value"])
-    v = statistics.mean(samples)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # reference-arm baseline (port) only
+    from paper_2605_23057_b200.configs import model_cfg
+    n_tok = args.warmup + args.steps
+    t0 = time.perf_counter()
+    m = O.OracleModel(model_cfg("llama8b"), seed=0, modes_mask=1 << 2, max_ctx=n_tok + 4)
+    init_s = time.perf_counter() - t0
+    p = synth_prompt(1, 1, 128256)
+    # generate() runs one full forward per token; time W warm-up + K timed tokens
+    t0 = time.perf_counter()
+    m.generate(2, p, args.warmup)
+    t_warm = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    m.generate(2, p, n_tok)
+    t_all = time.perf_counter() - t0
+    m.close()
+    dt = max(1e-9, t_all - t_warm)
+    v = args.steps / dt
     line = {"metric": "decode tokens/s per mode and routed mix (1/2/4/8 B200); mean latency vs FP16 mode",
             "impl": "reference", "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "w4a16",
             "data": "synthetic", "config": {"workload": "llama8b batch-1 decode (gptq4 mode)",
                                             "model": "llama3.1-8b-shape random-init"},
-            "cpu_baseline": dict(cb, value=v),
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": O.lib().orc_threads(),
+                             "kind": "port",
+                             "sample": f"8B-shape W4 g128 decode, {args.steps} timed tokens after "
+                                       f"{args.warmup} warm-up (weight init {init_s:.1f} s excluded)"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "reference_route_cost": ref_route_cost(),
             "note": "reference has no inference path (SPEC.md:20); arm = C oracle port of the same math"}
@@ -325,8 +341,82 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def deploy_mix_trace(per_class: int, seed: int = 7) -> str:
+    """BASELINE config 5: short interactive (SyntheticSS 128->32), long-gen
+    (SyntheticSL 128->128, GSM8K 250->256), shared-prefix chat (1024->128),
+    8K long-context (MemoryPressureLongContext, prompt x4 -> ~8192, 64 out),
+    tagged, jitter 0.10 via the reference generator (workload.cpp:61-91)."""
+    from paper_2605_23057_b200 import controller as ctl
+    counts = {"SyntheticSS": per_class, "SyntheticSL": per_class, "GSM8K": per_class,
+              "SharedPrefixChat": per_class, "MemoryPressureLongContext": per_class}
+    lines = []
+    for line in ctl.generate_trace(counts, jitter=0.10, seed=seed).splitlines():
+        d = ctl.parse_trace_line(line)
+        if d["workload_tag"] == "MemoryPressureLongContext":
+            d["prompt_tokens"] *= 4  # 2048 nominal -> 8192 (8K long context)
+        lines.append(ctl.format_trace_line(d))
+    return "\n".join(lines) + "\n"
+
+
+def run_mix(args):
+    """Routed deployment mix (config 5), request-sharded over ranks: each rank
+    executes its share through the C++ executor (RulePolicy -> C ABI)."""
+    import torch
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2605_23057_b200 import engine_cfg
+    from paper_2605_23057_b200.engine import Engine, execute_trace
+    eng = Engine(engine_cfg(target="llama8b", draft="llama1b", seed=0, kv_blocks=1536, max_batch=64,
+                            max_seq_len=9400, use_graphs=True), device=local)
+    lines = deploy_mix_trace(args.mix_per_class).splitlines()
+    mine = "\n".join(l for i, l in enumerate(lines) if i % ws == rank) + "\n"
+    execute_trace(eng, "\n".join(lines[:2]) + "\n", max_output_tokens=4)  # warm-up (graphs, attrs)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rows, summ = execute_trace(eng, mine, prefix_len=768)
+    wall = time.perf_counter() - t0
+    vals = torch.tensor([summ["generated_tokens"], summ["mode_time_ms"], wall], dtype=torch.float64,
+                        device="cuda")
+    if ws > 1:
+        toks = vals[0].clone()
+        torch.distributed.all_reduce(toks)
+        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
+        vals[0] = toks
+    if rank == 0:
+        from paper_2605_23057_b200.controller import MODES
+        per_mode = {}
+        for r in rows:
+            m = MODES[r["mode"]]
+            pm = per_mode.setdefault(m, {"requests": 0, "tokens": 0, "mode_ms": 0.0, "speedups": []})
+            pm["requests"] += 1
+            pm["tokens"] += r["output_tokens"]
+            pm["mode_ms"] += r["mode_latency_ms"]
+            pm["speedups"].append(r["speedup"])
+        for m, pm in per_mode.items():
+            pm["tok_s"] = pm["tokens"] / (pm["mode_ms"] / 1000.0)
+            pm["mean_speedup_vs_fp16"] = statistics.mean(pm.pop("speedups"))
+        print(json.dumps({
+            "metric": "decode tokens/s per mode and routed mix (1/2/4/8 B200); mean latency vs FP16 mode",
+            "workload": "deploy_mix", "value": vals[0].item() / (vals[1].item() / 1000.0),
+            "unit": "tokens/s (generated tokens / routed-mode request time, max over ranks)",
+            "n_gpus": ws, "requests": len(lines), "mean_speedup_vs_fp16": summ["mean_speedup"],
+            "aggregate_latency_speedup": summ["aggregate_latency_speedup"],
+            "collapsed_mean_speedup": summ["collapsed_mean_speedup"], "per_mode_rank0": per_mode,
+            "scaling": "weak", "data": "synthetic", "wall_s": vals[2].item()}), flush=True)
+    eng.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", choices=["decode8b", "mix"], default="decode8b")
+    ap.add_argument("--mix-per-class", type=int, default=4)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
@@ -335,6 +425,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "mix":
+        run_mix(args)
     else:
         run_ours(args)
 

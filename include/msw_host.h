@@ -10,6 +10,9 @@
  *   msw_trace_format_line <- format_trace_line          (trace_io.cpp:78-92)
  *   msw_trace_generate    <- generate_trace             (workload.cpp:61-91)
  *   msw_route_cost        <- the per-decision overhead stamp (routing.cpp:188-192)
+ *   msw_execute_trace     <- run_policy + simulate_request + summarize
+ *                            (sim.cpp:80-235): route, EXECUTE on the B200
+ *                            engine (include/msw_engine.h), aggregate
  *
  * Return codes mirror the reference CLI's exit codes (tools/modeswitch.cpp:26-30):
  *   0 ok, 2 ConfigError, 3 DataError, 1 anything else. Message via
@@ -83,6 +86,57 @@ int msw_trace_generate(const int32_t counts[11], double jitter, uint64_t seed,
  * policy's own overhead stamps and the wall time per decision (ms). */
 int msw_route_cost(const char* ndjson, int32_t passes, double* mean_stamp_ms,
                    double* wall_ms_per_decision);
+
+/* ---- executor (include/modeswitch/executor.hpp) ---- */
+struct msw_engine;
+
+typedef struct msw_exec_opts {
+  int32_t fallback_enabled;  /* FP16 emergency fallback (sim.cpp:112-124) */
+  int32_t zero_overhead;
+  double extra_overhead_ms;
+  int32_t measure_fp16_baseline;
+  uint64_t token_seed;
+  int32_t prefix_len;        /* shared-prefix tokens, e.g. 768 */
+  int32_t max_output_tokens; /* > 0 caps generation */
+  int32_t max_prompt_tokens; /* > 0 caps prompts */
+  int32_t cohort_max;        /* continuous-batching cohort size (64) */
+} msw_exec_opts;
+
+typedef struct msw_exec_row {
+  int32_t mode;          /* routed InferenceMode */
+  int32_t reason;        /* RoutingReason */
+  int32_t executed_mode; /* FP16 when the fallback hit */
+  int32_t family;
+  int32_t prompt_tokens;
+  int32_t output_tokens;
+  int32_t fallback_used;
+  int32_t spec_proposed;
+  int32_t spec_accepted;
+  int32_t prefix_hit_tokens;
+  double fp16_latency_ms;
+  double mode_latency_ms;
+  double speedup;
+  double overhead_ms;
+  double prefill_ms;
+  double decode_ms;
+} msw_exec_row;
+
+typedef struct msw_exec_summary {
+  int32_t request_count;
+  int32_t fallback_count;
+  double mean_speedup;
+  double aggregate_latency_speedup;
+  double collapsed_mean_speedup;
+  double mean_overhead_ms;
+  double mode_time_ms;
+  int64_t generated_tokens;
+} msw_exec_summary;
+
+/* Routes (RulePolicy, cfg NULL = defaults) and executes every request of an
+ * NDJSON trace on the engine; rows in trace order. */
+int msw_execute_trace(struct msw_engine* engine, int32_t vocab, const char* ndjson,
+                      const msw_classifier_cfg* cfg, const msw_exec_opts* opts, int32_t n_max,
+                      msw_exec_row* rows, int32_t* n_out, msw_exec_summary* summary);
 
 const char* msw_host_last_error(void);
 

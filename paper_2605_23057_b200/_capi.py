@@ -77,6 +77,35 @@ class RouteOut(C.Structure):
     ]
 
 
+class ExecOpts(C.Structure):
+    _fields_ = [
+        ("fallback_enabled", C.c_int32), ("zero_overhead", C.c_int32),
+        ("extra_overhead_ms", C.c_double), ("measure_fp16_baseline", C.c_int32),
+        ("token_seed", C.c_uint64), ("prefix_len", C.c_int32), ("max_output_tokens", C.c_int32),
+        ("max_prompt_tokens", C.c_int32), ("cohort_max", C.c_int32),
+    ]
+
+
+class ExecRow(C.Structure):
+    _fields_ = [
+        ("mode", C.c_int32), ("reason", C.c_int32), ("executed_mode", C.c_int32),
+        ("family", C.c_int32), ("prompt_tokens", C.c_int32), ("output_tokens", C.c_int32),
+        ("fallback_used", C.c_int32), ("spec_proposed", C.c_int32), ("spec_accepted", C.c_int32),
+        ("prefix_hit_tokens", C.c_int32), ("fp16_latency_ms", C.c_double),
+        ("mode_latency_ms", C.c_double), ("speedup", C.c_double), ("overhead_ms", C.c_double),
+        ("prefill_ms", C.c_double), ("decode_ms", C.c_double),
+    ]
+
+
+class ExecSummary(C.Structure):
+    _fields_ = [
+        ("request_count", C.c_int32), ("fallback_count", C.c_int32), ("mean_speedup", C.c_double),
+        ("aggregate_latency_speedup", C.c_double), ("collapsed_mean_speedup", C.c_double),
+        ("mean_overhead_ms", C.c_double), ("mode_time_ms", C.c_double),
+        ("generated_tokens", C.c_int64),
+    ]
+
+
 def _load(name: str) -> C.CDLL:
     path = os.path.join(LIB_DIR, name)
     if not os.path.exists(path):
@@ -129,6 +158,9 @@ def host_lib() -> C.CDLL:
                                            C.c_double, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
         lib.msw_route_cost.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]
+        lib.msw_execute_trace.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.POINTER(ClassifierCfg),
+                                          C.POINTER(ExecOpts), C.c_int32, C.POINTER(ExecRow),
+                                          C.POINTER(C.c_int32), C.POINTER(ExecSummary)]
         lib.msw_host_last_error.restype = C.c_char_p
         _host = lib
     return _host

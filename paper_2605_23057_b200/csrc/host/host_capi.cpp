@@ -5,6 +5,7 @@
 #include <string>
 
 #include "modeswitch/classifier.hpp"
+#include "modeswitch/executor.hpp"
 #include "modeswitch/routing.hpp"
 #include "modeswitch/trace_io.hpp"
 #include "modeswitch/workload.hpp"
@@ -194,6 +195,62 @@ int msw_route_cost(const char* ndjson, int32_t passes, double* mean_stamp_ms,
                             .count();
     if (mean_stamp_ms) *mean_stamp_ms = stamped / double(n);
     if (wall_ms_per_decision) *wall_ms_per_decision = wall / double(n);
+  });
+}
+
+int msw_execute_trace(struct msw_engine* engine, int32_t vocab, const char* ndjson,
+                      const msw_classifier_cfg* c, const msw_exec_opts* opts, int32_t n_max,
+                      msw_exec_row* rows, int32_t* n_out, msw_exec_summary* summary) {
+  return guarded([&] {
+    if (!engine || !opts) throw ms::ConfigError("NULL engine/options");
+    const auto trace = parse_ndjson(ndjson);
+    if (n_out) *n_out = static_cast<int32_t>(trace.size());
+    if (static_cast<int64_t>(trace.size()) > n_max) throw ms::Error("output array too small");
+    ms::ExecOptions o;
+    o.classifier = to_cpp(c);
+    o.fallback_enabled = opts->fallback_enabled != 0;
+    o.zero_overhead = opts->zero_overhead != 0;
+    o.extra_overhead_ms = opts->extra_overhead_ms;
+    o.measure_fp16_baseline = opts->measure_fp16_baseline != 0;
+    o.token_seed = opts->token_seed;
+    o.prefix_len = opts->prefix_len;
+    o.max_output_tokens = opts->max_output_tokens;
+    o.max_prompt_tokens = opts->max_prompt_tokens;
+    o.cohort_max = opts->cohort_max > 0 ? opts->cohort_max : 64;
+    o.vocab = vocab;
+    const ms::RulePolicy policy(o.classifier);
+    const ms::ExecRunResult run = ms::run_policy(trace, policy, engine, o);
+    for (size_t i = 0; i < run.results.size(); ++i) {
+      const auto& r = run.results[i];
+      msw_exec_row& w = rows[i];
+      w.mode = static_cast<int32_t>(r.decision.mode);
+      w.reason = static_cast<int32_t>(r.decision.reason);
+      w.executed_mode = static_cast<int32_t>(r.executed_mode);
+      w.family = static_cast<int32_t>(r.family);
+      w.prompt_tokens = r.prompt_tokens;
+      w.output_tokens = r.output_tokens;
+      w.fallback_used = r.fallback_used;
+      w.spec_proposed = r.spec_proposed;
+      w.spec_accepted = r.spec_accepted;
+      w.prefix_hit_tokens = r.prefix_hit_tokens;
+      w.fp16_latency_ms = r.fp16_latency_ms;
+      w.mode_latency_ms = r.mode_latency_ms;
+      w.speedup = r.speedup;
+      w.overhead_ms = r.overhead_ms;
+      w.prefill_ms = r.prefill_ms;
+      w.decode_ms = r.decode_ms;
+    }
+    if (summary) {
+      const auto& p = run.report;
+      summary->request_count = p.request_count;
+      summary->fallback_count = p.fallback_count;
+      summary->mean_speedup = p.mean_speedup;
+      summary->aggregate_latency_speedup = p.aggregate_latency_speedup;
+      summary->collapsed_mean_speedup = p.collapsed_mean_speedup;
+      summary->mean_overhead_ms = p.mean_overhead_ms;
+      summary->mode_time_ms = p.mode_time_ms;
+      summary->generated_tokens = p.generated_tokens;
+    }
   });
 }
 

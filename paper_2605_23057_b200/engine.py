@@ -112,3 +112,21 @@ class Engine:
 
 
 __all__ = ["Engine", "RunResult", "_capi"]
+
+
+def execute_trace(engine: Engine, ndjson: str, *, token_seed: int = 0, prefix_len: int = 768,
+                  max_output_tokens: int = 0, max_prompt_tokens: int = 0, fallback: bool = True,
+                  measure_fp16: bool = True, zero_overhead: bool = False, cohort_max: int = 64):
+    """Route (RulePolicy) and execute a trace through the C++ executor
+    (libmodeswitch msw_execute_trace). Returns (rows as dicts, summary dict)."""
+    from ._capi import ExecOpts, ExecRow, ExecSummary, check_host, host_lib
+    n_max = ndjson.count("\n") + 1
+    rows = (ExecRow * n_max)()
+    n = C.c_int32()
+    summ = ExecSummary()
+    opts = ExecOpts(int(fallback), int(zero_overhead), 0.0, int(measure_fp16), token_seed, prefix_len,
+                    max_output_tokens, max_prompt_tokens, cohort_max)
+    check_host(host_lib().msw_execute_trace(engine.h, engine.vocab, ndjson.encode(), None,
+                                            C.byref(opts), n_max, rows, C.byref(n), C.byref(summ)))
+    out = [{f: getattr(rows[i], f) for f, _ in ExecRow._fields_} for i in range(n.value)]
+    return out, {f: getattr(summ, f) for f, _ in ExecSummary._fields_}

@@ -1,0 +1,65 @@
+"""The executor seam on the B200 (tiny model): the reference's run_policy /
+simulate_request / summarize flow (sim.cpp:80-263) with every request routed
+by the C++ RulePolicy and EXECUTED through the engine C ABI.
+
+Checks: routing identical to the reference goldens; every routed mode runs
+natively (no FP16 fallback); continuous-batching cohorts, speculative
+decoding and prefix-cache reuse are exercised; summary fields follow the reference's aggregation formulas.
+"""
+import csv
+import os
+
+import pytest
+
+from paper_2605_23057_b200 import controller as ctl
+from paper_2605_23057_b200 import engine_cfg
+from paper_2605_23057_b200.engine import Engine, execute_trace
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def eng(cuda_ok):
+    e = Engine(engine_cfg(target="tiny", draft="tiny_draft", seed=9, kv_blocks=2048,
+                          max_seq_len=2600))
+    yield e
+    e.close()
+
+
+def test_config1_mixed_trace_executes_routed_modes(eng):
+    text = open(os.path.join(GOLDEN, "config1_mixed.ndjson")).read()
+    gold = list(csv.DictReader(open(os.path.join(GOLDEN, "config1_mixed.decisions.csv"))))
+    rows, summ = execute_trace(eng, text, max_output_tokens=24, prefix_len=96)
+    assert len(rows) == len(gold) == 55
+    for r, g in zip(rows, gold):
+        assert ctl.MODES[r["mode"]] == g["mode"]
+        assert ctl.REASONS[r["reason"]] == g["reason"]
+        assert ctl.FAMILIES[r["family"]] == g["family"]
+        assert r["fallback_used"] == 0 and r["executed_mode"] == r["mode"]
+        assert r["fp16_latency_ms"] > 0 and r["mode_latency_ms"] > 0
+        assert abs(r["speedup"] - r["fp16_latency_ms"] / r["mode_latency_ms"]) < 1e-9
+    modes = {ctl.MODES[r["mode"]] for r in rows}
+    assert {"int8_continuous_batching", "gptq4", "speculative_decoding", "int8",
+            "gptq_prefix_caching"} <= modes
+    spec = [r for r in rows if ctl.MODES[r["mode"]] == "speculative_decoding"]
+    assert all(r["spec_proposed"] > 0 for r in spec)
+    pc = [r for r in rows if ctl.MODES[r["mode"]] == "gptq_prefix_caching"]
+    assert pc[-1]["prefix_hit_tokens"] == 96  # shared 96-token prefix reused (6 blocks)
+    # reference aggregation (sim.cpp:149-207)
+    n = len(rows)
+    assert summ["request_count"] == n and summ["fallback_count"] == 0
+    assert abs(summ["mean_speedup"] - sum(r["speedup"] for r in rows) / n) < 1e-9
+    agg = sum(r["fp16_latency_ms"] for r in rows) / sum(r["mode_latency_ms"] for r in rows)
+    assert abs(summ["aggregate_latency_speedup"] - agg) < 1e-9
+    assert summ["generated_tokens"] == sum(r["output_tokens"] for r in rows)
+
+
+def test_single_request_cohort(eng):
+    # rule 1 (batch_pressure >= 2) routes to INT8 + continuous batching; a
+    # cohort of one still runs through the batch path, not the FP16 fallback
+    line = ctl.format_trace_line(dict(request_id="solo", prompt_tokens=40, expected_output_tokens=5,
+                                      batch_pressure=2, workload_tag=None))
+    rows, summ = execute_trace(eng, line + "\n")
+    assert ctl.MODES[rows[0]["executed_mode"]] == "int8_continuous_batching"
+    assert summ["fallback_count"] == 0
