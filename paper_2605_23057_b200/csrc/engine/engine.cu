@@ -1109,6 +1109,9 @@ int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n, int3
       // test entry: weights arrive row-major; build the decode layout first
       uint8_t* tf = dalloc<uint8_t>(tf_bytes(wtype, n, k));
       launch_repack_tf(wtype, w, n, k, tf, st);
+      // the GEMV's producer streams weights BEFORE griddepcontrol.wait (PDL), so
+      // freshly repacked weights must be complete before it launches
+      MSW_CUDA(cudaStreamSynchronize(st));
       W.w_tf = tf;
       launch_gemv(W, kProPlain, kEpiStore, x, t, nullptr, 1e-5f, y, st);
       MSW_CUDA(cudaStreamSynchronize(st));
