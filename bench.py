@@ -160,6 +160,22 @@ def time_dominant_kernel(iters: int = 50):
             "gbs": algo_bytes / (ms * 1e-3) / 1e9}
 
 
+def profiled_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel, from the committed `ncu --set full` capture (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_w4_gemv_gate_up.txt")
+    try:
+        vals = {}
+        for line in open(path):
+            parts = line.split()
+            if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[parts[2]]
+                vals[parts[0]] = float(parts[1]) * scale
+        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    except Exception:
+        return None
+
+
 def cpu_baseline_8b(new_tokens: int = 3, prompt_len: int = 4):
     """CPU oracle (C port, OpenMP over all host cores), 8B shape, W4 mode."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -326,7 +342,8 @@ def run_ours(args):
                 "d2h_bytes_per_step": NEW * 4 * len(MODES)},
         "per_mode": per_mode,
         "roofline": {"bound": "hbm", "achieved": kern["gbs"], "peak": peak, "unit": "GB/s",
-                     "frac": kern["gbs"] / peak, "traffic": None, "kernel": kern["kernel"],
+                     "frac": kern["gbs"] / peak, "traffic": profiled_traffic(),
+                     "kernel": kern["kernel"],
                      "kernel_ms": kern["ms"], "bytes_per_launch": kern["bytes"],
                      "peak_source": peak_kind,
                      "decode_step_frac": per_mode["gptq4"]["hbm_frac_of_measured"]},

@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   constexpr int RS = D + kKvPad;  // staged row stride (halves)
   extern __shared__ __align__(16) half kv_smem[];  // [warp][K|V][32][RS]
   __shared__ __align__(16) float qs[G][D];
-  __shared__ float knew[D], vnew[D];
+  __shared__ __align__(16) half knew[D], vnew[D];
   __shared__ float wm[kAttnWarps][G], wl[kAttnWarps][G];
   __shared__ float wacc[kAttnWarps][G][D];
   __shared__ int is_last;
@@ -324,14 +324,14 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   half* sK = kv_smem + size_t(warp) * 2 * 32 * RS;
   half* sV = sK + 32 * RS;
 
-  // stage one 32-position tile of K and V rows (lane = position) into smem
+  // stage one 32-position tile (lane = position) of cached K / V rows
   auto stage_tile = [&](int base) {
     const int p = base + lane;
     if (p < end && p != p_self) {
       const int sl = bt[p >> 4] * kKvBlock + (p & 15);
       const half* kr = kc + kv_off(sl, hk, Hk, D);
       const half* vr = vc + kv_off(sl, hk, Hk, D);
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < D / 8; ++c) {
         cp_async16(sK + lane * RS + c * 8, kr + c * 8);
         cp_async16(sV + lane * RS + c * 8, vr + c * 8);
@@ -343,38 +343,36 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 
   pdl_wait();
   pdl_trigger();
-  {
-    const int width = (Hq + 2 * Hk) * D;
-    const float* row = qkv + size_t(t) * width;
+  {  // RoPE of this kv head's G query heads and the new key (table lookup)
+    const float* row = qkv + size_t(t) * (Hq + 2 * Hk) * D;
     const float2* rp = rope + size_t(p_self) * (D / 2);
     for (int i = threadIdx.x; i < (G + 1) * (D / 2); i += blockDim.x) {
       const int h = i / (D / 2), j = i % (D / 2);
       const float* src = h < G ? row + size_t(hk * G + h) * D : row + size_t(Hq + hk) * D;
       const float2 r = rp[j];
-      const float cs = r.x, sn = r.y;
       const float x0 = src[j], x1 = src[j + D / 2];
-      const float y0 = __half2float(__float2half_rn(__fsub_rn(__fmul_rn(x0, cs), __fmul_rn(x1, sn))));
-      const float y1 = __half2float(__float2half_rn(__fadd_rn(__fmul_rn(x1, cs), __fmul_rn(x0, sn))));
+      const half y0 = __float2half_rn(__fsub_rn(__fmul_rn(x0, r.x), __fmul_rn(x1, r.y)));
+      const half y1 = __float2half_rn(__fadd_rn(__fmul_rn(x1, r.x), __fmul_rn(x0, r.y)));
       if (h < G) {
-        qs[h][j] = y0;
-        qs[h][j + D / 2] = y1;
+        qs[h][j] = __half2float(y0);
+        qs[h][j + D / 2] = __half2float(y1);
       } else {
         knew[j] = y0;
         knew[j + D / 2] = y1;
       }
     }
     for (int d = threadIdx.x; d < D; d += blockDim.x)
-      vnew[d] = __half2float(__float2half_rn(row[size_t(Hq + Hk + hk) * D + d]));
+      vnew[d] = __float2half_rn(row[size_t(Hq + Hk + hk) * D + d]);
   }
   __syncthreads();
   if (sp == 0) {
     const size_t off = kv_off(slot[t], hk, Hk, D);
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
-      kc[off + d] = __float2half_rn(knew[d]);
-      vc[off + d] = __float2half_rn(vnew[d]);
+      kc[off + d] = knew[d];
+      vc[off + d] = vnew[d];
     }
   }
-  const float scale = 1.0f / sqrtf(float(D));
+  const float scale = rsqrtf(float(D));
   float m[G], l[G], acc[G][DPL];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -383,38 +381,39 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 #pragma unroll
     for (int d = 0; d < DPL; ++d) acc[g][d] = 0.0f;
   }
+#pragma unroll 1
   for (int base = first; base < end; base += kAttnWarps * 32) {
     if (base != first) {
       __syncwarp();
       stage_tile(base);
     }
     cp_async_wait_all();
-    __syncwarp();
     const int p = base + lane;
+    if (p == p_self) {  // the new token's row comes from smem, not the cache
+#pragma unroll 1
+      for (int c = 0; c < D / 8; ++c) {
+        *reinterpret_cast<uint4*>(sK + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(knew + c * 8);
+        *reinterpret_cast<uint4*>(sV + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(vnew + c * 8);
+      }
+    }
+    __syncwarp();
     float s[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) s[g] = 0.0f;
     if (p < end) {
-      if (p == p_self) {
-#pragma unroll 4
-        for (int d = 0; d < D; ++d)
+      const half* kr = sK + lane * RS;
+#pragma unroll 1
+      for (int c = 0; c < D / 8; ++c) {
+        const uint4 kv = *reinterpret_cast<const uint4*>(kr + c * 8);
+        const half2* kh = reinterpret_cast<const half2*>(&kv);
+        const float2 k0 = __half22float2(kh[0]), k1 = __half22float2(kh[1]);
+        const float2 k2 = __half22float2(kh[2]), k3 = __half22float2(kh[3]);
 #pragma unroll
-          for (int g = 0; g < G; ++g) s[g] = fmaf(qs[g][d], knew[d], s[g]);
-      } else {
-        const half* kr = sK + lane * RS;
-#pragma unroll 2
-        for (int c = 0; c < D / 8; ++c) {
-          const uint4 kv = *reinterpret_cast<const uint4*>(kr + c * 8);
-          const half2* kh = reinterpret_cast<const half2*>(&kv);
-          const float2 k0 = __half22float2(kh[0]), k1 = __half22float2(kh[1]);
-          const float2 k2 = __half22float2(kh[2]), k3 = __half22float2(kh[3]);
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const float4 q0 = *reinterpret_cast<const float4*>(&qs[g][c * 8]);
-            const float4 q1 = *reinterpret_cast<const float4*>(&qs[g][c * 8 + 4]);
-            s[g] = fmaf(q0.x, k0.x, fmaf(q0.y, k0.y, fmaf(q0.z, k1.x, fmaf(q0.w, k1.y, s[g]))));
-            s[g] = fmaf(q1.x, k2.x, fmaf(q1.y, k2.y, fmaf(q1.z, k3.x, fmaf(q1.w, k3.y, s[g]))));
-          }
+        for (int g = 0; g < G; ++g) {
+          const float4 q0 = *reinterpret_cast<const float4*>(&qs[g][c * 8]);
+          const float4 q1 = *reinterpret_cast<const float4*>(&qs[g][c * 8 + 4]);
+          s[g] = fmaf(q0.x, k0.x, fmaf(q0.y, k0.y, fmaf(q0.z, k1.x, fmaf(q0.w, k1.y, s[g]))));
+          s[g] = fmaf(q1.x, k2.x, fmaf(q1.y, k2.y, fmaf(q1.z, k3.x, fmaf(q1.w, k3.y, s[g]))));
         }
       }
     }
@@ -423,28 +422,23 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     for (int g = 0; g < G; ++g) {
       const float sv = p < end ? s[g] * scale : -INFINITY;
       const float mn = fmaxf(m[g], warp_max(sv));
-      const float corr = expf(m[g] - mn);
-      e[g] = p < end ? expf(sv - mn) : 0.0f;
+      const float corr = __expf(m[g] - mn);
+      e[g] = p < end ? __expf(sv - mn) : 0.0f;
       l[g] = l[g] * corr + warp_sum(e[g]);
       m[g] = mn;
 #pragma unroll
       for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
     }
     const int n_here = min(32, end - base);
-#pragma unroll 2
+#pragma unroll 1
     for (int j = 0; j < n_here; ++j) {
       float vf[DPL];
-      if (base + j == p_self) {
+      const half2* vh = reinterpret_cast<const half2*>(sV + j * RS + lane * DPL);
 #pragma unroll
-        for (int d = 0; d < DPL; ++d) vf[d] = vnew[lane * DPL + d];
-      } else {
-        const half2* vh = reinterpret_cast<const half2*>(sV + j * RS + lane * DPL);
-#pragma unroll
-        for (int d = 0; d < DPL / 2; ++d) {
-          const float2 f = __half22float2(vh[d]);
-          vf[2 * d] = f.x;
-          vf[2 * d + 1] = f.y;
-        }
+      for (int d = 0; d < DPL / 2; ++d) {
+        const float2 f = __half22float2(vh[d]);
+        vf[2 * d] = f.x;
+        vf[2 * d + 1] = f.y;
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
@@ -465,6 +459,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     for (int d = 0; d < DPL; ++d) wacc[warp][g][lane * DPL + d] = acc[g][d];
   }
   __syncthreads();
+#pragma unroll 1
   for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
     const int g = i / D, d = i % D;
     float M = -INFINITY;
@@ -472,13 +467,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     float L = 0.0f, A = 0.0f;
     if (M != -INFINITY)
       for (int w = 0; w < kAttnWarps; ++w) {
-        const float f = expf(wm[w][g] - M);
+        const float f = __expf(wm[w][g] - M);
         L += wl[w][g] * f;
         A += wacc[w][g][d] * f;
       }
     const int hq = hk * G + g;
     if (active == 1) {
-      o[(size_t(t) * Hq + hq) * D + d] = L > 0.0f ? A / L : 0.0f;
+      o[(size_t(t) * Hq + hq) * D + d] = L > 0.0f ? __fdividef(A, L) : 0.0f;
     } else {
       const size_t idx = (size_t(t) * Hq + hq) * nsplit + sp;
       part_o[idx * D + d] = A;
@@ -500,6 +495,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   __syncthreads();
   if (!is_last) return;
   __threadfence();
+#pragma unroll 1
   for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
     const int g = i / D, d = i % D;
     const size_t base = (size_t(t) * Hq + hk * G + g) * nsplit;
@@ -509,11 +505,11 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     for (int s2 = 0; s2 < active; ++s2) {
       const float ms = __ldcg(&part_ml[(base + s2) * 2]);
       if (ms == -INFINITY) continue;
-      const float f = expf(ms - M);
+      const float f = __expf(ms - M);
       L += __ldcg(&part_ml[(base + s2) * 2 + 1]) * f;
       A += __ldcg(&part_o[(base + s2) * D + d]) * f;
     }
-    o[(size_t(t) * Hq + hk * G + g) * D + d] = L > 0.0f ? A / L : 0.0f;
+    o[(size_t(t) * Hq + hk * G + g) * D + d] = L > 0.0f ? __fdividef(A, L) : 0.0f;
   }
 }
 
