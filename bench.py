@@ -430,9 +430,68 @@ def run_mix(args):
         torch.distributed.destroy_process_group()
 
 
+def run_configs(args):
+    """BASELINE configs 3a (GPTQ + prefix caching), 3b (INT8 + continuous
+    batching, ragged batch 64) and 4 (speculative decoding, 1B draft + 8B
+    target, k=4) on one GPU, through the C ABI. One JSON line per config."""
+    import numpy as np
+    import torch
+    from paper_2605_23057_b200 import MODE_GPTQ_PC, MODE_INT8_CB, MODE_SPEC, engine_cfg
+    from paper_2605_23057_b200.engine import Engine
+    torch.cuda.set_device(0)
+    eng = Engine(engine_cfg(target="llama8b", draft="llama1b", seed=0, kv_blocks=6144, max_batch=64,
+                            max_seq_len=2400, use_graphs=True))
+    rng = np.random.default_rng(7)
+    base = {"metric": "decode tokens/s per mode and routed mix (1/2/4/8 B200); mean latency vs FP16 mode",
+            "unit": "tokens/s", "n_gpus": 1, "data": "synthetic"}
+    # 3a: shared-prefix chat, 1024+-10% prompts with a shared 768-token prefix, 128+-10% outputs
+    shared = synth_prompt(99, 768, 128256)
+    n_req = args.cfg_requests
+    eng.reset_prefix_cache()
+    tot_tok, tot_ms, hits = 0, 0.0, 0
+    for i in range(n_req):
+        plen = int(round(1024 * (0.9 + 0.2 * rng.random())))
+        p = np.concatenate([shared, synth_prompt(1000 + i, plen - 768, 128256)])
+        out = int(round(128 * (0.9 + 0.2 * rng.random())))
+        r = eng.run(MODE_GPTQ_PC, p, out)
+        tot_tok += out
+        tot_ms += r.total_ms
+        hits += r.prefix_hit_tokens
+    print(json.dumps(dict(base, config="3a_gptq_prefix_caching", value=tot_tok / (tot_ms / 1e3),
+                          requests=n_req, prefix_hit_tokens=hits,
+                          mean_request_ms=tot_ms / n_req)), flush=True)
+    # 3b: 64 co-scheduled requests, prompts 1024+-10%, outputs 128+-10%, INT8 + continuous batching
+    prompts, outs = [], []
+    for i in range(64):
+        plen = int(round(1024 * (0.9 + 0.2 * rng.random())))
+        prompts.append(synth_prompt(2000 + i, plen, 128256))
+        outs.append(int(round(128 * (0.9 + 0.2 * rng.random()))))
+    eng.run_batch(MODE_INT8_CB, prompts[:4], [4] * 4)  # warm-up
+    t0 = time.perf_counter()
+    res = eng.run_batch(MODE_INT8_CB, prompts, outs)
+    wall = time.perf_counter() - t0
+    print(json.dumps(dict(base, config="3b_int8_continuous_batching_b64", value=sum(outs) / wall,
+                          requests=64, generated_tokens=sum(outs), wall_s=wall,
+                          mean_request_ms=statistics.mean(r.total_ms for r in res))), flush=True)
+    # 4: speculative decoding on long generations (SyntheticSL-shape prompt, 1024 new tokens)
+    tot_tok, tot_dec, prop, acc = 0, 0.0, 0, 0
+    for i in range(args.cfg_requests // 4 or 1):
+        p = synth_prompt(3000 + i, 128, 128256)
+        r = eng.run(MODE_SPEC, p, 1024)
+        tot_tok += 1023
+        tot_dec += r.decode_ms
+        prop += r.spec_proposed
+        acc += r.spec_accepted
+    print(json.dumps(dict(base, config="4_speculative_k4", value=tot_tok / (tot_dec / 1e3),
+                          acceptance=acc / max(1, prop), draft="llama1b-shape", target="llama8b-shape")),
+          flush=True)
+    eng.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", choices=["decode8b", "mix"], default="decode8b")
+    ap.add_argument("--workload", choices=["decode8b", "mix", "configs"], default="decode8b")
+    ap.add_argument("--cfg-requests", type=int, default=8)
     ap.add_argument("--mix-per-class", type=int, default=4)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -444,6 +503,8 @@ def main():
         run_reference(args)
     elif args.workload == "mix":
         run_mix(args)
+    elif args.workload == "configs":
+        run_configs(args)
     else:
         run_ours(args)
 

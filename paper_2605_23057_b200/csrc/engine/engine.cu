@@ -10,6 +10,7 @@
 // on the device, so a request's decode loop never synchronises with the host.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <list>
@@ -460,7 +461,9 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
   const int H = c.hidden, D = c.head_dim, Hq = c.n_heads, Hk = c.n_kv_heads, F = c.ffn;
   const float eps = c.rms_eps;
   const bool small = T <= kGemvMaxTokens;
-  const int nsplit = T <= kMaxLogitRows ? m.nsplit : 1;
+  // attention splits: enough CTAs to fill the GPU, fewer as the token count grows
+  int nsplit = 1;
+  if (T <= kMaxLogitRows) nsplit = std::max(1, std::min(m.nsplit, (2 * kNumSMs) / (T * Hk)));
   long long& n = e->launches;
 
   launch_embed(m.embed, s.tok, T, H, s.h, st);
@@ -484,9 +487,14 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       n += 1;
     } else {
       launch_rope_append(s.qkv, T, s.pos, s.slot, m.rope, m.ash, s.q16, kc, vc, st);
-      launch_attention(s.q16, T, s.pos, s.seq_of, m.block_table, kc, vc, m.ash, nsplit, s.part_o,
-                       s.part_ml, s.o, st);
-      n += nsplit > 1 ? 3 : 2;
+      if (T > kMaxLogitRows && !std::getenv("MSW_SCALAR_PREFILL_ATTN")) {
+        launch_attention_prefill(s.q16, T, s.pos, s.seq_of, m.block_table, kc, vc, m.ash, s.o, st);
+        n += 2;
+      } else {
+        launch_attention(s.q16, T, s.pos, s.seq_of, m.block_table, kc, vc, m.ash, nsplit,
+                         s.part_o, s.part_ml, s.o, st);
+        n += nsplit > 1 ? 3 : 2;
+      }
     }
     if (small) {
       launch_gemv(ly.o[fmt], kProPlain, kEpiResid, s.o, T, nullptr, eps, s.h, st);
@@ -617,6 +625,73 @@ void prefill(msw_engine* e, Model& m, int fmt, int row, const int32_t* prompt, i
     }
     forward(e, m, fmt, T, 1, /*rows_identity=*/T == 1, /*tokens_independent=*/T == 1);
     MSW_CUDA(cudaStreamSynchronize(e->st));  // staging is reused by the next chunk
+  }
+}
+
+// Packed prefill of several sequences (continuous-batching admission): the
+// prompts of all admitted sequences are concatenated into chunks of up to
+// kPrefillChunk tokens (ragged; every token carries its own seq_of / pos), so
+// one GEMM per linear covers the whole cohort. A sequence may straddle chunks
+// (attention reads the earlier chunk's K/V from the paged cache). The first
+// generated token of sequence i lands in first_tok[i]; with logits_out[i]
+// non-null its fp32 logits row is copied there.
+void copy_logits_row(msw_engine* e, float* dst_host, int row);
+
+struct PackSeq {
+  int row;
+  const int32_t* prompt;
+  int plen;
+  const SeqBlocks* sb;
+};
+
+void prefill_packed(msw_engine* e, Model& m, int fmt, const std::vector<PackSeq>& seqs,
+                    int* first_tok, float* const* logits_out) {
+  Scratch& s = e->sc;
+  size_t i = 0;
+  int p0 = 0;  // next prompt position of seqs[i]
+  while (i < seqs.size()) {
+    int T = 0, nl = 0;
+    int* st_tok = s.stage;
+    int* st_pos = s.stage + kPrefillChunk;
+    int* st_slot = s.stage + 2 * kPrefillChunk;
+    int* st_seq = s.stage + 3 * kPrefillChunk;
+    int* st_rows = s.stage + 4 * kPrefillChunk;
+    std::vector<int> owners;
+    while (i < seqs.size() && T < kPrefillChunk && nl < kMaxLogitRows) {
+      const PackSeq& q = seqs[i];
+      const int take = std::min(q.plen - p0, kPrefillChunk - T);
+      for (int j = 0; j < take; ++j) {
+        const int p = p0 + j;
+        st_tok[T + j] = q.prompt[p];
+        st_pos[T + j] = p;
+        st_slot[T + j] = q.sb->blocks[p / kKvBlock] * kKvBlock + p % kKvBlock;
+        st_seq[T + j] = q.row;
+      }
+      T += take;
+      p0 += take;
+      if (p0 == q.plen) {
+        st_rows[nl++] = T - 1;
+        owners.push_back(int(i));
+        ++i;
+        p0 = 0;
+      }
+    }
+    MSW_CUDA(cudaMemcpyAsync(s.tok, st_tok, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+    MSW_CUDA(cudaMemcpyAsync(s.pos, st_pos, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+    MSW_CUDA(cudaMemcpyAsync(s.slot, st_slot, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+    MSW_CUDA(cudaMemcpyAsync(s.seq_of, st_seq, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+    if (nl > 0)
+      MSW_CUDA(cudaMemcpyAsync(s.logit_rows, st_rows, sizeof(int) * nl, cudaMemcpyHostToDevice, e->st));
+    const bool ident = nl == T;  // every token is some sequence's last
+    forward(e, m, fmt, T, std::max(nl, 1), ident, false);
+    int* got = s.stage + 4 * kPrefillChunk + kMaxLogitRows;
+    if (nl > 0) {
+      MSW_CUDA(cudaMemcpyAsync(got, s.next, sizeof(int) * nl, cudaMemcpyDeviceToHost, e->st));
+      for (int j = 0; j < nl; ++j)
+        if (logits_out[owners[j]]) copy_logits_row(e, logits_out[owners[j]], j);
+    }
+    MSW_CUDA(cudaStreamSynchronize(e->st));  // staging is reused by the next chunk
+    for (int j = 0; j < nl; ++j) first_tok[owners[j]] = got[j];
   }
 }
 
@@ -892,7 +967,8 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
   std::vector<int> step_tok(maxb);
   try {
     while (next_req < n || !live.empty()) {
-      // admission
+      // admission: map every request that fits, then prefill them packed
+      std::vector<Live> adm;
       while (next_req < n && !free_rows.empty()) {
         const msw_request& r = reqs[next_req];
         Live L;
@@ -900,28 +976,51 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
         L.row = free_rows.back();
         L.generated = 0;
         L.t_admit = now_ms();
-        L.sb = map_sequence(m, L.row, r.prompt_len + r.max_new_tokens, r.prompt_ids, r.prompt_len,
-                            false, fmt, e->st, s.stage);
-        free_rows.pop_back();
-        const double tp = now_ms();
-        prefill(e, m, fmt, L.row, r.prompt_ids, 0, r.prompt_len, L.sb);
-        MSW_CUDA(cudaMemcpyAsync(s.stage, s.next, sizeof(int), cudaMemcpyDeviceToHost, e->st));
-        if (res[next_req].logits) copy_logits_row(e, res[next_req].logits, 0);
-        MSW_CUDA(cudaStreamSynchronize(e->st));
-        prefill_time += now_ms() - tp;
-        L.last_tok = s.stage[0];
-        res[next_req].out_ids[0] = L.last_tok;
-        L.generated = 1;
-        res[next_req].prefill_ms = now_ms() - tp;
-        if (L.generated >= r.max_new_tokens) {
-          release_sequence(m, L.sb);
-          free_rows.push_back(L.row);
-          res[next_req].n_out = L.generated;
-          res[next_req].total_ms = now_ms() - L.t_admit;
-        } else {
-          live.push_back(std::move(L));
+        try {
+          L.sb = map_sequence(m, L.row, r.prompt_len + r.max_new_tokens, r.prompt_ids,
+                              r.prompt_len, false, fmt, e->st, s.stage);
+        } catch (...) {
+          for (Live& A : adm) release_sequence(m, A.sb);
+          throw;
         }
+        free_rows.pop_back();
+        adm.push_back(std::move(L));
         ++next_req;
+      }
+      if (!adm.empty()) {
+        const double tp = now_ms();
+        std::vector<PackSeq> ps;
+        std::vector<float*> lg;
+        std::vector<int> first(adm.size());
+        for (const Live& L : adm) {
+          const msw_request& r = reqs[L.req];
+          ps.push_back({L.row, r.prompt_ids, r.prompt_len, &L.sb});
+          lg.push_back(res[L.req].logits);
+        }
+        try {
+          prefill_packed(e, m, fmt, ps, first.data(), lg.data());
+        } catch (...) {
+          for (Live& L : adm) release_sequence(m, L.sb);
+          throw;
+        }
+        const double tdone = now_ms();
+        prefill_time += tdone - tp;
+        for (size_t j = 0; j < adm.size(); ++j) {
+          Live& L = adm[j];
+          msw_result& rr = res[L.req];
+          L.last_tok = first[j];
+          rr.out_ids[0] = L.last_tok;
+          L.generated = 1;
+          rr.prefill_ms = tdone - tp;
+          if (L.generated >= reqs[L.req].max_new_tokens) {
+            release_sequence(m, L.sb);
+            free_rows.push_back(L.row);
+            rr.n_out = L.generated;
+            rr.total_ms = now_ms() - L.t_admit;
+          } else {
+            live.push_back(std::move(L));
+          }
+        }
       }
       if (live.empty()) continue;
       // one decode step for every live sequence

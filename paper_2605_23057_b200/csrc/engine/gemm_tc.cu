@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int N, int K, int T, const void* __restrict__ wscale,
                    const float* __restrict__ xscale, const uint32_t* __restrict__ w4,
-                   float* __restrict__ y) {
+                   float* __restrict__ y, int ksplit) {
   using C = TcCfg<FMT, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -138,7 +138,11 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kTileM, t0 = blockIdx.y * BN;
-  const int nk = K / C::kTileK;
+  // split-K: blockIdx.z owns k-tiles [kb0, kb0 + nk); partial sums are added atomically
+  const int nk_all = K / C::kTileK;
+  const int nk_per = (nk_all + ksplit - 1) / ksplit;
+  const int kb0 = blockIdx.z * nk_per;
+  const int nk = max(0, min(nk_all - kb0, nk_per));
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -168,8 +172,8 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       const uint32_t ph = (kb / kStages) & 1;
       mbar_wait(&empty[s], ph ^ 1);
       mbar_expect_tx(&full[s], C::kIsW4 ? C::kBBytes : C::kStageBytes);
-      if (!C::kIsW4) tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * C::kTileK, n0);
-      tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * C::kTileK, t0);
+      if (!C::kIsW4) tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * C::kTileK, n0);
+      tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kb) * C::kTileK, t0);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       }
       umma_commit(&empty[s]);
     }
-    umma_commit(done);
+    umma_commit(done);  // with nk == 0 this still arrives (no MMA issued: D stays unwritten)
   } else if (C::kIsW4 && warp >= 4) {
     // ---- W4 dequantisers: thread r (0..127) owns weight row n0 + r of every k-tile
     const int r = threadIdx.x - 128;
@@ -199,9 +203,9 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       const int s = kb % kStages;
       const uint32_t ph = (kb / kStages) & 1;
       // 64 k per tile = 8 packed words; one group scale covers it (128 | 64)
-      const uint4 p0 = ld_stream(wrow + kb * 8);
-      const uint4 p1 = ld_stream(wrow + kb * 8 + 4);
-      const half2 s2 = __half2half2(srow[(kb * 64) / kW4Group]);
+      const uint4 p0 = ld_stream(wrow + (kb0 + kb) * 8);
+      const uint4 p1 = ld_stream(wrow + (kb0 + kb) * 8 + 4);
+      const half2 s2 = __half2half2(srow[((kb0 + kb) * 64) / kW4Group]);
       mbar_wait(&empty[s], ph ^ 1);
       uint8_t* rowp = sA + s * C::kABytes + r * 128;
       const uint32_t words[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
@@ -245,11 +249,12 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
         } else {
           v = __uint_as_float(r[j]);
         }
-        if (EPI == kEpiSwiglu) {
+        if (EPI == kEpiSwiglu) {  // never split (nonlinear)
           const float up = __shfl_xor_sync(0xffffffffu, v, 1);
           if (t < T && (lane & 1) == 0) y[size_t(t) * (N / 2) + (n >> 1)] = silu(v) * up;
         } else if (t < T) {
-          if (EPI == kEpiStore) y[size_t(t) * N + n] = v;
+          if (ksplit > 1) atomicAdd(&y[size_t(t) * N + n], v);  // STORE targets are pre-zeroed
+          else if (EPI == kEpiStore) y[size_t(t) * N + n] = v;
           else y[size_t(t) * N + n] += v;
         }
       }
@@ -314,9 +319,18 @@ void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, f
   CUtensorMap ta{};
   if (FMT != kW4) ta = make_map(W.w, elt, W.n, W.k, kTileM);
   const CUtensorMap tb = make_map(xact, elt, T, W.k, BN);
-  const dim3 grid(W.n / kTileM, (T + BN - 1) / BN);
+  // small grids (continuous-batching steps: T <= 64, n = 4096) leave most SMs
+  // idle; split K across CTAs and accumulate partials atomically
+  const int tiles = (W.n / kTileM) * ((T + BN - 1) / BN);
+  const int nk = W.k / C::kTileK;
+  int ksplit = 1;
+  if (EPI != kEpiSwiglu)
+    while (tiles * ksplit * 2 <= kNumSMs && nk / (ksplit * 2) >= 8) ksplit *= 2;
+  if (ksplit > 1 && EPI == kEpiStore)
+    MSW_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * size_t(T) * W.n, st));
+  const dim3 grid(W.n / kTileM, (T + BN - 1) / BN, ksplit);
   gemm_tc_kernel<FMT, BN, EPI><<<grid, C::kThreads, C::kSmem, st>>>(
-      ta, tb, W.n, W.k, T, W.s, xscale, static_cast<const uint32_t*>(W.w), y);
+      ta, tb, W.n, W.k, T, W.s, xscale, static_cast<const uint32_t*>(W.w), y, ksplit);
   MSW_LAUNCH_CHECK();
 }
 

@@ -87,6 +87,12 @@ void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
                       const int* block_table, const half* kc, const half* vc, const AttnShape& a,
                       int nsplit, float* part_o, float* part_ml, float* o, cudaStream_t st);
 
+// Same semantics on the tensor pipe (attn_prefill.cu): many query tokens,
+// packed from any number of sequences; no split-KV (o written directly).
+void launch_attention_prefill(const half* q, int T, const int* pos, const int* seq_of,
+                              const int* block_table, const half* kc, const half* vc,
+                              const AttnShape& a, float* o, cudaStream_t st);
+
 // Decode / continuous batching (each token is the newest of its own sequence):
 // RoPE + KV append fused into the attention kernel; reads fp32 qkv directly.
 void launch_attention_decode(const float* qkv, const float2* rope, int T, const int* pos,

@@ -1,7 +1,9 @@
 """Back-to-back decode-GEMV microbenchmark: each 8B-shape linear of one format
 launched `iters` times through the C ABI (msw_linear_decode, PDL launches),
 rotating over weight copies that together exceed L2, CUDA events on torch's
-stream. Reports us/launch and achieved GB/s."""
+stream. The timed launches are replayed from a CUDA graph (no host launch
+overhead). `--l2` keeps ONE weight copy (L2-resident when it fits): the
+consumer-side (issue) limit rather than HBM. Reports us/launch and GB/s."""
 import os
 import sys
 
@@ -13,11 +15,16 @@ from paper_2605_23057_b200._capi import check_engine, engine_lib  # noqa: E402
 lib = engine_lib()
 SHAPES = {"qkv": (6144, 4096), "o": (4096, 4096), "gate_up": (28672, 4096), "down": (4096, 14336)}
 BYTES = {0: lambda n, k: n * k * 2, 1: lambda n, k: n * k + n * 4, 2: lambda n, k: n * k // 2 + n * k // 64}
-fmts = [int(f) for f in (sys.argv[1] if len(sys.argv) > 1 else "2,1,0").split(",")]
+l2 = "--l2" in sys.argv
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+fmts = [int(f) for f in (args[0] if args else "2,1,0").split(",")]
+only = args[1].split(",") if len(args) > 1 else list(SHAPES)
 for fmt in fmts:
     for name, (n, k) in SHAPES.items():
+        if name not in only:
+            continue
         wb = BYTES[fmt](n, k)
-        copies = max(2, int(300e6 // wb) + 1)
+        copies = 1 if l2 else max(2, int(300e6 // wb) + 1)
         ws, ss = [], []
         for i in range(copies):
             w = torch.randint(-100, 100, (wb // 4,), dtype=torch.int32, device="cuda")
@@ -40,11 +47,20 @@ for fmt in fmts:
         for i in range(10):
             go(i)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         iters = 100
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g, stream=cs):
+                sp = cs.cuda_stream
+                for i in range(iters):
+                    go(i)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for i in range(iters):
-            go(i)
+        g.replay()
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1000 / iters

@@ -7,8 +7,9 @@ Bars (DESIGN.md "Numerics contract"):
   * speculative decoding: tokens == target greedy, and round/proposal/accept
     counts equal the oracle's (they are a deterministic function of tokens);
   * logits: max |gpu - oracle| / std(oracle logits) < 2e-3 (FP16),
-    < 1e-2 (W4: fp16 partial sums) — per generated step. INT8: < 5e-3 (a 1-ulp
-    difference in an fp32 activation can flip one int8 rounding; tokens stay exact).
+    < 1e-2 (W4: fp16 partial sums) — per generated step. INT8: < 1e-2 (a 1-ulp
+    difference in an fp32 activation can flip one int8 activation rounding, and
+    the tensor-core prefill attention rounds P to fp16; tokens stay exact).
 """
 import numpy as np
 import pytest
@@ -21,7 +22,7 @@ from paper_2605_23057_b200.engine import Engine
 
 pytestmark = pytest.mark.gpu
 
-TOL = {MODE_FP16: 2e-3, MODE_INT8: 5e-3, MODE_GPTQ4: 1e-2, MODE_GPTQ_PC: 1e-2, MODE_INT8_CB: 5e-3,
+TOL = {MODE_FP16: 2e-3, MODE_INT8: 1e-2, MODE_GPTQ4: 1e-2, MODE_GPTQ_PC: 1e-2, MODE_INT8_CB: 1e-2,
        MODE_SPEC: 2e-3}
 ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_GPTQ_PC: 2, MODE_INT8_CB: 1}
 
@@ -121,3 +122,52 @@ def test_error_codes(pair):
     with pytest.raises(MswError) as e:
         eng.run(MODE_FP16, np.arange(10, dtype=np.int32), 5000)
     assert e.value.code == 3
+
+
+@pytest.fixture(scope="module")
+def long_pair(cuda_ok):
+    cfg = engine_cfg(target="tiny128", draft=None, seed=11, kv_blocks=2048, max_seq_len=4096)
+    eng = Engine(cfg)
+    orc = O.OracleModel(model_cfg("tiny128"), seed=11, max_ctx=4096)
+    yield eng, orc
+    eng.close()
+
+
+@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8])
+def test_long_prefill_crosses_chunks(long_pair, mode):
+    # 2100-token prompt: tensor-core prefill attention over 33 KV tiles, and a
+    # second 2048-token prefill chunk reading the first chunk's paged K/V
+    eng, orc = long_pair
+    p = prompt(77 + mode, 2100, eng.vocab)
+    r = eng.run(mode, p, 6, want_logits=True)
+    toks, lg = orc.generate(ORACLE_MODE[mode], p, 6, want_logits=True)
+    assert np.array_equal(r.tokens, toks)
+    _check_logits(r.logits, lg, TOL[mode])
+
+
+def test_continuous_batching_packed_prefill_straddles_chunks(long_pair):
+    # ~2.8K prompt tokens packed into two prefill chunks; sequences straddle the
+    # chunk boundary and tensor-core attention windows hold several sequences
+    eng, orc = long_pair
+    rng = np.random.default_rng(21)
+    plens = [int(x) for x in rng.integers(150, 420, size=10)]
+    nnew = [int(x) for x in rng.integers(2, 12, size=10)]
+    prompts = [prompt(900 + i, plens[i], eng.vocab) for i in range(10)]
+    res = eng.run_batch(MODE_INT8_CB, prompts, nnew, want_logits=True)
+    for i, r in enumerate(res):
+        toks, lg = orc.generate(1, prompts[i], nnew[i], want_logits=True)
+        assert np.array_equal(r.tokens, toks), i
+        _check_logits(r.logits, lg, TOL[MODE_INT8_CB])
+
+
+def test_continuous_batching_more_requests_than_rows(long_pair):
+    # 70 requests > 64 block-table rows: admission waits for retirements
+    eng, orc = long_pair
+    rng = np.random.default_rng(5)
+    plens = [int(x) for x in rng.integers(3, 24, size=70)]
+    nnew = [int(x) for x in rng.integers(1, 6, size=70)]
+    prompts = [prompt(3000 + i, plens[i], eng.vocab) for i in range(70)]
+    res = eng.run_batch(MODE_INT8_CB, prompts, nnew)
+    for i, r in enumerate(res):
+        toks, _ = orc.generate(1, prompts[i], nnew[i])
+        assert np.array_equal(r.tokens, toks), i
