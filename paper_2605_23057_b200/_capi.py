@@ -122,7 +122,8 @@ _host = None
 def engine_lib() -> C.CDLL:
     global _engine
     if _engine is None:
-        lib = _load("libmsw_engine.so")
+        # MSW_ENGINE_SO selects a diagnostics build (libmsw_engine_trace.so); scripts only
+        lib = _load(os.environ.get("MSW_ENGINE_SO", "libmsw_engine.so"))
         vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
         lib.msw_engine_create.argtypes = [C.c_int, C.POINTER(EngineCfg), C.POINTER(vp)]
         lib.msw_engine_run.argtypes = [vp, C.POINTER(Request), C.POINTER(Result)]

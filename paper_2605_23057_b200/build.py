@@ -12,6 +12,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -54,17 +55,41 @@ def build_engine(force: bool = False) -> str:
     if force or _stale(ENGINE_SO, deps):
         objdir = os.path.join(ROOT, "build", "engine")
         os.makedirs(objdir, exist_ok=True)
-        objs = []
+        objs, jobs = [], []
         for s in srcs:
             o = os.path.join(objdir, os.path.basename(s) + ".o")
             objs.append(o)
             if force or _stale(o, [s] + deps[len(srcs):]):
-                _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                      "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", INC,
-                      "-I", os.path.join(CSRC, "engine"), "-c", s, "-o", o])
+                jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                             "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", INC,
+                             "-I", os.path.join(CSRC, "engine"), "-c", s, "-o", o])
+        with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+            for f in [ex.submit(_run, j) for j in jobs]:
+                f.result()
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", ENGINE_SO, *objs,
               "-lpthread", "-ldl", "-lrt"])
     return ENGINE_SO
+
+
+def build_engine_trace() -> str:
+    """Diagnostics build with the MSW_TP timeline probes (-DMSW_TRACE); used
+    only by scripts/gemv_timeline.py, never by the product path or tests."""
+    out = os.path.join(LIB, "libmsw_engine_trace.so")
+    srcs = sorted(glob.glob(os.path.join(CSRC, "engine", "*.cu")))
+    objdir = os.path.join(ROOT, "build", "engine_trace")
+    os.makedirs(objdir, exist_ok=True)
+    objs, jobs = [], []
+    for s in srcs:
+        o = os.path.join(objdir, os.path.basename(s) + ".o")
+        objs.append(o)
+        jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                     "-DMSW_TRACE", "--expt-relaxed-constexpr", "-I", INC,
+                     "-I", os.path.join(CSRC, "engine"), "-c", s, "-o", o])
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        for f in [ex.submit(_run, j) for j in jobs]:
+            f.result()
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-lpthread", "-ldl", "-lrt"])
+    return out
 
 
 def build_host(force: bool = False) -> str:

@@ -89,6 +89,32 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + expf(-g)); }
 
+// Intra-CTA timeline probes, compiled only into the diagnostics build
+// (-DMSW_TRACE -> libmsw_engine_trace.so, scripts/gemv_timeline.py). Slot i of
+// CTA b receives clock64() relative to the CTA's first probe; slot 15 holds
+// %globaltimer at probe 0 (cross-CTA skew). Zero cost in the product build.
+#ifdef MSW_TRACE
+__device__ __forceinline__ unsigned long long* msw_trace_buf();
+#define MSW_TP(i)                                                                  \
+  do {                                                                             \
+    unsigned long long* tb_ = msw_trace_buf();                                     \
+    if (tb_) {                                                                     \
+      unsigned long long c_ = clock64();                                           \
+      if ((i) == 0) {                                                              \
+        unsigned long long g_;                                                     \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                     \
+        tb_[blockIdx.x * 16 + 15] = g_;                                            \
+        tb_[blockIdx.x * 16 + 14] = c_;                                            \
+      }                                                                            \
+      tb_[blockIdx.x * 16 + (i)] = c_;                                             \
+    }                                                                              \
+  } while (0)
+#else
+#define MSW_TP(i) \
+  do {            \
+  } while (0)
+#endif
+
 // Programmatic dependent launch: everything before pdl_wait() may only touch
 // data the previous kernel does not write (weights); pdl_trigger() lets the
 // next kernel in the stream start its own weight prefetch early.

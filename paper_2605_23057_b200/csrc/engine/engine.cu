@@ -171,6 +171,10 @@ struct Model {
   std::vector<void*> allocations;
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
   int graph_nodes[3] = {0, 0, 0};
+  // persistent decode step (decode_mk.cu), built on first use per format
+  bool mk_ready[3] = {false, false, false};
+  MkParams mk[3];
+  size_t mk_smem[3] = {0, 0, 0};
 
   size_t weight_bytes(int fmt) const {
     size_t b = size_t(c.vocab) * c.hidden * 2;  // fp16 lm_head in every mode
@@ -199,6 +203,7 @@ struct Scratch {
   int* slot = nullptr;
   int* seq_of = nullptr;
   int* logit_rows = nullptr;
+  unsigned long long* amax_ws = nullptr;  // argmax slots + counters [2 * kMaxLogitRows], self-resetting
   int* split_cnt = nullptr;  // attention split-merge counters [tokens, kv heads], self-resetting
   int* next = nullptr;
   int* step = nullptr;
@@ -436,6 +441,8 @@ void alloc_scratch(msw_engine* e) {
   s.split_cnt = dalloc<int>(tsplit * 64);
   MSW_CUDA(cudaMemset(s.split_cnt, 0, sizeof(int) * tsplit * 64));
   s.next = dalloc<int>(kMaxLogitRows);
+  s.amax_ws = dalloc<unsigned long long>(2 * kMaxLogitRows);
+  MSW_CUDA(cudaMemset(s.amax_ws, 0, sizeof(unsigned long long) * 2 * kMaxLogitRows));
   s.step = dalloc<int>(1);
   s.hist = dalloc<int>(size_t(e->cfg.max_seq_len) + 64);
   s.stage_ints = size_t(T) * 4 + 256;
@@ -444,7 +451,7 @@ void alloc_scratch(msw_engine* e) {
   for (void* p : {(void*)s.h, (void*)s.qkv, (void*)s.q16, (void*)s.o, (void*)s.act, (void*)s.xh,
                   (void*)s.xq, (void*)s.xscale, (void*)s.hsel, (void*)s.logits, (void*)s.part_o,
                   (void*)s.part_ml, (void*)s.tok, (void*)s.pos, (void*)s.slot, (void*)s.seq_of,
-                  (void*)s.logit_rows, (void*)s.split_cnt, (void*)s.next, (void*)s.step,
+                  (void*)s.logit_rows, (void*)s.split_cnt, (void*)s.next, (void*)s.amax_ws, (void*)s.step,
                   (void*)s.hist})
     e->owned.push_back(p);
 }
@@ -453,6 +460,14 @@ void alloc_scratch(msw_engine* e) {
 // Runs T tokens (inputs already in sc.tok/pos/slot/seq_of) through model m in
 // format fmt; logits + argmax for the n_logits rows listed in sc.logit_rows
 // (rows == nullptr means rows 0..n_logits-1 == all T rows).
+// Diagnostics only: MSW_SKIP="attn,qkv,o,gu,down,head,argmax" drops those
+// launches from the step (outputs become meaningless) to attribute in-graph
+// step time per kernel class. Never set on a product path.
+bool diag_skip(const char* what) {
+  static const char* env = std::getenv("MSW_SKIP");
+  return env && std::strstr(env, what);
+}
+
 void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_identity,
              bool tokens_independent) {
   Scratch& s = e->sc;
@@ -474,7 +489,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
     half* vc = m.vc + m.kv_layer_elems * l;
     // attention block
     if (small) {
-      launch_gemv(ly.qkv[fmt], kProNorm, kEpiStore, s.h, T, ly.attn_norm, eps, s.qkv, st);
+      if (!diag_skip("qkv")) launch_gemv(ly.qkv[fmt], kProNorm, kEpiStore, s.h, T, ly.attn_norm, eps, s.qkv, st);
       ++n;
     } else {
       launch_prep_act(fmt, s.h, T, H, ly.attn_norm, eps, s.xh, s.xq, s.xscale, st);
@@ -482,7 +497,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       n += 2;
     }
     if (tokens_independent) {  // decode / CB: RoPE + KV append fused into attention
-      launch_attention_decode(s.qkv, m.rope, T, s.pos, s.slot, s.seq_of, m.block_table, kc,
+      if (!diag_skip("attn")) launch_attention_decode(s.qkv, m.rope, T, s.pos, s.slot, s.seq_of, m.block_table, kc,
                               vc, m.ash, nsplit, s.part_o, s.part_ml, s.split_cnt, s.o, st);
       n += 1;
     } else {
@@ -497,9 +512,9 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       }
     }
     if (small) {
-      launch_gemv(ly.o[fmt], kProPlain, kEpiResid, s.o, T, nullptr, eps, s.h, st);
-      launch_gemv(ly.gu[fmt], kProNorm, kEpiSwiglu, s.h, T, ly.ffn_norm, eps, s.act, st);
-      launch_gemv(ly.down[fmt], kProPlain, kEpiResid, s.act, T, nullptr, eps, s.h, st);
+      if (!diag_skip("o,") && !diag_skip("oonly")) launch_gemv(ly.o[fmt], kProPlain, kEpiResid, s.o, T, nullptr, eps, s.h, st);
+      if (!diag_skip("gu")) launch_gemv(ly.gu[fmt], kProNorm, kEpiSwiglu, s.h, T, ly.ffn_norm, eps, s.act, st);
+      if (!diag_skip("down")) launch_gemv(ly.down[fmt], kProPlain, kEpiResid, s.act, T, nullptr, eps, s.h, st);
       n += 3;
     } else {
       launch_prep_act(fmt, s.o, T, Hq * D, nullptr, eps, s.xh, s.xq, s.xscale, st);
@@ -526,14 +541,14 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
   head.w = m.lm_head;
   head.w_tf = m.lm_head_tf;
   if (n_logits <= kGemvMaxTokens) {
-    launch_gemv(head, kProNorm, kEpiStore, hrows, n_logits, m.final_norm, eps, s.logits, st);
+    if (!diag_skip("head")) launch_gemv(head, kProNorm, kEpiStore, hrows, n_logits, m.final_norm, eps, s.logits, st);
     ++n;
   } else {
     launch_prep_act(kFP16, hrows, n_logits, H, m.final_norm, eps, s.xh, s.xq, s.xscale, st);
     launch_gemm(head, kEpiStore, s.xh, s.xq, s.xscale, n_logits, s.logits, st);
     n += 2;
   }
-  launch_argmax(s.logits, n_logits, c.vocab, s.next, st);
+  if (!diag_skip("argmax")) launch_argmax(s.logits, n_logits, c.vocab, s.next, s.amax_ws, st);
   ++n;
 }
 
@@ -695,9 +710,89 @@ void prefill_packed(msw_engine* e, Model& m, int fmt, const std::vector<PackSeq>
   }
 }
 
+// The persistent decode step's parameters for (m, fmt): device layer table,
+// barrier words, shared-memory plan. Returns false if the shape is outside
+// what decode_mk.cu covers (the per-kernel path below then runs).
+bool ensure_mk(msw_engine* e, Model& m, int fmt) {
+  static const bool on = std::getenv("MSW_MK") != nullptr;  // opt-in while it is tuned
+  if (!on) return false;
+  if (m.mk_ready[fmt]) return true;
+  Scratch& s = e->sc;
+  const msw_model_cfg& c = m.c;
+  MkParams P;
+  P.n_layers = c.n_layers;
+  P.H = c.hidden;
+  P.Hq = c.n_heads;
+  P.Hk = c.n_kv_heads;
+  P.D = c.head_dim;
+  P.F = c.ffn;
+  P.eps = c.rms_eps;
+  if (!mk_supported(P)) return false;
+  std::vector<MkLayer> ly(c.n_layers);
+  auto lin = [](const LinearW& W) {
+    MkLinear L;
+    L.w_tf = W.w_tf;
+    L.s = W.s;
+    L.n = W.n;
+    L.k = W.k;
+    return L;
+  };
+  for (int l = 0; l < c.n_layers; ++l) {
+    const Layer& src = m.layers[l];
+    ly[l].qkv = lin(src.qkv[fmt]);
+    ly[l].o = lin(src.o[fmt]);
+    ly[l].gu = lin(src.gu[fmt]);
+    ly[l].down = lin(src.down[fmt]);
+    ly[l].attn_norm = src.attn_norm;
+    ly[l].ffn_norm = src.ffn_norm;
+    ly[l].kc = m.kc + m.kv_layer_elems * l;
+    ly[l].vc = m.vc + m.kv_layer_elems * l;
+  }
+  MkLayer* d_ly = model_alloc<MkLayer>(m, ly.size());
+  MSW_CUDA(cudaMemcpy(d_ly, ly.data(), sizeof(MkLayer) * ly.size(), cudaMemcpyHostToDevice));
+  unsigned* sync = model_alloc<unsigned>(m, 2 + 64);  // bar, epoch, attn counters
+  MSW_CUDA(cudaMemset(sync, 0, sizeof(unsigned) * (2 + 64)));
+  P.layers = d_ly;
+  P.embed = m.embed;
+  P.head.w_tf = m.lm_head_tf;
+  P.head.n = c.vocab;
+  P.head.k = c.hidden;
+  P.final_norm = m.final_norm;
+  P.rope = m.rope;
+  P.block_table = m.block_table;
+  P.tok = s.tok;
+  P.pos = s.pos;
+  P.slot = s.slot;
+  P.step = s.step;
+  P.hist = s.hist;
+  P.next = s.next;
+  P.h = s.h;
+  P.qkv = s.qkv;
+  P.o = s.o;
+  P.act = s.act;
+  P.logits = s.logits;
+  P.part_o = s.part_o;
+  P.part_ml = s.part_ml;
+  P.bar = sync;
+  P.epoch = sync + 1;
+  P.attn_cnt = reinterpret_cast<int*>(sync + 2);
+  P.amax = s.amax_ws + (2 * kMaxLogitRows - 1);  // never touched by launch_argmax (T <= 64)
+  P.nsplit_max = std::max(1, std::min(32, kNumSMs / c.n_kv_heads));
+  P.one = 1;
+  m.mk_smem[fmt] = mk_smem_plan(P, fmt);
+  m.mk[fmt] = P;
+  m.mk_ready[fmt] = true;
+  return true;
+}
+
 // One batch-1 decode step for model m / fmt, as a graph or eagerly.
 void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph) {
   Scratch& s = e->sc;
+  if (ensure_mk(e, m, fmt)) {  // one persistent launch: forward + argmax + advance
+    launch_decode_mk(fmt, m.mk[fmt], m.mk_smem[fmt], e->st);
+    ++e->launches;
+    return;
+  }
   auto body = [&]() {
     forward(e, m, fmt, 1, 1, true, true);
     launch_advance(s.next, s.tok, s.pos, s.slot, s.step, s.hist, m.block_table, e->st);

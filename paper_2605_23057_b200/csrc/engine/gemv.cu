@@ -22,8 +22,13 @@
 // warps in smem at tile boundaries. The activation prologue (RMSNorm, fp16
 // rounding / per-token int8 quantisation) runs once per CTA into smem.
 #include "kernels.cuh"
+#include "mma_frag.cuh"
 
 namespace msw {
+#ifdef MSW_TRACE
+__device__ unsigned long long* g_msw_trace = nullptr;
+__device__ __forceinline__ unsigned long long* msw_trace_buf() { return g_msw_trace; }
+#endif
 namespace {
 
 constexpr int kConsumers = 16;
@@ -32,31 +37,6 @@ constexpr int kConsThreads = kConsumers * 32;
 constexpr int kChunkBytes = 512;
 constexpr int kMaxStages = 8;
 constexpr int kSmemBudget = 190 * 1024;
-
-__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-__device__ __forceinline__ half2 u2h2(uint32_t u) { return *reinterpret_cast<half2*>(&u); }
-__device__ __forceinline__ uint32_t h22u(half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
-
-__device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
-                                        uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void mma_s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0,
-                                       uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
 
 template <int FMT>
 struct TF {
@@ -82,19 +62,6 @@ __device__ __forceinline__ float cons_max(float v, float* red) {
   named_sync(1, kConsThreads);
   const float t = lane < kConsumers ? red[lane] : -3.402823466e38f;
   return warp_max(t);
-}
-
-// Activations are stored permuted so that lane (g, tq) fetches both B-fragment
-// registers of an MMA with one 8-byte LDS:
-//   fp16, per 16-k block: [0,1,8,9 | 2,3,10,11 | 4,5,12,13 | 6,7,14,15]
-//   int8, per 32-k block: [0..3,16..19 | 4..7,20..23 | 8..11,24..27 | 12..15,28..31]
-__device__ __forceinline__ int perm_f16(int k) {  // pairs (k, k+1), k even, stay adjacent
-  const int w = k & 15;
-  return (k & ~15) + ((w & 7) >> 1) * 4 + (w >> 3) * 2 + (w & 1);
-}
-__device__ __forceinline__ int perm_i8(int k) {  // quads (k..k+3), k % 4 == 0, stay adjacent
-  const int w = k & 31;
-  return (k & ~31) + ((w & 15) >> 2) * 8 + (w >> 4) * 4 + (w & 3);
 }
 
 // x fp32 [T, k] -> smem: fp16 [NT][k] (FP16 / W4) or int8 [NT][k] + scale.
@@ -192,6 +159,69 @@ __device__ __forceinline__ void prologue(const float* __restrict__ x, const half
     }
     named_sync(1, kConsThreads);
   }
+}
+
+// Batch-1 W4 prologue (k <= 16384): x stays in registers between the RMSNorm
+// reduction and the conversion, and the per-group offsets are reduced inside
+// the conversion loop. Thread tid converts float4 i = tid + 512 j, so warp w
+// covers exactly k in [128 (w + 16 j), +128) = one scale group per j, and
+// lane bit 2 is the k16-step parity: four xor-shuffles (1, 2, 8, 16) leave
+// the even-step sum in lane 0 and the odd-step sum in lane 4.
+// Group sums are fp32 (pairwise tree over the fp16-rounded x).
+constexpr int kW4ProRegs = 8;
+template <int PRO>
+__device__ __forceinline__ void prologue_w4_t1(const float* __restrict__ x,
+                                               const half* __restrict__ gamma, float eps, int k,
+                                               uint8_t* xs, float* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k4 = k / 4;
+  const float4* xt = reinterpret_cast<const float4*>(x);
+  float4 v[kW4ProRegs];
+#pragma unroll
+  for (int j = 0; j < kW4ProRegs; ++j)
+    if (tid + j * kConsThreads < k4) v[j] = xt[tid + j * kConsThreads];
+  float r = 1.0f;
+  if (PRO == kProNorm) {
+    float ss = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kW4ProRegs; ++j)
+      if (tid + j * kConsThreads < k4)
+        ss = fmaf(v[j].x, v[j].x, fmaf(v[j].y, v[j].y, fmaf(v[j].z, v[j].z, fmaf(v[j].w, v[j].w, ss))));
+    ss = cons_sum(ss, red);
+    r = 1.0f / sqrtf(ss / float(k) + eps);
+  }
+  half* xh = reinterpret_cast<half*>(xs);
+  half* xh16 = reinterpret_cast<half*>(xs + size_t(2) * k);
+  float* corr = reinterpret_cast<float*>(xs + size_t(4) * k);
+  const half2 sixteenth = __float2half2_rn(0.0625f);
+#pragma unroll
+  for (int j = 0; j < kW4ProRegs; ++j) {
+    const int i = tid + j * kConsThreads;
+    if (warp * 32 + j * kConsThreads >= k4) continue;  // warp-uniform: k4 % 32 == 0
+    float4 a = v[j];
+    if (PRO == kProNorm) {
+      const half2* gm = reinterpret_cast<const half2*>(gamma) + 2 * i;
+      const float2 g0 = __half22float2(gm[0]), g1 = __half22float2(gm[1]);
+      a.x = (a.x * r) * g0.x;
+      a.y = (a.y * r) * g0.y;
+      a.z = (a.z * r) * g1.x;
+      a.w = (a.w * r) * g1.y;
+    }
+    const half2 lo = __floats2half2_rn(a.x, a.y), hi = __floats2half2_rn(a.z, a.w);
+    *reinterpret_cast<half2*>(xh + perm_f16(4 * i)) = lo;
+    *reinterpret_cast<half2*>(xh + perm_f16(4 * i + 2)) = hi;
+    *reinterpret_cast<half2*>(xh16 + perm_f16(4 * i)) = __hmul2(lo, sixteenth);
+    *reinterpret_cast<half2*>(xh16 + perm_f16(4 * i + 2)) = __hmul2(hi, sixteenth);
+    const float2 lf = __half22float2(lo), hf = __half22float2(hi);
+    float gs = (lf.x + lf.y) + (hf.x + hf.y);
+    gs += __shfl_xor_sync(0xffffffffu, gs, 1);
+    gs += __shfl_xor_sync(0xffffffffu, gs, 2);
+    gs += __shfl_xor_sync(0xffffffffu, gs, 8);
+    gs += __shfl_xor_sync(0xffffffffu, gs, 16);
+    const float odd = __shfl_sync(0xffffffffu, gs, 4);
+    if (lane == 0) corr[warp + j * kConsumers] = 1032.0f * gs + 72.0f * odd;
+  }
+  named_sync(1, kConsThreads);
 }
 
 template <int EPI>
@@ -462,6 +492,256 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// W4 decode GEMV, issue-lean variant (8B shapes: K = 4096 and K = 14336).
+// The generic kernel above spends ~68 warp instructions per 1024 weights at
+// 2 chunks per warp per stage (barrier / loop / tile bookkeeping dominate)
+// and is issue-bound below the HBM rate even with L2-resident weights. Here:
+//   * every warp takes CPW = 4 chunks (two 128-k groups) per stage, so the
+//     per-stage overhead is amortised over 4096 weights;
+//   * GW warp groups take alternate stages (GW = 2 for K = 14336: 16 KB
+//     stages, 8 warps each), so all 16 warps stay busy when a 32 KB stage
+//     does not divide the tile;
+//   * when the tile is exactly one stage (K = 4096, XREG) each warp's k-slice
+//     never changes: its B fragments (fp16 x and x/16) and its two group
+//     offsets live in registers for the whole kernel, leaving one LDS.128 of
+//     weights plus two scale loads per 4096 weights;
+//   * a warp flushes its 16 x 8 tile partial when its slice moves to the next
+//     tile (stages may straddle tiles in the GW = 2 configuration).
+// Same numerics as gemv_tf_kernel<kW4>: identical MMA operands, per-group
+// fp32 accumulation of 8 MMAs, correction subtracted before the group scale.
+template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemv_w4_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
+                   const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
+                   float* __restrict__ y, int n_stages, uint32_t shr8_mul) {
+  constexpr int WPG = kConsumers / GW;  // warps sharing one stage
+  constexpr int CPW = S / WPG;          // chunks per warp per stage
+  static_assert(CPW == 4, "two 128-k groups per warp per stage");
+  constexpr int STAGE_BYTES = S * kChunkBytes;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages], sbar;
+  __shared__ uint64_t tile_full[2], tile_free[2];
+  __shared__ float red[32];
+  __shared__ float xscale[NT];
+  __shared__ __align__(16) float part[2][kConsumers][16][8];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunks_tile = k / 64;
+  const int ntiles = n / 16;
+  const int per_cta = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int tile_begin = blockIdx.x * per_cta;
+  const int tile_end = min(ntiles, tile_begin + per_cta);
+  const int ntile_cta = max(0, tile_end - tile_begin);
+  const int total_stages = ntile_cta * chunks_tile / S;
+  const int groups_k = k / kW4Group;
+  const int rows = ntile_cta * 16;
+  const int xbytes = NT * 4 * k + NT * groups_k * 4;
+  const int sbytes = rows * groups_k * 2;
+  uint8_t* xs = smem;
+  uint8_t* sc_smem = smem + ((xbytes + 127) & ~127);
+  uint8_t* ring = sc_smem + ((sbytes + 127) & ~127);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], WPG);
+    }
+    mbar_init(&sbar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tile_full[b], kConsumers);
+      mbar_init(&tile_free[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumers) {  // producer: weights + scales only, ahead of the PDL wait
+    if (lane == 0) MSW_TP(0);
+    if (lane == 0 && total_stages > 0) {
+      mbar_expect_tx(&sbar, sbytes);
+      bulk_g2s(sc_smem, static_cast<const uint8_t*>(ws) + size_t(tile_begin) * 16 * groups_k * 2,
+               sbytes, &sbar);
+      const uint8_t* src = wtf + size_t(tile_begin) * chunks_tile * kChunkBytes;
+      int s = 0;
+      uint32_t phase = 0;
+      for (int st = 0; st < total_stages; ++st) {
+        mbar_wait(&empty[s], phase ^ 1);
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        bulk_g2s(ring + size_t(s) * STAGE_BYTES, src + size_t(st) * STAGE_BYTES, STAGE_BYTES,
+                 &full[s]);
+        if (st == n_stages - 1) MSW_TP(1);  // ring primed
+        if (++s == n_stages) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+      MSW_TP(2);  // last stage issued
+    }
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
+  if (warp == kConsumers + 1) {  // epilogue: 16 per-warp partials -> y
+    pdl_wait();
+    pdl_trigger();
+    named_sync(3, kConsThreads + 32);
+    for (int i = 0; i < ntile_cta; ++i) {
+      const int b = i & 1;
+      mbar_wait(&tile_full[b], (i >> 1) & 1);
+      const int tile = tile_begin + i;
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+        const int row = 2 * ((lane >> 3) + pass * 4);
+        const int col = lane & 7;
+        float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+        for (int w2 = 0; w2 < kConsumers; ++w2) {
+          v0 += part[b][w2][row][col];
+          v1 += part[b][w2][row + 1][col];
+        }
+        if (col < T) store_pair<EPI>(y, n, col, tile * 16 + row, v0, v1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_free[b]);
+      if (lane == 0 && i == 0) MSW_TP(8);  // first tile stored
+    }
+    if (lane == 0) MSW_TP(9);  // all tiles stored
+    return;
+  }
+
+  // consumers
+  pdl_wait();
+  if (threadIdx.x == 0) MSW_TP(3);  // dependency resolved
+  pdl_trigger();
+  if (NT == 1 && k <= kW4ProRegs * 4 * kConsThreads)
+    prologue_w4_t1<PRO>(x, gamma, eps, k, xs, red);
+  else
+    prologue<kW4, PRO, NT>(x, gamma, eps, k, T, xs, red, xscale);
+  if (threadIdx.x == 0) MSW_TP(4);  // activations staged
+  named_sync(3, kConsThreads + 32);
+  const int g = lane >> 2, tq = lane & 3;
+  const int gw = warp / WPG, wi = warp % WPG;
+  const int brow = g < T ? g : 0;
+  const uint8_t* xrow = xs + size_t(brow) * 2 * k + tq * 8;
+  const uint8_t* xrow16 = xs + size_t(NT) * 2 * k + size_t(brow) * 2 * k + tq * 8;
+  const half* sc_h = reinterpret_cast<const half*>(sc_smem);
+  const float* corr = reinterpret_cast<const float*>(xs + size_t(NT) * 4 * k);
+  const int tc0 = 2 * tq < NT ? 2 * tq : 0, tc1 = 2 * tq + 1 < NT ? 2 * tq + 1 : 0;
+  // XREG: this warp's k-slice is chunks [wi*CPW, wi*CPW + CPW) of every tile
+  uint2 bx[XREG ? CPW : 1][2][2];
+  float cx[XREG ? CPW / 2 : 1][2];
+  if (XREG) {
+#pragma unroll
+    for (int j = 0; j < CPW; ++j)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int kb = ((wi * CPW + j) * 64 + p * 32) * 2;
+        bx[XREG ? j : 0][p][0] = *reinterpret_cast<const uint2*>(xrow + kb);
+        bx[XREG ? j : 0][p][1] = *reinterpret_cast<const uint2*>(xrow16 + kb + 32);
+      }
+#pragma unroll
+    for (int jj = 0; jj < CPW / 2; ++jj) {
+      const int grp = (wi * CPW) / 2 + jj;
+      cx[XREG ? jj : 0][0] = corr[tc0 * groups_k + grp];
+      cx[XREG ? jj : 0][1] = corr[tc1 * groups_k + grp];
+    }
+  }
+  if (total_stages > 0) mbar_wait(&sbar, 0);
+
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  int cur = -1;  // tile (CTA-local) the accumulator belongs to
+  // ring position of this warp's first stage; advanced incrementally by GW
+  int slot = gw % n_stages;
+  uint32_t phase = (gw / n_stages) & 1;
+  auto flush = [&](int ti) {
+    const int b = ti & 1;
+    if (ti >= 2) mbar_wait(&tile_free[b], ((ti >> 1) - 1) & 1);
+    float* pw = &part[b][warp][0][0];
+    *reinterpret_cast<float2*>(pw + g * 8 + 2 * tq) = make_float2(acc[0], acc[1]);
+    *reinterpret_cast<float2*>(pw + (g + 8) * 8 + 2 * tq) = make_float2(acc[2], acc[3]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tile_full[b]);
+    acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+  };
+#pragma unroll 1
+  for (int st = gw; st < total_stages; st += GW) {
+    const int gc = st * S + wi * CPW;  // chunk index in this CTA's stream
+    const int ti = XREG ? st : gc / chunks_tile;  // XREG: one tile per stage
+    const int c0 = XREG ? wi * CPW : gc - ti * chunks_tile;
+    if (ti != cur) {
+      if (cur >= 0) flush(cur);
+      cur = ti;
+    }
+    mbar_wait(&full[slot], phase);
+    if (threadIdx.x == 0 && st == 0) MSW_TP(5);  // first stage consumed
+    if (threadIdx.x == 0 && st == n_stages) MSW_TP(6);  // ring wrapped once
+    const uint4* stage = reinterpret_cast<const uint4*>(ring + size_t(slot) * STAGE_BYTES) +
+                         wi * CPW * 32 + lane;
+    uint4 a4[CPW];
+#pragma unroll
+    for (int j = 0; j < CPW; ++j) a4[j] = stage[j * 32];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);  // operands are in registers
+    slot += GW;
+    if (slot >= n_stages) {
+      slot -= n_stages;
+      phase ^= 1;
+    }
+    const int lr = ti * 16 + g;
+#pragma unroll
+    for (int jj = 0; jj < CPW / 2; ++jj) {
+      float cg[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 2 * jj; j < 2 * jj + 2; ++j) {
+        const uint32_t wv[4] = {a4[j].x, a4[j].y, a4[j].z, a4[j].w};
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const uint32_t w0 = wv[2 * p], w1 = wv[2 * p + 1];
+          // w >> 8 as mul.hi by a runtime 2^24: FMA pipe instead of the ALU pipe,
+          // which the 16 lop3 per 1024 weights already saturate to ~2/cycle/SM
+          const uint32_t w0s = __umulhi(w0, shr8_mul), w1s = __umulhi(w1, shr8_mul);
+          const uint32_t a_lo[4] = {lop3_and_or(w0, 0x000F000Fu, 0x64006400u),
+                                    lop3_and_or(w0s, 0x000F000Fu, 0x64006400u),
+                                    lop3_and_or(w1, 0x000F000Fu, 0x64006400u),
+                                    lop3_and_or(w1s, 0x000F000Fu, 0x64006400u)};
+          const uint32_t a_hi[4] = {lop3_and_or(w0, 0x00F000F0u, 0x64006400u),
+                                    lop3_and_or(w0s, 0x00F000F0u, 0x64006400u),
+                                    lop3_and_or(w1, 0x00F000F0u, 0x64006400u),
+                                    lop3_and_or(w1s, 0x00F000F0u, 0x64006400u)};
+          uint2 be, bo;
+          if (XREG) {
+            be = bx[XREG ? j : 0][p][0];
+            bo = bx[XREG ? j : 0][p][1];
+          } else {
+            const int kb = ((c0 + j) * 64 + p * 32) * 2;
+            be = *reinterpret_cast<const uint2*>(xrow + kb);
+            bo = *reinterpret_cast<const uint2*>(xrow16 + kb + 32);
+          }
+          mma_f16(cg, a_lo, be.x, be.y);
+          mma_f16(cg, a_hi, bo.x, bo.y);
+        }
+      }
+      const int grp = (c0 >> 1) + jj;
+      const float slo = __half2float(sc_h[lr * groups_k + grp]);
+      const float shi = __half2float(sc_h[(lr + 8) * groups_k + grp]);
+      float k0, k1;
+      if (XREG) {
+        k0 = cx[XREG ? jj : 0][0];
+        k1 = cx[XREG ? jj : 0][1];
+      } else {
+        k0 = corr[tc0 * groups_k + grp];
+        k1 = corr[tc1 * groups_k + grp];
+      }
+      acc[0] = fmaf(slo, cg[0] - k0, acc[0]);
+      acc[1] = fmaf(slo, cg[1] - k1, acc[1]);
+      acc[2] = fmaf(shi, cg[2] - k0, acc[2]);
+      acc[3] = fmaf(shi, cg[3] - k1, acc[3]);
+    }
+  }
+  if (cur >= 0) flush(cur);
+  if (threadIdx.x == 0) MSW_TP(7);  // warp 0 done
+}
+
 // --------------------------------------------------------------- repacking
 // Row-major source -> tile-fragment layout. Source formats:
 //   FP16: half [n][k]; INT8: int8 [n][k]; W4: row-packed words [n][k/8]
@@ -539,10 +819,45 @@ void launch_tf_s(const LinearW& W, const float* x, int T, const half* gamma, flo
              static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages);
 }
 
+template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
+void launch_w4(const LinearW& W, const float* x, int T, const half* gamma, float eps, float* y,
+               cudaStream_t st) {
+  const int ntiles = W.n / 16;
+  const int grid = std::max(1, std::min(ntiles, kNumSMs));
+  const int stage_bytes = S * kChunkBytes;
+  const int groups = W.k / kW4Group;
+  const size_t xbytes = (size_t(NT) * 4 * W.k + size_t(NT) * groups * 4 + 127) & ~size_t(127);
+  const int per_cta = (ntiles + grid - 1) / grid;
+  const size_t sbytes = (size_t(per_cta) * 16 * groups * 2 + 127) & ~size_t(127);
+  const size_t fixed = xbytes + sbytes;
+  if (fixed + 2 * size_t(stage_bytes) > size_t(kSmemBudget))
+    throw ConfigErr("gemv(w4): shared memory budget exceeded");
+  const int stages = std::min<int>(kMaxStages, int((kSmemBudget - fixed) / stage_bytes));
+  const size_t smem = fixed + size_t(stages) * stage_bytes;
+  static bool attr_done = false;
+  if (!attr_done) {
+    MSW_CUDA(cudaFuncSetAttribute(gemv_w4_kernel<PRO, EPI, NT, S, GW, XREG>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_done = true;
+  }
+  launch_pdl(gemv_w4_kernel<PRO, EPI, NT, S, GW, XREG>, dim3(grid), dim3(kThreads), smem, st,
+             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages,
+             uint32_t(1u << 24));
+}
+
 template <int FMT, int PRO, int EPI, int NT>
 void launch_tf(const LinearW& W, const float* x, int T, const half* gamma, float eps, float* y,
                cudaStream_t st) {
   const int chunks_tile = W.k / TF<FMT>::kChunkK;
+  if constexpr (FMT == kW4 && NT == 1) {  // the GPTQ modes decode batch-1
+    static const bool generic = std::getenv("MSW_GEMV_W4_GENERIC") != nullptr;  // A/B switch
+    if (!generic) {
+    if (chunks_tile == 64) return launch_w4<PRO, EPI, NT, 64, 1, true>(W, x, T, gamma, eps, y, st);
+    if (chunks_tile % 64 == 0) return launch_w4<PRO, EPI, NT, 64, 1, false>(W, x, T, gamma, eps, y, st);
+    if (chunks_tile % 32 == 0 && chunks_tile >= 64)
+      return launch_w4<PRO, EPI, NT, 32, 2, false>(W, x, T, gamma, eps, y, st);
+    }
+  }
   if (chunks_tile % 32 == 0) return launch_tf_s<FMT, PRO, EPI, NT, 32>(W, x, T, gamma, eps, y, st);
   if (chunks_tile % 8 == 0) return launch_tf_s<FMT, PRO, EPI, NT, 8>(W, x, T, gamma, eps, y, st);
   if (chunks_tile % 4 == 0) return launch_tf_s<FMT, PRO, EPI, NT, 4>(W, x, T, gamma, eps, y, st);
@@ -593,6 +908,12 @@ __global__ void gemv_i8_acc_kernel(const int8_t* __restrict__ w, const int8_t* _
 }
 
 }  // namespace
+
+#ifdef MSW_TRACE
+extern "C" int msw_trace_set(void* buf) {
+  return cudaMemcpyToSymbol(g_msw_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
                  float eps, float* y, cudaStream_t st) {

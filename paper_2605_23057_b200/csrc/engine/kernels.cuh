@@ -103,12 +103,57 @@ void launch_attention_decode(const float* qkv, const float2* rope, int T, const 
 // ---- misc.cu ------------------------------------------------------------------
 void launch_embed(const half* emb, const int* tok, int T, int H, float* h, cudaStream_t st);
 // out[t] = argmax_v logits[t, v] (lowest index on ties)
-void launch_argmax(const float* logits, int T, int V, int* out, cudaStream_t st);
+// ws: 2*T zeroed u64 words (slots + counters), left zeroed on return.
+void launch_argmax(const float* logits, int T, int V, int* out, unsigned long long* ws,
+                   cudaStream_t st);
 void launch_gather_rows(const float* src, const int* rows, int n, int width, float* dst,
                         cudaStream_t st);
 // batch-1 decode bookkeeping for graph replay: tok = history[step] = next[0],
 // step += 1, pos += 1, slot from block-table row 0
 void launch_advance(const int* next, int* tok, int* pos, int* slot, int* step, int* history,
                     const int* block_table, cudaStream_t st);
+
+// ---- decode_mk.cu: persistent batch-1 decode step (one launch per token) ----
+struct MkLinear {
+  const void* w_tf = nullptr;  // tile-fragment weights
+  const void* s = nullptr;     // INT8: float [n]; W4: half [n][k/128]; FP16: unused
+  int n = 0, k = 0;
+};
+struct MkLayer {
+  MkLinear qkv, o, gu, down;
+  const half* attn_norm = nullptr;
+  const half* ffn_norm = nullptr;
+  half* kc = nullptr;  // this layer's paged K / V pool
+  half* vc = nullptr;
+};
+struct MkParams {
+  const MkLayer* layers = nullptr;  // device array [n_layers]
+  int n_layers = 0;
+  int H = 0, Hq = 0, Hk = 0, D = 0, F = 0;
+  float eps = 1e-5f;
+  const half* embed = nullptr;
+  MkLinear head;  // fp16 lm_head (tile-fragment), n = vocab
+  const half* final_norm = nullptr;
+  const float2* rope = nullptr;
+  const int* block_table = nullptr;  // row 0
+  // batch-1 decode state (advanced in-kernel: tok = hist[step] = next, pos += 1, slot)
+  int *tok = nullptr, *pos = nullptr, *slot = nullptr, *step = nullptr, *hist = nullptr,
+      *next = nullptr;
+  // scratch
+  float *h = nullptr, *qkv = nullptr, *o = nullptr, *act = nullptr, *logits = nullptr;
+  float *part_o = nullptr, *part_ml = nullptr;  // [Hq][nsplit_max][D], [Hq][nsplit_max][2]
+  int* attn_cnt = nullptr;                      // [Hk], self-resetting
+  unsigned* bar = nullptr;                      // grid-barrier arrivals (monotonic)
+  unsigned* epoch = nullptr;                    // launches completed
+  unsigned long long* amax = nullptr;           // argmax key, self-resetting
+  int nsplit_max = 1;
+  int xs_bytes = 0, sc_bytes = 0, n_slots = 0;  // shared-memory plan (mk_smem_plan)
+  uint32_t one = 1;                             // runtime 1 (keeps mul.hi shifts on the FMA pipe)
+};
+constexpr size_t kMkSmemMax = 223 * 1024;
+// Fills P.xs_bytes / sc_bytes / n_slots for format fmt; returns the dynamic smem bytes.
+size_t mk_smem_plan(MkParams& P, int fmt);
+bool mk_supported(const MkParams& P);
+void launch_decode_mk(int fmt, const MkParams& P, size_t smem, cudaStream_t st);
 
 }  // namespace msw

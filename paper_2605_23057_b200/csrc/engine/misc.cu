@@ -22,39 +22,56 @@ __device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
   }
 }
 
-__global__ void argmax_kernel(const float* __restrict__ logits, int V, int* __restrict__ out) {
-  __shared__ float sv[32];
-  __shared__ int si[32];
+// Multi-CTA greedy argmax: grid (blocks, T). Every CTA reduces a slice of the
+// row to one (value, index) key, folds it into slot[t] with a 64-bit
+// atomicMax, and the last CTA of the row (counter) publishes the index and
+// resets slot / counter for the next step. Key = order-preserving fp32 bits
+// in the high word, ~index in the low word, so equal values resolve to the
+// lowest index.
+constexpr int kArgmaxThreads = 256;
+constexpr int kArgmaxPerCta = 4096;
+
+__device__ __forceinline__ unsigned long long amax_key(float v, int i) {
+  const uint32_t u = __float_as_uint(v);
+  const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return (static_cast<unsigned long long>(o) << 32) | (0xFFFFFFFFu - uint32_t(i));
+}
+
+__global__ void __launch_bounds__(kArgmaxThreads)
+    argmax_kernel(const float* __restrict__ logits, int V, int* __restrict__ out,
+                  unsigned long long* __restrict__ slot, int* __restrict__ cnt) {
+  __shared__ unsigned long long sk[kArgmaxThreads / 32];
+  __shared__ int is_last;
   pdl_wait();
   pdl_trigger();
-  const int t = blockIdx.x;
+  const int t = blockIdx.y;
   const float* row = logits + size_t(t) * V;
-  float bv = -INFINITY;
-  int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) better(bv, bi, row[i], i);
+  const int b0 = blockIdx.x * kArgmaxPerCta;
+  const int b1 = min(V, b0 + kArgmaxPerCta);
+  unsigned long long best = 0;
+  for (int i = b0 + threadIdx.x; i < b1; i += kArgmaxThreads) {
+    const unsigned long long kk = amax_key(__ldcg(row + i), i);
+    best = kk > best ? kk : best;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    better(bv, bi, ov, oi);
+    const unsigned long long ok = __shfl_xor_sync(0xffffffffu, best, o);
+    best = ok > best ? ok : best;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) {
-    sv[warp] = bv;
-    si[warp] = bi;
-  }
+  if (lane == 0) sk[warp] = best;
   __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x >> 5;
-    bv = lane < nw ? sv[lane] : -INFINITY;
-    bi = lane < nw ? si[lane] : 0x7fffffff;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      better(bv, bi, ov, oi);
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kArgmaxThreads / 32; ++w) best = sk[w] > best ? sk[w] : best;
+    atomicMax(slot + t, best);
+    __threadfence();
+    is_last = atomicAdd(cnt + t, 1) == int(gridDim.x) - 1;
+    if (is_last) {
+      __threadfence();
+      const unsigned long long k = atomicExch(slot + t, 0ull);
+      cnt[t] = 0;
+      out[t] = int(0xFFFFFFFFu - uint32_t(k & 0xFFFFFFFFull));
     }
-    if (lane == 0) out[t] = bi == 0x7fffffff ? 0 : bi;
   }
 }
 
@@ -91,8 +108,10 @@ void launch_embed(const half* emb, const int* tok, int T, int H, float* h, cudaS
   launch_pdl(embed_kernel, dim3(T), dim3(256), 0, st, emb, tok, H, h);
 }
 
-void launch_argmax(const float* logits, int T, int V, int* out, cudaStream_t st) {
-  launch_pdl(argmax_kernel, dim3(T), dim3(1024), 0, st, logits, V, out);
+void launch_argmax(const float* logits, int T, int V, int* out, unsigned long long* ws,
+                   cudaStream_t st) {
+  launch_pdl(argmax_kernel, dim3(ceil_div(V, kArgmaxPerCta), T), dim3(kArgmaxThreads), 0, st,
+             logits, V, out, ws, reinterpret_cast<int*>(ws + T));
 }
 
 void launch_gather_rows(const float* src, const int* rows, int n, int width, float* dst,

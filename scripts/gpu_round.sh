@@ -1,5 +1,3 @@
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "EXIT $?" >> gpurun_out/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "EXIT $?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo "EXIT $?" >> gpurun_out/bench_default.log
-timeout 900 python bench.py --workload configs > gpurun_out/bench_configs.log 2>&1; echo "EXIT $?" >> gpurun_out/bench_configs.log
+timeout 600 python -m pytest tests/test_engine_gpu.py -x -q > gpurun_out/gpu_tests.log 2>&1; echo "EXIT $?" >> gpurun_out/gpu_tests.log
+timeout 600 python -m pytest tests/test_engine_8b_gpu.py -x -q > gpurun_out/gpu_tests8b.log 2>&1; echo "EXIT $?" >> gpurun_out/gpu_tests8b.log
+for m in 2 1 0; do timeout 300 python scripts/decode_once.py --mode $m --new 129 --reps 2 > gpurun_out/mk_decode_m$m.txt 2>&1; done
