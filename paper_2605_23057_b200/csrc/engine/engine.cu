@@ -780,6 +780,11 @@ bool ensure_mk(msw_engine* e, Model& m, int fmt) {
   P.nsplit_max = std::max(1, std::min(32, kNumSMs / c.n_kv_heads));
   P.one = 1;
   m.mk_smem[fmt] = mk_smem_plan(P, fmt);
+  if (const char* ns = std::getenv("MSW_MK_SLOTS")) {  // ring-depth experiments
+    const int want = std::max(2, std::min(P.n_slots, std::atoi(ns)));
+    m.mk_smem[fmt] -= size_t(P.n_slots - want) * 32 * 1024;
+    P.n_slots = want;
+  }
   m.mk[fmt] = P;
   m.mk_ready[fmt] = true;
   return true;

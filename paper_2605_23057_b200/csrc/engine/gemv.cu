@@ -513,7 +513,7 @@ template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_w4_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
                    const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
-                   float* __restrict__ y, int n_stages, uint32_t shr8_mul) {
+                   float* __restrict__ y, int n_stages, uint32_t /*unused*/) {
   constexpr int WPG = kConsumers / GW;  // warps sharing one stage
   constexpr int CPW = S / WPG;          // chunks per warp per stage
   static_assert(CPW == 4, "two 128-k groups per warp per stage");
@@ -697,9 +697,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
           const uint32_t w0 = wv[2 * p], w1 = wv[2 * p + 1];
-          // w >> 8 as mul.hi by a runtime 2^24: FMA pipe instead of the ALU pipe,
-          // which the 16 lop3 per 1024 weights already saturate to ~2/cycle/SM
-          const uint32_t w0s = __umulhi(w0, shr8_mul), w1s = __umulhi(w1, shr8_mul);
+          const uint32_t w0s = w0 >> 8, w1s = w1 >> 8;
           const uint32_t a_lo[4] = {lop3_and_or(w0, 0x000F000Fu, 0x64006400u),
                                     lop3_and_or(w0s, 0x000F000Fu, 0x64006400u),
                                     lop3_and_or(w1, 0x000F000Fu, 0x64006400u),

@@ -41,6 +41,22 @@ __global__ void lop_kernel(uint32_t* out, int iters, uint32_t seed) {
   if (s == 0x12345678u) out[threadIdx.x] = s;
 }
 
+template <int OP>
+__global__ void alu_kernel(uint32_t* out, int iters, uint32_t seed, uint32_t mul) {
+  uint32_t v[8];
+  for (int j = 0; j < 8; ++j) v[j] = seed + threadIdx.x * 7 + j;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (OP == 0) v[j] = __umulhi(v[j], mul) ^ j;            // IMAD.HI (+LOP3)
+      if (OP == 1) v[j] = (v[j] >> (mul & 31)) + j;           // SHF (+IADD)
+      if (OP == 2) v[j] = v[j] * mul + j;                     // IMAD
+    }
+  uint32_t s = 0;
+  for (int j = 0; j < 8; ++j) s ^= v[j];
+  if (s == 0x12345678u) out[threadIdx.x] = s;
+}
+
 __global__ void w4loop_kernel(float* out, int iters, uint32_t seed) {
   uint4 a4[4];
   for (int j = 0; j < 4; ++j) a4[j] = make_uint4(seed ^ j, seed * 3 + j, seed * 5 ^ j, seed + 9 * j);
@@ -94,7 +110,18 @@ int main() {
     double inst = 148.0 * warps * 8192 * 8;  // warp-level lop3
     printf("LOP3 warps/SM=%2d: %.2f warp-inst/cycle/SM (at %d MHz)\n", warps, inst / 148 / (ms * 1e-3 * clk * 1e3), clk / 1000);
   }
-  for (int warps : {4, 8, 12, 16, 24, 32}) {
+  const char* names[3] = {"IMAD.HI+LOP3", "SHF+IADD", "IMAD"};
+  for (int op = 0; op < 3; ++op) {
+    auto k = op == 0 ? alu_kernel<0> : (op == 1 ? alu_kernel<1> : alu_kernel<2>);
+    k<<<148, 512>>>((uint32_t*)o, 16, 1, op == 1 ? 8u : (1u << 24));
+    cudaEventRecord(e0);
+    k<<<148, 512>>>((uint32_t*)o, 4096, 1, op == 1 ? 8u : (1u << 24));
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    double pairs = 148.0 * 16 * 4096 * 8;
+    printf("%s: %.2f op-pairs/cycle/SM (warp-level)\n", names[op], pairs / 148 / (ms * 1e-3 * clk * 1e3));
+  }
+  for (int warps : {4, 8, 12, 16}) {
     w4loop_kernel<<<148, warps * 32>>>(o, 16, 1);
     cudaEventRecord(e0);
     w4loop_kernel<<<148, warps * 32>>>(o, 4096, 1);
