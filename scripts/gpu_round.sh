@@ -1,7 +1,4 @@
-ncu --set full --import-source on --clock-control none -k regex:gemv_w4 -s 3 -c 1 -o gpurun_out/w4_gu python scripts/gemv_micro.py 2 gate_up > gpurun_out/ncu1.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_w4.csv python scripts/decode_once.py --mode 2 --new 4 > gpurun_out/ncu2.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_int8.csv python scripts/decode_once.py --mode 1 --new 4 > gpurun_out/ncu3.log 2>&1
-timeout 300 python scripts/gemv_micro.py 2,1,0 > gpurun_out/gemv_micro_all.txt 2>&1
-timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1
-timeout 900 python bench.py --workload configs > gpurun_out/bench_configs.log 2>&1
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1
+timeout -s KILL 60 python scripts/decode_once.py --mode 0 --target tiny --prompt 20 --new 5 --graphs 0 > gpurun_out/t1.log 2>&1; echo "EXIT $?" >> gpurun_out/t1.log
+timeout -s KILL 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "EXIT $?" >> gpurun_out/gpu_tests.log
+for m in 2 1 0; do timeout -s KILL 200 python scripts/decode_once.py --mode $m --new 129 --reps 2 > gpurun_out/dec_m$m.txt 2>&1; done
+MSW_NO_ATTN_TAIL=1 timeout -s KILL 200 python scripts/decode_once.py --mode 2 --new 129 --reps 2 > gpurun_out/dec_m2_notail.txt 2>&1
