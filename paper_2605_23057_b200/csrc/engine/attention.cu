@@ -10,6 +10,26 @@
 #include "kernels.cuh"
 
 namespace msw {
+#ifdef MSW_TRACE
+__device__ unsigned long long* g_attn_trace = nullptr;
+extern "C" int msw_attn_trace_set(void* buf) {
+  return cudaMemcpyToSymbol(g_attn_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : 1;
+}
+// globaltimer at event e of CTA (blockIdx linearised): buf[cta * 8 + e]
+#define ATT_TP(e)                                                                           \
+  do {                                                                                      \
+    if (g_attn_trace && threadIdx.x == 0) {                                                 \
+      unsigned long long g_;                                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                                \
+      const int c_ = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;        \
+      g_attn_trace[c_ * 8 + (e)] = g_;                                                      \
+    }                                                                                       \
+  } while (0)
+#else
+#define ATT_TP(e) \
+  do {            \
+  } while (0)
+#endif
 namespace {
 
 __device__ __forceinline__ size_t kv_off(int slot, int hk, int Hk, int D) {
@@ -232,6 +252,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     }
   }
 
+  ATT_TP(3);
   // merge the warps of this CTA
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -309,6 +330,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   __shared__ int is_last;
   const int t = blockIdx.x, hk = blockIdx.y, sp = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ATT_TP(0);
   const int p_self = pos[t];
   const int ctx = p_self + 1;
   const int chunk = split_chunk(ctx, nsplit);
@@ -316,6 +338,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   if (begin >= ctx) {
     pdl_wait();
     pdl_trigger();
+    ATT_TP(7);  // idle split
     return;
   }
   const int end = min(ctx, begin + chunk);
@@ -342,6 +365,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   if (first < end) stage_tile(first);  // cache history only: safe before the wait
 
   pdl_wait();
+  ATT_TP(1);
   pdl_trigger();
   {  // RoPE of this kv head's G query heads and the new key (table lookup)
     const float* row = qkv + size_t(t) * (Hq + 2 * Hk) * D;
@@ -365,6 +389,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       vnew[d] = __float2half_rn(row[size_t(Hq + Hk + hk) * D + d]);
   }
   __syncthreads();
+  ATT_TP(2);
   if (sp == 0) {
     const size_t off = kv_off(slot[t], hk, Hk, D);
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
@@ -448,6 +473,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       }
     }
   }
+  ATT_TP(3);
   // merge the warps of this CTA
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -483,6 +509,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       }
     }
   }
+  ATT_TP(4);
   if (active == 1) return;
   // the last split to finish merges all partials of this (token, kv head)
   __threadfence();
@@ -511,6 +538,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     }
     o[(size_t(t) * Hq + hk * G + g) * D + d] = L > 0.0f ? __fdividef(A, L) : 0.0f;
   }
+  ATT_TP(5);
 }
 
 __global__ void attn_combine_kernel(const float* __restrict__ part_o,

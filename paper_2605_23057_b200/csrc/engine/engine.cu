@@ -169,10 +169,8 @@ struct Model {
   AttnShape ash{};
   BlockPool pool;
   std::vector<void*> allocations;
-  // decode-step graphs per format: [0] separate split-KV attention kernel,
-  // [1] attention fused into the QKV GEMV tail (ctx <= kAttnTailMaxCtx)
-  cudaGraphExec_t graph[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
-  int graph_nodes[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  int graph_nodes[3] = {0, 0, 0};
   // persistent decode step (decode_mk.cu), built on first use per format
   bool mk_ready[3] = {false, false, false};
   MkParams mk[3];
@@ -207,7 +205,6 @@ struct Scratch {
   int* logit_rows = nullptr;
   unsigned long long* amax_ws = nullptr;  // argmax slots + counters [2 * kMaxLogitRows], self-resetting
   int* split_cnt = nullptr;  // attention split-merge counters [tokens, kv heads], self-resetting
-  int* tail_cnt = nullptr;   // fused-attention tile counters [kv heads], self-resetting
   int* next = nullptr;
   int* step = nullptr;
   int* hist = nullptr;
@@ -400,9 +397,8 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
 }
 
 void free_model(Model& m) {
-  for (auto& gf : m.graph)
-    for (auto& g : gf)
-      if (g) cudaGraphExecDestroy(g);
+  for (auto& g : m.graph)
+    if (g) cudaGraphExecDestroy(g);
   for (void* p : m.allocations) cudaFree(p);
   m.allocations.clear();
 }
@@ -444,8 +440,6 @@ void alloc_scratch(msw_engine* e) {
   s.logit_rows = dalloc<int>(kMaxLogitRows);
   s.split_cnt = dalloc<int>(tsplit * 64);
   MSW_CUDA(cudaMemset(s.split_cnt, 0, sizeof(int) * tsplit * 64));
-  s.tail_cnt = dalloc<int>(64);
-  MSW_CUDA(cudaMemset(s.tail_cnt, 0, sizeof(int) * 64));
   s.next = dalloc<int>(kMaxLogitRows);
   s.amax_ws = dalloc<unsigned long long>(2 * kMaxLogitRows);
   MSW_CUDA(cudaMemset(s.amax_ws, 0, sizeof(unsigned long long) * 2 * kMaxLogitRows));
@@ -457,7 +451,7 @@ void alloc_scratch(msw_engine* e) {
   for (void* p : {(void*)s.h, (void*)s.qkv, (void*)s.q16, (void*)s.o, (void*)s.act, (void*)s.xh,
                   (void*)s.xq, (void*)s.xscale, (void*)s.hsel, (void*)s.logits, (void*)s.part_o,
                   (void*)s.part_ml, (void*)s.tok, (void*)s.pos, (void*)s.slot, (void*)s.seq_of,
-                  (void*)s.logit_rows, (void*)s.split_cnt, (void*)s.tail_cnt, (void*)s.next, (void*)s.amax_ws, (void*)s.step,
+                  (void*)s.logit_rows, (void*)s.split_cnt, (void*)s.next, (void*)s.amax_ws, (void*)s.step,
                   (void*)s.hist})
     e->owned.push_back(p);
 }
@@ -475,7 +469,7 @@ bool diag_skip(const char* what) {
 }
 
 void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_identity,
-             bool tokens_independent, bool fuse_attn = false) {
+             bool tokens_independent) {
   Scratch& s = e->sc;
   cudaStream_t st = e->st;
   const msw_model_cfg& c = m.c;
@@ -494,35 +488,15 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
     half* kc = m.kc + m.kv_layer_elems * l;
     half* vc = m.vc + m.kv_layer_elems * l;
     // attention block
-    const bool fused = fuse_attn && T == 1 && tokens_independent;
     if (small) {
-      AttnTail tail;
-      if (fused) {
-        tail.on = 1;
-        tail.rope = m.rope;
-        tail.pos = s.pos;
-        tail.slot = s.slot;
-        tail.block_table = m.block_table;  // batch-1 decode: row 0
-        tail.kc = kc;
-        tail.vc = vc;
-        tail.o = s.o;
-        tail.cnt = s.tail_cnt;
-        tail.Hq = Hq;
-        tail.Hk = Hk;
-        tail.D = D;
-      }
-      if (!diag_skip("qkv"))
-        launch_gemv(ly.qkv[fmt], kProNorm, kEpiStore, s.h, T, ly.attn_norm, eps, s.qkv, st,
-                    fused ? &tail : nullptr);
+      if (!diag_skip("qkv")) launch_gemv(ly.qkv[fmt], kProNorm, kEpiStore, s.h, T, ly.attn_norm, eps, s.qkv, st);
       ++n;
     } else {
       launch_prep_act(fmt, s.h, T, H, ly.attn_norm, eps, s.xh, s.xq, s.xscale, st);
       launch_gemm(ly.qkv[fmt], kEpiStore, s.xh, s.xq, s.xscale, T, s.qkv, st);
       n += 2;
     }
-    if (fused) {
-      // attention ran in the QKV GEMV's tail
-    } else if (tokens_independent) {  // decode / CB: RoPE + KV append fused into attention
+    if (tokens_independent) {  // decode / CB: RoPE + KV append fused into attention
       if (!diag_skip("attn")) launch_attention_decode(s.qkv, m.rope, T, s.pos, s.slot, s.seq_of, m.block_table, kc,
                               vc, m.ash, nsplit, s.part_o, s.part_ml, s.split_cnt, s.o, st);
       n += 1;
@@ -816,22 +790,16 @@ bool ensure_mk(msw_engine* e, Model& m, int fmt) {
   return true;
 }
 
-// One batch-1 decode step for model m / fmt, as a graph or eagerly. ctx =
-// positions the step attends over (the token's position + 1): up to
-// kAttnTailMaxCtx the attention runs fused in the QKV GEMV's tail.
-void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph, int ctx) {
+// One batch-1 decode step for model m / fmt, as a graph or eagerly.
+void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph) {
   Scratch& s = e->sc;
-  // opt-in: measured slower than the split-KV kernel on B200 (2.22 vs 2.00 ms
-  // per 8B W4 token): the group's last QKV CTA serialises the whole head
-  static const bool tail = std::getenv("MSW_ATTN_TAIL") != nullptr;
-  const int var = (tail && ctx <= kAttnTailMaxCtx) ? 1 : 0;
   if (ensure_mk(e, m, fmt)) {  // one persistent launch: forward + argmax + advance
     launch_decode_mk(fmt, m.mk[fmt], m.mk_smem[fmt], e->st);
     ++e->launches;
     return;
   }
   auto body = [&]() {
-    forward(e, m, fmt, 1, 1, true, true, var == 1);
+    forward(e, m, fmt, 1, 1, true, true);
     launch_advance(s.next, s.tok, s.pos, s.slot, s.step, s.hist, m.block_table, e->st);
     ++e->launches;
   };
@@ -839,7 +807,7 @@ void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph, int ctx) {
     body();
     return;
   }
-  if (!m.graph[fmt][var]) {
+  if (!m.graph[fmt]) {
     const long long before = e->launches;
     cudaGraph_t g;
     MSW_CUDA(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
@@ -850,13 +818,13 @@ void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph, int ctx) {
       throw;
     }
     MSW_CUDA(cudaStreamEndCapture(e->st, &g));
-    MSW_CUDA(cudaGraphInstantiate(&m.graph[fmt][var], g, 0));
+    MSW_CUDA(cudaGraphInstantiate(&m.graph[fmt], g, 0));
     cudaGraphDestroy(g);
-    m.graph_nodes[fmt][var] = int(e->launches - before);
+    m.graph_nodes[fmt] = int(e->launches - before);
     e->launches = before;
   }
-  MSW_CUDA(cudaGraphLaunch(m.graph[fmt][var], e->st));
-  e->launches += m.graph_nodes[fmt][var];
+  MSW_CUDA(cudaGraphLaunch(m.graph[fmt], e->st));
+  e->launches += m.graph_nodes[fmt];
 }
 
 // Sets the batch-1 decode state so the next decode_step processes `tok_src`
@@ -914,7 +882,7 @@ void run_single(msw_engine* e, const msw_request& r, msw_result& res) {
     start_decode(e, m, e->sc.next, r.prompt_len - 1, 0);
     MSW_CUDA(cudaEventRecord(e->ev[1], e->st));
     for (int i = 1; i < n_new; ++i) {
-      decode_step(e, m, fmt, graphs, r.prompt_len + i);
+      decode_step(e, m, fmt, graphs);
       if (want_logits) copy_logits_row(e, res.logits + size_t(i) * m.c.vocab, 0);
     }
     MSW_CUDA(cudaEventRecord(e->ev[2], e->st));
@@ -1008,7 +976,7 @@ void run_spec(msw_engine* e, const msw_request& r, msw_result& res) {
       s.stage[0] = seq[n - 1];
       MSW_CUDA(cudaMemcpyAsync(s.next, s.stage, sizeof(int), cudaMemcpyHostToDevice, e->st));
       start_decode(e, dr, s.next, n - 2, 0);  // tok = seq[n-1], pos = n-1, hist[0] = seq[n-1]
-      for (int i = 0; i < k; ++i) decode_step(e, dr, kFP16, graphs, n + i);
+      for (int i = 0; i < k; ++i) decode_step(e, dr, kFP16, graphs);
       // hist[1..k] are the proposals
       MSW_CUDA(cudaMemcpyAsync(s.stage + 8, s.hist + 1, sizeof(int) * k, cudaMemcpyDeviceToHost, e->st));
       MSW_CUDA(cudaStreamSynchronize(e->st));

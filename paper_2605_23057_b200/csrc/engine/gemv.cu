@@ -237,163 +237,6 @@ __device__ __forceinline__ void store_pair(float* y, int n, int t, int row, floa
   }
 }
 
-// ------------------------------------------------------ fused attention tail
-thread_local AttnTail t_tail;  // set by launch_gemv for the launch being issued
-
-__device__ __forceinline__ int tail_group(const AttnTail& at, int tile) {
-  const int row = tile * 16, G = at.Hq / at.Hk;
-  if (row < at.Hq * at.D) return (row / at.D) / G;
-  if (row < (at.Hq + at.Hk) * at.D) return (row - at.Hq * at.D) / at.D;
-  return (row - (at.Hq + at.Hk) * at.D) / at.D;
-}
-
-// Epilogue warp, after storing qkv tile `tile`: count it for its kv-head
-// group; the CTA that completes a group records it for its consumers.
-__device__ __forceinline__ void tail_count(const AttnTail& at, int tile, int* list, int* n) {
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) {
-    __threadfence();
-    const int grp = tail_group(at, tile);
-    const int tpg = (at.Hq / at.Hk + 2) * at.D / 16;
-    if (atomicAdd(&at.cnt[grp], 1) == tpg - 1) {
-      at.cnt[grp] = 0;  // self-reset for the next launch
-      __threadfence();
-      list[(*n)++] = grp;
-    }
-  }
-  __syncwarp();
-}
-
-// Attention of kv head hk for the single new token (consumer threads, named
-// barrier 1). Numerics as attn_decode_kernel: fp16 q / k / v after RoPE, fp32
-// scores, softmax (__expf) and accumulation, scale 1/sqrt(D). K / V of up to
-// R positions per round arrive as cp.async.bulk copies of whole 16-position
-// paged blocks (16 x D fp16 contiguous per head) into the drained ring.
-template <int D>
-__device__ void attn_tail_run(const AttnTail& at, int hk, const float* __restrict__ qkv,
-                              uint8_t* buf, int buf_bytes, uint64_t* bar, uint32_t& par) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = at.Hq / at.Hk, Hq = at.Hq, Hk = at.Hk;
-  const int p_self = at.pos[0], ctx = p_self + 1;
-  // smem: scores [G][R] | q [G][D] f32 | knew, vnew [D] f16 | K [R][D] | V [R][D]
-  const int fixed = G * 256 * 4 + G * D * 4 + 2 * D * 2;
-  int R = ((buf_bytes - fixed) / (4 * D)) / 32 * 32;
-  R = min(256, R);
-  float* scs = reinterpret_cast<float*>(buf);
-  float* qs = scs + G * 256;
-  half* knew = reinterpret_cast<half*>(qs + G * D);
-  half* vnew = knew + D;
-  half* Kb = reinterpret_cast<half*>(buf + ((fixed + 127) & ~127));
-  half* Vb = Kb + R * D;
-  {
-    const float* row = qkv;
-    const float2* rp = at.rope + size_t(p_self) * (D / 2);
-    for (int i = tid; i < (G + 1) * (D / 2); i += kConsThreads) {
-      const int h = i / (D / 2), j = i % (D / 2);
-      const float* src = h < G ? row + size_t(hk * G + h) * D : row + size_t(Hq + hk) * D;
-      const float2 r = rp[j];
-      const float x0 = __ldcg(src + j), x1 = __ldcg(src + j + D / 2);
-      const half y0 = __float2half_rn(__fsub_rn(__fmul_rn(x0, r.x), __fmul_rn(x1, r.y)));
-      const half y1 = __float2half_rn(__fadd_rn(__fmul_rn(x1, r.x), __fmul_rn(x0, r.y)));
-      if (h < G) {
-        qs[h * D + j] = __half2float(y0);
-        qs[h * D + j + D / 2] = __half2float(y1);
-      } else {
-        knew[j] = y0;
-        knew[j + D / 2] = y1;
-      }
-    }
-    for (int d = tid; d < D; d += kConsThreads)
-      vnew[d] = __float2half_rn(__ldcg(row + size_t(Hq + Hk + hk) * D + d));
-  }
-  named_sync(1, kConsThreads);
-  {
-    const int s = at.slot[0];
-    const size_t off = ((size_t(s >> 4) * Hk + hk) * 16 + (s & 15)) * size_t(D);
-    for (int d = tid; d < D; d += kConsThreads) {
-      at.kc[off + d] = knew[d];
-      at.vc[off + d] = vnew[d];
-    }
-  }
-  const float scale = rsqrtf(float(D));
-  const bool owner = tid < G * D;
-  const int og = owner ? tid / D : 0, od = tid % D;
-  float M = -INFINITY, L = 0.0f, A = 0.0f;
-  constexpr int DPL = D / 16;
-  const int ql = lane & 15;
-#pragma unroll 1
-  for (int r0 = 0; r0 < ctx; r0 += R) {
-    const int n = min(R, ctx - r0);
-    if (tid == 0) {
-      const int nblk = (n + 15) / 16;
-      const uint32_t bb = 16 * D * 2;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(bar, 2 * nblk * bb);
-      for (int b = 0; b < nblk; ++b) {
-        const size_t off = (size_t(at.block_table[(r0 >> 4) + b]) * Hk + hk) * 16 * D;
-        bulk_g2s(Kb + b * 16 * D, at.kc + off, bb, bar);
-        bulk_g2s(Vb + b * 16 * D, at.vc + off, bb, bar);
-      }
-    }
-    mbar_wait(bar, par);
-    par ^= 1;
-    // QK: 2 positions per warp per step (16 lanes x D/16 dims each)
-    for (int pb = 2 * warp; pb < n; pb += 2 * kConsumers) {  // warp-uniform trip count
-      const int pp = pb + (lane >> 4);
-      const bool valid = pp < n;
-      const half* kr = (r0 + pp) == p_self ? knew : Kb + (valid ? pp : pb) * D;
-      float sg[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < DPL; c += 4) {
-        const uint2 kv = *reinterpret_cast<const uint2*>(kr + ql * DPL + c);
-        const float2 k0 = __half22float2(*reinterpret_cast<const half2*>(&kv.x));
-        const float2 k1 = __half22float2(*reinterpret_cast<const half2*>(&kv.y));
-#pragma unroll
-        for (int gg = 0; gg < 4; ++gg)
-          if (gg < G) {
-            const float4 q0 = *reinterpret_cast<const float4*>(qs + gg * D + ql * DPL + c);
-            sg[gg] = fmaf(q0.x, k0.x, fmaf(q0.y, k0.y, fmaf(q0.z, k1.x, fmaf(q0.w, k1.y, sg[gg]))));
-          }
-      }
-#pragma unroll
-      for (int gg = 0; gg < 4; ++gg)
-        if (gg < G) {
-#pragma unroll
-          for (int o = 8; o > 0; o >>= 1) sg[gg] += __shfl_xor_sync(0xffffffffu, sg[gg], o);
-          if (ql == 0 && valid) scs[gg * 256 + pp] = sg[gg] * scale;
-        }
-    }
-    named_sync(1, kConsThreads);
-    if (owner) {
-      float mx = M;
-      for (int j = 0; j < n; ++j) mx = fmaxf(mx, scs[og * 256 + j]);
-      const float corr = __expf(M - mx);
-      A *= corr;
-      L *= corr;
-      M = mx;
-#pragma unroll 4
-      for (int j = 0; j < n; ++j) {
-        const float e = __expf(scs[og * 256 + j] - mx);
-        const half v = (r0 + j) == p_self ? vnew[od] : Vb[j * D + od];
-        L += e;
-        A = fmaf(e, __half2float(v), A);
-      }
-    }
-    named_sync(1, kConsThreads);  // buffers and scores are free for the next round
-  }
-  if (owner) at.o[size_t(hk * G + og) * D + od] = L > 0.0f ? __fdividef(A, L) : 0.0f;
-}
-
-__device__ __forceinline__ void attn_tail(const AttnTail& at, const int* list, int n,
-                                          const float* qkv, uint8_t* buf, int buf_bytes,
-                                          uint64_t* bar) {
-  uint32_t par = 0;
-  for (int i = 0; i < n; ++i) {
-    if (at.D == 128) attn_tail_run<128>(at, list[i], qkv, buf, buf_bytes, bar, par);
-    else attn_tail_run<64>(at, list[i], qkv, buf, buf_bytes, bar, par);
-  }
-}
-
 // Warp roles (one CTA per SM, a contiguous range of 16-row tiles):
 //   warps 0..kConsumers-1 : consumers. Every contiguous 16 KB ring stage holds
 //                           S chunks of one tile; warp w takes CPW of them.
@@ -408,7 +251,7 @@ template <int FMT, int PRO, int EPI, int NT, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_tf_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
                    const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
-                   float* __restrict__ y, int n_stages, const AttnTail tail) {
+                   float* __restrict__ y, int n_stages) {
   using Acc = typename std::conditional<FMT == kINT8, int, float>::type;
   constexpr int CK = TF<FMT>::kChunkK;
   constexpr int CPW = (S / kConsumers) > TF<FMT>::kMinChunksPerWarp ? (S / kConsumers)
@@ -422,8 +265,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ float xscale[NT];
   __shared__ __align__(16) uint32_t part[2][kConsumers][16][8];  // per-warp tile partials
   __shared__ __align__(16) uint8_t zero_b[64];
-  __shared__ uint64_t tail_bar;
-  __shared__ int tail_list[8], tail_n;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunks_tile = k / CK;
@@ -454,8 +295,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tile_full[b], ACTIVE);
       mbar_init(&tile_free[b], 1);
     }
-    mbar_init(&tail_bar, 1);
-    tail_n = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -532,11 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           store_pair<EPI>(y, n, col, tile * 16 + row, v0, v1);
         }
       }
-      if (tail.on) tail_count(tail, tile, tail_list, &tail_n);
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_free[b]);
     }
-    if (tail.on) named_sync(4, kConsThreads + 32);  // hand the completed groups to the consumers
     return;
   }
 
@@ -653,10 +490,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++ti;
     }
   }
-  if (tail.on) {
-    named_sync(4, kConsThreads + 32);
-    attn_tail(tail, tail_list, tail_n, y, ring, n_stages * STAGE_BYTES, &tail_bar);
-  }
 }
 
 // W4 decode GEMV, issue-lean variant (8B shapes: K = 4096 and K = 14336).
@@ -680,7 +513,7 @@ template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_w4_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
                    const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
-                   float* __restrict__ y, int n_stages, const AttnTail tail) {
+                   float* __restrict__ y, int n_stages, uint32_t /*unused*/) {
   constexpr int WPG = kConsumers / GW;  // warps sharing one stage
   constexpr int CPW = S / WPG;          // chunks per warp per stage
   static_assert(CPW == 4, "two 128-k groups per warp per stage");
@@ -691,8 +524,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ float red[32];
   __shared__ float xscale[NT];
   __shared__ __align__(16) float part[2][kConsumers][16][8];
-  __shared__ uint64_t tail_bar;
-  __shared__ int tail_list[8], tail_n;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunks_tile = k / 64;
@@ -720,8 +551,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tile_full[b], kConsumers);
       mbar_init(&tile_free[b], 1);
     }
-    mbar_init(&tail_bar, 1);
-    tail_n = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -772,13 +601,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (col < T) store_pair<EPI>(y, n, col, tile * 16 + row, v0, v1);
       }
-      if (tail.on) tail_count(tail, tile, tail_list, &tail_n);
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_free[b]);
       if (lane == 0 && i == 0) MSW_TP(8);  // first tile stored
     }
     if (lane == 0) MSW_TP(9);  // all tiles stored
-    if (tail.on) named_sync(4, kConsThreads + 32);  // hand the completed groups to the consumers
     return;
   }
 
@@ -911,10 +738,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (cur >= 0) flush(cur);
   if (threadIdx.x == 0) MSW_TP(7);  // warp 0 done
-  if (tail.on) {
-    named_sync(4, kConsThreads + 32);
-    attn_tail(tail, tail_list, tail_n, y, ring, n_stages * STAGE_BYTES, &tail_bar);
-  }
 }
 
 // --------------------------------------------------------------- repacking
@@ -991,7 +814,7 @@ void launch_tf_s(const LinearW& W, const float* x, int T, const half* gamma, flo
     attr_done = true;
   }
   launch_pdl(gemv_tf_kernel<FMT, PRO, EPI, NT, S>, dim3(grid), dim3(kThreads), smem, st,
-             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages, t_tail);
+             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages);
 }
 
 template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
@@ -1016,7 +839,8 @@ void launch_w4(const LinearW& W, const float* x, int T, const half* gamma, float
     attr_done = true;
   }
   launch_pdl(gemv_w4_kernel<PRO, EPI, NT, S, GW, XREG>, dim3(grid), dim3(kThreads), smem, st,
-             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages, t_tail);
+             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages,
+             uint32_t(1u << 24));
 }
 
 template <int FMT, int PRO, int EPI, int NT>
@@ -1090,13 +914,8 @@ extern "C" int msw_trace_set(void* buf) {
 #endif
 
 void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
-                 float eps, float* y, cudaStream_t st, const AttnTail* tail) {
+                 float eps, float* y, cudaStream_t st) {
   if (W.n % 16 != 0 || W.k % 128 != 0) throw ConfigErr("gemv: n % 16, k % 128 required");
-  if (tail && (T != 1 || epi != kEpiStore)) throw ConfigErr("gemv: attention tail needs T == 1, store");
-  struct TailScope {  // the tail applies to this launch only
-    explicit TailScope(const AttnTail* t) { t_tail = t ? *t : AttnTail{}; }
-    ~TailScope() { t_tail = AttnTail{}; }
-  } tail_scope(tail);
   if (T < 1 || T > kGemvMaxTokens) throw ConfigErr("gemv: 1..6 tokens");
   if (!W.w_tf) throw ConfigErr("gemv: decode (tile-fragment) weight layout missing");
   switch (W.fmt) {

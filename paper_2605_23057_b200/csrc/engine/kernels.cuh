@@ -47,26 +47,8 @@ enum Epilogue { kEpiStore = 0, kEpiResid = 1, kEpiSwiglu = 2 };
 // kEpiStore: y[n] = v; kEpiResid: y[n] += v; kEpiSwiglu: y[i] = silu(v[2i]) * v[2i+1].
 // x is fp32 [T, k], 1 <= T <= kGemvMaxTokens; y rows are per token.
 constexpr int kGemvMaxTokens = 6;
-// Batch-1 decode attention fused into the tail of the QKV GEMV (T = 1): the
-// CTA whose epilogue stores the last q/k/v tile of a kv-head group (per-group
-// counter) runs that group's RoPE + KV append + attention over [0, pos] on its
-// idle consumer warps, staging K/V through the drained weight ring. Used when
-// ctx <= kAttnTailMaxCtx; o is written directly (no split merge).
-struct AttnTail {
-  int on = 0;
-  const float2* rope = nullptr;
-  const int* pos = nullptr;          // pos[0]: the token's position
-  const int* slot = nullptr;         // slot[0]: its KV slot
-  const int* block_table = nullptr;  // row 0
-  half* kc = nullptr;                // this layer's K / V pool
-  half* vc = nullptr;
-  float* o = nullptr;                // [Hq * D]
-  int* cnt = nullptr;                // [Hk] self-resetting tile counters
-  int Hq = 0, Hk = 0, D = 0;
-};
-constexpr int kAttnTailMaxCtx = 1024;
 void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
-                 float eps, float* y, cudaStream_t st, const AttnTail* tail = nullptr);
+                 float eps, float* y, cudaStream_t st);
 void launch_gemv_i8_acc(const int8_t* w, const int8_t* x, int n, int k, int* acc, cudaStream_t st);
 // row-major weights (FP16 half / INT8 int8 / W4 row-packed words) -> the
 // tile-fragment layout the decode GEMV streams (same byte count)
