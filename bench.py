@@ -270,9 +270,20 @@ def run_ours(args):
     wbytes = {name: eng.weight_bytes(m) for m, name in MODES}
     prompts = [synth_prompt(1000 * rank + i, PROMPT, 128256) for i in range(args.warmup + args.steps)]
 
-    def one_step(p):
+    from paper_2605_23057_b200.energy import PowerSampler
+    energy = {name: [] for _, name in MODES}
+
+    def one_step(p, measure_energy=False):
         out = {}
         for m, name in MODES:
+            if measure_energy:
+                try:  # whole-GPU power over the request, reference trapezoid rule
+                    with PowerSampler(local, period_ms=5.0) as ps:
+                        out[name] = eng.run(m, p, NEW)
+                        energy[name].append(ps.finish(NEW))
+                    continue
+                except Exception:
+                    pass
             out[name] = eng.run(m, p, NEW)
         return out
 
@@ -287,7 +298,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         t_wall = time.perf_counter()
         for i in range(args.steps):
-            res = one_step(prompts[args.warmup + i])
+            res = one_step(prompts[args.warmup + i], measure_energy=True)
             for _, name in MODES:
                 r = res[name]
                 a = agg[name]
@@ -325,6 +336,12 @@ def run_ours(args):
                           "weight_bytes_per_token": wbytes[name],
                           "hbm_frac_of_measured": wbytes[name] * tps / 1e9 / peaks()[0],
                           "latency_speedup_vs_fp16": statistics.mean(speedups[name])}
+        if energy[name]:
+            per_mode[name]["joules_per_token"] = statistics.mean(energy[name])
+    if energy["fp16"]:
+        for _, name in MODES:
+            if energy[name]:  # reference ratio_vs_baseline(mode, fp16) = mode / fp16 (domain.cpp:118-133)
+                per_mode[name]["energy_ratio_vs_fp16"] = statistics.mean(energy[name]) / statistics.mean(energy["fp16"])
     kern = time_dominant_kernel()
     peak, peak_kind = peaks()
     launches = sum(agg[n]["launches"] for _, n in MODES)
@@ -489,9 +506,39 @@ def run_configs(args):
     eng.close()
 
 
+def run_profile(args):
+    """Measured B200 profile in the reference's load_profile schema:
+    every family's nominal request in every mode, 8B target + 1B draft, written
+    to --profile-out. Prints one JSON line summarising it."""
+    import torch
+    from paper_2605_23057_b200 import ALL_MODES, engine_cfg
+    from paper_2605_23057_b200.configs import MODE_FP16
+    from paper_2605_23057_b200.engine import Engine
+    from paper_2605_23057_b200.profile_writer import build_profile, measure, write_profile
+    _, rank, local = _dist()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    eng = Engine(engine_cfg(target="llama8b", draft="llama1b", modes=ALL_MODES, seed=0,
+                            kv_blocks=1024, max_batch=8, max_seq_len=2048 + 512), device=local)
+    t0 = time.perf_counter()
+    meas = measure(eng, device=local, out_cap=args.profile_out_cap)
+    fp16 = [m for (mode, _), m in meas.items() if mode == MODE_FP16]
+    e16 = [m["energy_j_per_token"] for m in fp16 if m["energy_j_per_token"]]
+    prof = build_profile(meas, statistics.mean(e16) if e16 else 0.0,
+                         max(m["mem_bytes"] for m in fp16) / 2**20)
+    write_profile(args.profile_out, prof)
+    eng.close()
+    print(json.dumps({"workload": "profile", "out": args.profile_out, "cells": len(prof["cells"]),
+                      "baseline_costs": prof["baseline_costs"], "wall_s": time.perf_counter() - t0}),
+          flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", choices=["decode8b", "mix", "configs"], default="decode8b")
+    ap.add_argument("--workload", choices=["decode8b", "mix", "configs", "profile"], default="decode8b")
+    ap.add_argument("--profile-out", default="profiles/b200_profile.json")
+    ap.add_argument("--profile-out-cap", type=int, default=0, help="cap generated tokens per request")
     ap.add_argument("--cfg-requests", type=int, default=8)
     ap.add_argument("--mix-per-class", type=int, default=4)
     ap.add_argument("--gpus", type=int, default=1)
@@ -506,6 +553,8 @@ def main():
         run_mix(args)
     elif args.workload == "configs":
         run_configs(args)
+    elif args.workload == "profile":
+        run_profile(args)
     else:
         run_ours(args)
 

@@ -9,6 +9,9 @@
 //   <name>.ndjson / <name>.decisions.csv for every trace below; each decision
 //   row is request_id,mode,reason,class,family from the reference's
 //   RulePolicy::route, classify(extract_features()) and resolve_family.
+//   power_<k>.csv + power_golden.csv: power traces written by the reference's
+//   write_power_trace and their energy_from_power_trace (J/token, %.17g) or
+//   the DataError it raises (sim.cpp:10-78).
 #include <cstdio>
 #include <fstream>
 #include <random>
@@ -17,6 +20,8 @@
 
 #include "modeswitch/classifier.hpp"
 #include "modeswitch/routing.hpp"
+#include "modeswitch/profile.hpp"
+#include "modeswitch/sim.hpp"
 #include "modeswitch/trace_io.hpp"
 #include "modeswitch/workload.hpp"
 
@@ -39,6 +44,17 @@ static void emit(const std::string& dir, const std::string& name,
 }
 
 int main(int argc, char** argv) {
+  if (argc == 3 && std::string(argv[1]) == "--check-profile") {
+    // the reference's own loader + validate() on a profile written by this repo
+    try {
+      const ms::ProfileTable t = ms::load_profile(argv[2]);
+      std::printf("ok %zu families\n", t.families().size());
+      return 0;
+    } catch (const std::exception& e) {
+      std::printf("error %s\n", e.what());
+      return 3;
+    }
+  }
   if (argc != 2) {
     std::fprintf(stderr, "usage: %s <out_dir>\n", argv[0]);
     return 2;
@@ -119,6 +135,37 @@ int main(int argc, char** argv) {
       trace.push_back(r);
     }
     emit(dir, "boundary_fuzz", trace);
+  }
+    // (power) energy per token over deterministic traces, incl. error cases
+  {
+    std::ofstream g(dir + "/power_golden.csv");
+    g << "name,tokens,joules_per_token\n";
+    std::mt19937_64 rng(20260517);
+    std::uniform_real_distribution<double> watts(120.0, 1000.0), step(5.0, 80.0);
+    const int lens[] = {2, 3, 17, 200};
+    const int toks[] = {1, 7, 128, 1000};
+    for (int k = 0; k < 6; ++k) {
+      ms::PowerTrace tr;
+      const int n = k < 4 ? lens[k] : 12;
+      double t = 1000.0 * k;
+      for (int i = 0; i < n; ++i) {
+        tr.samples.push_back({t, watts(rng)});
+        t += step(rng);
+      }
+      if (k == 4) tr.samples[5].timestamp_ms = tr.samples[4].timestamp_ms;  // not increasing
+      if (k == 5) tr.samples[3].power_w = -1.0;                             // negative power
+      const std::string name = "power_" + std::to_string(k);
+      ms::write_power_trace(tr, dir + "/" + name + ".csv");
+      const int tokens = toks[k % 4];
+      char buf[64];
+      try {
+        std::snprintf(buf, sizeof(buf), "%.17g",
+                      ms::energy_from_power_trace(ms::read_power_trace(dir + "/" + name + ".csv"), tokens));
+        g << name << ',' << tokens << ',' << buf << '\n';
+      } catch (const ms::DataError&) {
+        g << name << ',' << tokens << ",DataError\n";
+      }
+    }
   }
   return 0;
 }

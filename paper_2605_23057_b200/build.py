@@ -99,7 +99,7 @@ def build_host(force: bool = False) -> str:
     if force or _stale(HOST_SO, deps):
         _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra",
               "-I", INC, "-I", NLOHMANN, *srcs, "-o", HOST_SO,
-              "-L", LIB, "-lmsw_engine", "-Wl,-rpath,$ORIGIN", "-lpthread"])
+              "-L", LIB, "-lmsw_engine", "-Wl,-rpath,$ORIGIN", "-lpthread", "-ldl"])
     return HOST_SO
 
 

@@ -1,0 +1,138 @@
+// Power traces and energy per token (include/modeswitch/energy.hpp).
+#include "modeswitch/energy.hpp"
+
+#include <dlfcn.h>
+
+#include <chrono>
+#include <cstdio>
+#include <fstream>
+#include <sstream>
+#include <string>
+
+#include "modeswitch/domain.hpp"
+
+namespace modeswitch {
+
+PowerTrace read_power_trace(const std::filesystem::path& path) {
+  std::ifstream in(path);
+  if (!in) throw DataError("cannot open power trace: " + path.string());
+  std::string line;
+  if (!std::getline(in, line) || line != "timestamp_ms,power_w")
+    throw DataError("power trace " + path.string() + ": expected header 'timestamp_ms,power_w'");
+  PowerTrace trace;
+  size_t no = 1;
+  while (std::getline(in, line)) {
+    ++no;
+    if (line.empty()) continue;
+    const size_t comma = line.find(',');
+    if (comma == std::string::npos || comma + 1 >= line.size())
+      throw DataError(path.string() + ":" + std::to_string(no) + ": malformed power sample");
+    try {
+      trace.samples.push_back({std::stod(line.substr(0, comma)), std::stod(line.substr(comma + 1))});
+    } catch (const std::exception&) {
+      throw DataError(path.string() + ":" + std::to_string(no) + ": non-numeric power sample");
+    }
+  }
+  return trace;
+}
+
+void write_power_trace(const PowerTrace& trace, const std::filesystem::path& path) {
+  std::ofstream out(path);
+  if (!out) throw DataError("cannot write power trace: " + path.string());
+  out << "timestamp_ms,power_w\n";
+  char buf[96];
+  for (const auto& s : trace.samples) {
+    std::snprintf(buf, sizeof(buf), "%.17g,%.17g", s.timestamp_ms, s.power_w);
+    out << buf << '\n';
+  }
+}
+
+double energy_from_power_trace(const PowerTrace& trace, int tokens) {
+  if (trace.samples.size() < 2) throw DataError("power trace needs at least 2 samples to integrate");
+  if (tokens < 1) throw DataError("energy_from_power_trace: tokens must be positive");
+  double joules = 0.0;
+  for (size_t i = 0; i + 1 < trace.samples.size(); ++i) {
+    const auto& a = trace.samples[i];
+    const auto& b = trace.samples[i + 1];
+    if (!(b.timestamp_ms > a.timestamp_ms))
+      throw DataError("power trace timestamps must be strictly increasing");
+    if (a.power_w < 0.0 || b.power_w < 0.0) throw DataError("power trace samples must be nonnegative");
+    joules += 0.5 * (a.power_w + b.power_w) * (b.timestamp_ms - a.timestamp_ms) / 1000.0;
+  }
+  return joules / tokens;
+}
+
+// ---- NVML, resolved at run time (no link dependency on the driver library)
+namespace {
+struct Nvml {
+  using InitFn = int (*)();
+  using HandleFn = int (*)(unsigned, void**);
+  using PowerFn = int (*)(void*, unsigned*);
+  InitFn init = nullptr;
+  HandleFn handle = nullptr;
+  PowerFn power = nullptr;
+  bool ok = false;
+  Nvml() {
+    void* lib = dlopen("libnvidia-ml.so.1", RTLD_LAZY | RTLD_LOCAL);
+    if (!lib) lib = dlopen("libnvidia-ml.so", RTLD_LAZY | RTLD_LOCAL);
+    if (!lib) return;
+    init = reinterpret_cast<InitFn>(dlsym(lib, "nvmlInit_v2"));
+    handle = reinterpret_cast<HandleFn>(dlsym(lib, "nvmlDeviceGetHandleByIndex_v2"));
+    power = reinterpret_cast<PowerFn>(dlsym(lib, "nvmlDeviceGetPowerUsage"));  // milliwatts
+    ok = init && handle && power && init() == 0;
+  }
+};
+Nvml& nvml() {
+  static Nvml n;
+  return n;
+}
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+}  // namespace
+
+PowerSampler::PowerSampler(int device, double period_ms) : device_(device), period_ms_(period_ms) {
+  if (!nvml().ok) throw ConfigError("NVML unavailable: cannot sample GPU power");
+  if (nvml().handle(unsigned(device), &dev_handle_) != 0)
+    throw ConfigError("NVML: no handle for device " + std::to_string(device));
+}
+
+PowerSampler::~PowerSampler() {
+  if (running_) stop();
+}
+
+void PowerSampler::sample_once() {
+  unsigned mw = 0;
+  if (nvml().power(dev_handle_, &mw) != 0) return;
+  const double t = now_ms() - t0_;
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!trace_.samples.empty() && !(t > trace_.samples.back().timestamp_ms)) return;
+  trace_.samples.push_back({t, mw / 1000.0});
+}
+
+void PowerSampler::start() {
+  if (running_) return;
+  trace_.samples.clear();
+  t0_ = now_ms();
+  sample_once();
+  running_ = true;
+  thread_ = std::thread([this] {
+    while (running_) {
+      std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(period_ms_));
+      sample_once();
+    }
+  });
+}
+
+PowerTrace PowerSampler::stop() {
+  if (running_) {
+    running_ = false;
+    thread_.join();
+  }
+  sample_once();
+  std::lock_guard<std::mutex> lk(mu_);
+  return trace_;
+}
+
+}  // namespace modeswitch

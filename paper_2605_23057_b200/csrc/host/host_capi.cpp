@@ -1,10 +1,12 @@
 // C ABI over the host controller (include/msw_host.h).
 #include <chrono>
+#include <memory>
 #include <cstring>
 #include <sstream>
 #include <string>
 
 #include "modeswitch/classifier.hpp"
+#include "modeswitch/energy.hpp"
 #include "modeswitch/executor.hpp"
 #include "modeswitch/routing.hpp"
 #include "modeswitch/trace_io.hpp"
@@ -251,6 +253,40 @@ int msw_execute_trace(struct msw_engine* engine, int32_t vocab, const char* ndjs
       summary->mode_time_ms = p.mode_time_ms;
       summary->generated_tokens = p.generated_tokens;
     }
+  });
+}
+
+struct msw_power_sampler {
+  ms::PowerSampler impl;
+  msw_power_sampler(int d, double p) : impl(d, p) {}
+};
+
+int msw_power_start(int32_t device, double period_ms, msw_power_sampler** out) {
+  return guarded([&] {
+    if (!out) throw ms::ConfigError("msw_power_start: out is NULL");
+    if (!(period_ms > 0.0)) throw ms::ConfigError("msw_power_start: period_ms must be positive");
+    auto* s = new msw_power_sampler(device, period_ms);
+    s->impl.start();
+    *out = s;
+  });
+}
+
+int msw_power_stop(msw_power_sampler* s, const char* csv_path, int32_t tokens,
+                   double* joules_per_token, int32_t* n_samples) {
+  return guarded([&] {
+    if (!s) throw ms::ConfigError("msw_power_stop: sampler is NULL");
+    std::unique_ptr<msw_power_sampler> own(s);
+    const ms::PowerTrace tr = own->impl.stop();
+    if (n_samples) *n_samples = int32_t(tr.samples.size());
+    if (csv_path && *csv_path) ms::write_power_trace(tr, csv_path);
+    if (joules_per_token) *joules_per_token = ms::energy_from_power_trace(tr, tokens);
+  });
+}
+
+int msw_energy_from_trace(const char* csv_path, int32_t tokens, double* joules_per_token) {
+  return guarded([&] {
+    if (!csv_path || !joules_per_token) throw ms::ConfigError("msw_energy_from_trace: NULL argument");
+    *joules_per_token = ms::energy_from_power_trace(ms::read_power_trace(csv_path), tokens);
   });
 }
 

@@ -102,6 +102,17 @@ class Engine:
         check_engine(engine_lib().msw_engine_run_batch(self.h, reqs, n, ress))
         return [self._wrap(o, l, ress[i]) for i, (o, l) in enumerate(outs)]
 
+    def has_mode(self, mode: int) -> bool:
+        """Mode resident in this engine (modes_mask; speculative decoding also needs a draft)."""
+        if mode == 4 and not self.cfg.has_draft:
+            return False
+        return bool(self.cfg.modes_mask & (1 << mode))
+
+    def kv_bytes_per_position(self) -> int:
+        """K + V fp16 bytes one token position occupies in the target's paged cache."""
+        t = self.cfg.target
+        return 2 * t.n_layers * t.n_kv_heads * t.head_dim * 2
+
     def weight_bytes(self, mode: int) -> int:
         b = C.c_int64()
         check_engine(engine_lib().msw_engine_weight_bytes(self.h, mode, C.byref(b)))

@@ -1,1 +1,3 @@
-for i in 1 2 3 4 5; do timeout -s KILL 300 python -m pytest tests/test_kernels_gpu.py -q -k "test_linear_formats_vs_oracle" > gpurun_out/kt_$i.log 2>&1; echo "EXIT $?" >> gpurun_out/kt_$i.log; done
+timeout -s KILL 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "EXIT $?" >> gpurun_out/gpu_tests.log
+timeout -s KILL 900 python bench.py > gpurun_out/bench_default.log 2>&1
+timeout -s KILL 1200 python bench.py --workload profile --profile-out gpurun_out/b200_profile.json > gpurun_out/bench_profile.log 2>&1
