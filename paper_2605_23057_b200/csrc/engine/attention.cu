@@ -290,6 +290,18 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   }
 }
 
+// Decode kernel geometry: 8 warps x 32 positions per CTA and >= 256 positions
+// per split, so a context of up to 256 positions is one CTA per kv head with
+// one tile per warp and no cross-CTA merge. (Measured in-graph, 8B W4, ctx 202:
+// the 4-warp / 64-position version spent 6.5 of its 17.8 us per layer in the
+// fence + atomic + last-CTA split merge; scripts/attn_timeline.py.)
+constexpr int kDecWarps = 8;
+constexpr int kDecMinChunk = 256;
+__device__ __forceinline__ int split_chunk_dec(int ctx, int nsplit) {
+  const int c = (ctx + nsplit - 1) / nsplit;
+  return ((max(c, kDecMinChunk) + 31) / 32) * 32;
+}
+
 // Decode / continuous-batching attention (each query token is the newest
 // token of its own sequence). Per CTA: one (token, kv head, split).
 //  * before griddepcontrol.wait: the K rows and V slices of the first tile of
@@ -313,7 +325,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kAttnWarps * 32)
+__global__ void __launch_bounds__(kDecWarps * 32)
     attn_decode_kernel(const float* __restrict__ qkv, const float2* __restrict__ rope,
                        const int* __restrict__ pos, const int* __restrict__ slot,
                        const int* __restrict__ seq_of, const int* __restrict__ block_table,
@@ -325,15 +337,15 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   extern __shared__ __align__(16) half kv_smem[];  // [warp][K|V][32][RS]
   __shared__ __align__(16) float qs[G][D];
   __shared__ __align__(16) half knew[D], vnew[D];
-  __shared__ float wm[kAttnWarps][G], wl[kAttnWarps][G];
-  __shared__ float wacc[kAttnWarps][G][D];
+  __shared__ float wm[kDecWarps][G], wl[kDecWarps][G];
+  __shared__ float wacc[kDecWarps][G][D];
   __shared__ int is_last;
   const int t = blockIdx.x, hk = blockIdx.y, sp = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   ATT_TP(0);
   const int p_self = pos[t];
   const int ctx = p_self + 1;
-  const int chunk = split_chunk(ctx, nsplit);
+  const int chunk = split_chunk_dec(ctx, nsplit);
   const int begin = sp * chunk;
   if (begin >= ctx) {
     pdl_wait();
@@ -407,7 +419,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     for (int d = 0; d < DPL; ++d) acc[g][d] = 0.0f;
   }
 #pragma unroll 1
-  for (int base = first; base < end; base += kAttnWarps * 32) {
+  for (int base = first; base < end; base += kDecWarps * 32) {
     if (base != first) {
       __syncwarp();
       stage_tile(base);
@@ -489,10 +501,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
     const int g = i / D, d = i % D;
     float M = -INFINITY;
-    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, wm[w][g]);
+    for (int w = 0; w < kDecWarps; ++w) M = fmaxf(M, wm[w][g]);
     float L = 0.0f, A = 0.0f;
     if (M != -INFINITY)
-      for (int w = 0; w < kAttnWarps; ++w) {
+      for (int w = 0; w < kDecWarps; ++w) {
         const float f = __expf(wm[w][g] - M);
         L += wl[w][g] * f;
         A += wacc[w][g][d] * f;
@@ -638,10 +650,10 @@ void launch_attention_decode(const float* qkv, const float2* rope, int T, const 
                              half* vc, const AttnShape& a, int nsplit, float* part_o,
                              float* part_ml, int* counters, float* o, cudaStream_t st) {
   const int G = a.n_heads / a.n_kv_heads;
-  const dim3 grid(T, a.n_kv_heads, nsplit), thr(kAttnWarps * 32);
+  const dim3 grid(T, a.n_kv_heads, nsplit), thr(kDecWarps * 32);
 #define MSW_DEC(DD, GG)                                                                       \
   if (a.head_dim == DD && G == GG) {                                                          \
-    const size_t smem = size_t(kAttnWarps) * 2 * 32 * (DD + kKvPad) * sizeof(half);           \
+    const size_t smem = size_t(kDecWarps) * 2 * 32 * (DD + kKvPad) * sizeof(half);            \
     static bool attr = false;                                                                 \
     if (!attr) {                                                                              \
       MSW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<DD, GG>,                               \

@@ -393,7 +393,10 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
   MSW_CUDA(cudaMemset(m.block_table, 0, sizeof(int) * size_t(m.bt_rows) * m.max_blocks));
   m.pool.init(m.nblk);
   m.ash = AttnShape{Hq, Hk, D, m.max_blocks};
-  m.nsplit = std::max(1, std::min(32, (2 * kNumSMs) / Hk));
+  // decode attention splits hold >= 256 positions (attention.cu kDecMinChunk):
+  // no more splits than max_seq_len needs, so short-context engines do not
+  // launch idle CTAs
+  m.nsplit = std::max(1, std::min({32, (2 * kNumSMs) / Hk, (cfg.max_seq_len + 255) / 256}));
 }
 
 void free_model(Model& m) {
