@@ -375,17 +375,29 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   };
   const int first = begin + warp * 32;
   if (first < end) stage_tile(first);  // cache history only: safe before the wait
+  // the RoPE row of this position is a cold table row: fetch it before the wait
+  // too (pos was written by the previous step's advance, long complete)
+  constexpr int kRopeIt = ((G + 1) * (D / 2) + kDecWarps * 32 - 1) / (kDecWarps * 32);
+  const float2* rp = rope + size_t(p_self) * (D / 2);
+  float2 rr[kRopeIt];
+#pragma unroll
+  for (int it = 0; it < kRopeIt; ++it) {
+    const int i = threadIdx.x + it * kDecWarps * 32;
+    if (i < (G + 1) * (D / 2)) rr[it] = rp[i % (D / 2)];
+  }
 
   pdl_wait();
   ATT_TP(1);
   pdl_trigger();
   {  // RoPE of this kv head's G query heads and the new key (table lookup)
     const float* row = qkv + size_t(t) * (Hq + 2 * Hk) * D;
-    const float2* rp = rope + size_t(p_self) * (D / 2);
-    for (int i = threadIdx.x; i < (G + 1) * (D / 2); i += blockDim.x) {
+#pragma unroll
+    for (int it = 0; it < kRopeIt; ++it) {
+      const int i = threadIdx.x + it * kDecWarps * 32;
+      if (i >= (G + 1) * (D / 2)) break;
       const int h = i / (D / 2), j = i % (D / 2);
       const float* src = h < G ? row + size_t(hk * G + h) * D : row + size_t(Hq + hk) * D;
-      const float2 r = rp[j];
+      const float2 r = rr[it];
       const float x0 = src[j], x1 = src[j + D / 2];
       const half y0 = __float2half_rn(__fsub_rn(__fmul_rn(x0, r.x), __fmul_rn(x1, r.y)));
       const half y1 = __float2half_rn(__fadd_rn(__fmul_rn(x1, r.x), __fmul_rn(x0, r.y)));
@@ -439,7 +451,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     for (int g = 0; g < G; ++g) s[g] = 0.0f;
     if (p < end) {
       const half* kr = sK + lane * RS;
-#pragma unroll 1
+#pragma unroll  // 8 warps x 256 threads: registers allow full ILP over D
       for (int c = 0; c < D / 8; ++c) {
         const uint4 kv = *reinterpret_cast<const uint4*>(kr + c * 8);
         const half2* kh = reinterpret_cast<const half2*>(&kv);
@@ -467,7 +479,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
     }
     const int n_here = min(32, end - base);
-#pragma unroll 1
+#pragma unroll 8
     for (int j = 0; j < n_here; ++j) {
       float vf[DPL];
       const half2* vh = reinterpret_cast<const half2*>(sV + j * RS + lane * DPL);
