@@ -406,8 +406,11 @@ def run_mix(args):
     from paper_2605_23057_b200.engine import Engine, execute_trace
     eng = Engine(engine_cfg(target="llama8b", draft="llama1b", seed=0, kv_blocks=1536, max_batch=64,
                             max_seq_len=9400, use_graphs=True), device=local)
-    lines = deploy_mix_trace(args.mix_per_class).splitlines()
-    mine = "\n".join(l for i, l in enumerate(lines) if i % ws == rank) + "\n"
+    from paper_2605_23057_b200.dispatch import aggregate_rows, shard_trace
+    text = deploy_mix_trace(args.mix_per_class)
+    lines = text.splitlines()
+    my_idx = shard_trace(text, ws)[rank]  # cohorts whole, prefix group sticky, least-loaded
+    mine = "".join(lines[i] + "\n" for i in my_idx)
     execute_trace(eng, "\n".join(lines[:2]) + "\n", max_output_tokens=4)  # warm-up (graphs, attrs)
     if ws > 1:
         torch.distributed.barrier()
@@ -417,11 +420,19 @@ def run_mix(args):
     wall = time.perf_counter() - t0
     vals = torch.tensor([summ["generated_tokens"], summ["mode_time_ms"], wall], dtype=torch.float64,
                         device="cuda")
+    mine_rows = {i: r for i, r in zip(my_idx, rows)}
+    gathered = [mine_rows]
     if ws > 1:
         toks = vals[0].clone()
         torch.distributed.all_reduce(toks)
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
         vals[0] = toks
+        gathered = [None] * ws
+        torch.distributed.all_gather_object(gathered, mine_rows)
+    all_rows = {}
+    for g in gathered:
+        all_rows.update(g)
+    agg = aggregate_rows(all_rows)  # the reference summarize over every request, trace order
     if rank == 0:
         from paper_2605_23057_b200.controller import MODES
         per_mode = {}
@@ -439,9 +450,11 @@ def run_mix(args):
             "metric": "decode tokens/s per mode and routed mix (1/2/4/8 B200); mean latency vs FP16 mode",
             "workload": "deploy_mix", "value": vals[0].item() / (vals[1].item() / 1000.0),
             "unit": "tokens/s (generated tokens / routed-mode request time, max over ranks)",
-            "n_gpus": ws, "requests": len(lines), "mean_speedup_vs_fp16": summ["mean_speedup"],
-            "aggregate_latency_speedup": summ["aggregate_latency_speedup"],
-            "collapsed_mean_speedup": summ["collapsed_mean_speedup"], "per_mode_rank0": per_mode,
+            "n_gpus": ws, "requests": len(lines), "mean_speedup_vs_fp16": agg["mean_speedup"],
+            "aggregate_latency_speedup": agg["aggregate_latency_speedup"],
+            "collapsed_mean_speedup": agg["collapsed_mean_speedup"],
+            "per_family_mean_speedup": agg["per_family_mean_speedup"], "per_mode_rank0": per_mode,
+            "placement": "CB cohorts whole per GPU, prefix group sticky, least outstanding tokens",
             "scaling": "weak", "data": "synthetic", "wall_s": vals[2].item()}), flush=True)
     eng.close()
     if ws > 1:
