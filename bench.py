@@ -433,6 +433,9 @@ def run_mix(args):
     for g in gathered:
         all_rows.update(g)
     agg = aggregate_rows(all_rows)  # the reference summarize over every request, trace order
+    if rank == 0 and args.decisions_out:  # the reference's decisions CSV (report.cpp:49-61)
+        from paper_2605_23057_b200.engine import write_decisions_csv
+        write_decisions_csv(text, [all_rows[i] for i in sorted(all_rows)], args.decisions_out)
     if rank == 0:
         from paper_2605_23057_b200.controller import MODES
         per_mode = {}
@@ -551,6 +554,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", choices=["decode8b", "mix", "configs", "profile"], default="decode8b")
     ap.add_argument("--profile-out", default="profiles/b200_profile.json")
+    ap.add_argument("--decisions-out", default="", help="mix: write the reference-format decisions CSV")
     ap.add_argument("--profile-out-cap", type=int, default=0, help="cap generated tokens per request")
     ap.add_argument("--cfg-requests", type=int, default=8)
     ap.add_argument("--mix-per-class", type=int, default=4)

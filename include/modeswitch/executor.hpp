@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cstdint>
+#include <filesystem>
 #include <string>
 #include <vector>
 
@@ -98,5 +99,12 @@ ExecRequestResult execute_request(msw_engine* engine, const RequestDescriptor& r
 // INT8PlusContinuousBatching, up to cohort_max), and summarises.
 ExecRunResult run_policy(const std::vector<RequestDescriptor>& trace, const RoutingPolicy& policy,
                          msw_engine* engine, const ExecOptions& options);
+
+// The reference's decisions CSV (report.cpp:49-61): header
+// "request_id,mode,reason,overhead_ms", one row per request in trace order,
+// overhead as %.17g, so its read_decisions_csv (report.cpp:63-81) and any diff
+// against its own routing output work on executed B200 runs.
+void write_decisions_csv(const std::vector<ExecRequestResult>& results,
+                         const std::filesystem::path& path);
 
 }  // namespace modeswitch

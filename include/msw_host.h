@@ -138,6 +138,11 @@ int msw_execute_trace(struct msw_engine* engine, int32_t vocab, const char* ndjs
                       const msw_classifier_cfg* cfg, const msw_exec_opts* opts, int32_t n_max,
                       msw_exec_row* rows, int32_t* n_out, msw_exec_summary* summary);
 
+/* The reference's decisions CSV (report.cpp:49-61) for executed rows: request
+ * ids from `ndjson` (trace order), mode / reason / overhead_ms from rows[0..n). */
+int msw_write_decisions_csv(const char* ndjson, const msw_exec_row* rows, int32_t n,
+                            const char* path);
+
 /* Energy (include/modeswitch/energy.hpp; reference sim.hpp:14-31, sim.cpp:10-78).
  * msw_power_start: NVML power polling of `device` every period_ms in a host
  * thread. msw_power_stop: stops, optionally writes the trace as the reference's

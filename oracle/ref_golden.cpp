@@ -21,6 +21,7 @@
 #include "modeswitch/classifier.hpp"
 #include "modeswitch/routing.hpp"
 #include "modeswitch/profile.hpp"
+#include "modeswitch/report.hpp"
 #include "modeswitch/sim.hpp"
 #include "modeswitch/trace_io.hpp"
 #include "modeswitch/workload.hpp"
@@ -44,6 +45,18 @@ static void emit(const std::string& dir, const std::string& name,
 }
 
 int main(int argc, char** argv) {
+  if (argc == 3 && std::string(argv[1]) == "--check-decisions") {
+    // the reference's own read_decisions_csv (report.cpp:63-81) on a CSV written by this repo
+    try {
+      for (const auto& r : ms::read_decisions_csv(argv[2]))
+        std::printf("%s,%s,%s\n", r.request_id.c_str(), std::string(ms::to_string(r.mode)).c_str(),
+                    std::string(ms::to_string(r.reason)).c_str());
+      return 0;
+    } catch (const std::exception& e) {
+      std::printf("error %s\n", e.what());
+      return 3;
+    }
+  }
   if (argc == 3 && std::string(argv[1]) == "--check-profile") {
     // the reference's own loader + validate() on a profile written by this repo
     try {

@@ -162,6 +162,7 @@ def host_lib() -> C.CDLL:
         lib.msw_execute_trace.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.POINTER(ClassifierCfg),
                                           C.POINTER(ExecOpts), C.c_int32, C.POINTER(ExecRow),
                                           C.POINTER(C.c_int32), C.POINTER(ExecSummary)]
+        lib.msw_write_decisions_csv.argtypes = [C.c_char_p, C.POINTER(ExecRow), C.c_int32, C.c_char_p]
         lib.msw_power_start.argtypes = [C.c_int32, C.c_double, C.POINTER(C.c_void_p)]
         lib.msw_power_stop.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.POINTER(C.c_double),
                                        C.POINTER(C.c_int32)]

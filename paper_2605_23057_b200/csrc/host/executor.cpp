@@ -3,6 +3,8 @@
 // engine through its C ABI. See include/modeswitch/executor.hpp.
 #include "modeswitch/executor.hpp"
 
+#include <cstdio>
+#include <fstream>
 #include <map>
 
 #include "msw_engine.h"
@@ -239,6 +241,19 @@ ExecRunResult run_policy(const std::vector<RequestDescriptor>& trace, const Rout
   }
   rep.collapsed_mean_speedup /= static_cast<double>(rep.per_family.size());
   return run;
+}
+
+void write_decisions_csv(const std::vector<ExecRequestResult>& results,
+                         const std::filesystem::path& path) {
+  std::ofstream out(path);
+  if (!out) throw DataError("cannot write decisions file: " + path.string());
+  out << "request_id,mode,reason,overhead_ms\n";
+  char buf[64];
+  for (const auto& r : results) {
+    std::snprintf(buf, sizeof(buf), "%.17g", r.decision.overhead_ms);
+    out << r.request_id << ',' << to_string(r.decision.mode) << ',' << to_string(r.decision.reason)
+        << ',' << buf << '\n';
+  }
 }
 
 }  // namespace modeswitch

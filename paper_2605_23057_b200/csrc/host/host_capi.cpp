@@ -256,6 +256,29 @@ int msw_execute_trace(struct msw_engine* engine, int32_t vocab, const char* ndjs
   });
 }
 
+int msw_write_decisions_csv(const char* ndjson, const msw_exec_row* rows, int32_t n,
+                            const char* path) {
+  return guarded([&] {
+    if (!ndjson || !rows || !path) throw ms::ConfigError("msw_write_decisions_csv: NULL argument");
+    std::istringstream in(ndjson);
+    std::string line;
+    std::vector<ms::ExecRequestResult> res;
+    while (std::getline(in, line) && int32_t(res.size()) < n) {
+      if (line.empty()) continue;
+      const ms::RequestDescriptor d = ms::parse_trace_line(line);
+      ms::ExecRequestResult r;
+      const msw_exec_row& w = rows[res.size()];
+      r.request_id = d.request_id;
+      r.decision.mode = static_cast<ms::InferenceMode>(w.mode);
+      r.decision.reason = static_cast<ms::RoutingReason>(w.reason);
+      r.decision.overhead_ms = w.overhead_ms;
+      res.push_back(std::move(r));
+    }
+    if (int32_t(res.size()) != n) throw ms::DataError("msw_write_decisions_csv: fewer trace lines than rows");
+    ms::write_decisions_csv(res, path);
+  });
+}
+
 struct msw_power_sampler {
   ms::PowerSampler impl;
   msw_power_sampler(int d, double p) : impl(d, p) {}

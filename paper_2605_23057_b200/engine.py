@@ -141,3 +141,14 @@ def execute_trace(engine: Engine, ndjson: str, *, token_seed: int = 0, prefix_le
                                             C.byref(opts), n_max, rows, C.byref(n), C.byref(summ)))
     out = [{f: getattr(rows[i], f) for f, _ in ExecRow._fields_} for i in range(n.value)]
     return out, {f: getattr(summ, f) for f, _ in ExecSummary._fields_}
+
+
+def write_decisions_csv(ndjson: str, rows: list[dict], path: str) -> None:
+    """The reference's decisions CSV (report.cpp:49-61) for rows returned by
+    execute_trace (trace order): request_id,mode,reason,overhead_ms."""
+    from ._capi import ExecRow, check_host, host_lib
+    arr = (ExecRow * max(1, len(rows)))()
+    for i, r in enumerate(rows):
+        for f, _ in ExecRow._fields_:
+            setattr(arr[i], f, r[f])
+    check_host(host_lib().msw_write_decisions_csv(ndjson.encode(), arr, len(rows), path.encode()))
