@@ -389,8 +389,7 @@ __device__ __noinline__ RingState mk_consume(const Slice sl, int groups_k, const
       pw[g] = FMT == kINT8 ? __int_as_float(int(acc[0])) : float(acc[0]);
       pw[g + 8] = FMT == kINT8 ? __int_as_float(int(acc[2])) : float(acc[2]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sh.tile_full[b]);
+    mbar_arrive(&sh.tile_full[b]);  // per-lane release of its own stores
     acc[0] = acc[1] = acc[2] = acc[3] = 0;
     ++tile_ctr;
     ++ti;
@@ -762,7 +761,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mk_kernel(const __grid_c
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sh.sc_full[b], 1);
       mbar_init(&sh.sc_empty[b], 1);
-      mbar_init(&sh.tile_full[b], kMkCons);
+      mbar_init(&sh.tile_full[b], kMkCons * 32);
       mbar_init(&sh.tile_free[b], 1);
       mbar_init(&sh.kv_full[b], 1);
       sh.kv_par[b] = 0;

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&sbar, 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&tile_full[b], ACTIVE);
+      mbar_init(&tile_full[b], ACTIVE * 32);  // every consumer lane publishes its own partial
       mbar_init(&tile_free[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -482,8 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         pw[g * 8 + 2 * tq + 1] = r4[1];
         pw[(g + 8) * 8 + 2 * tq] = r4[2];
         pw[(g + 8) * 8 + 2 * tq + 1] = r4[3];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tile_full[b]);
+        // each lane's arrive releases its OWN partial stores: a lane-0 arrive after
+        // __syncwarp() let the epilogue read other lanes' stale partials
+        // (~5-30% of 6-token K=14336 runs, scripts/repro_gemv_t6.py)
+        mbar_arrive(&tile_full[b]);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i] = acc2[i] = 0;
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&sbar, 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&tile_full[b], kConsumers);
+      mbar_init(&tile_full[b], kConsumers * 32);  // every consumer lane arrives
       mbar_init(&tile_free[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -659,8 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* pw = &part[b][warp][0][0];
     *reinterpret_cast<float2*>(pw + g * 8 + 2 * tq) = make_float2(acc[0], acc[1]);
     *reinterpret_cast<float2*>(pw + (g + 8) * 8 + 2 * tq) = make_float2(acc[2], acc[3]);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&tile_full[b]);
+    mbar_arrive(&tile_full[b]);  // per-lane release of its own stores (see gemv_tf_kernel)
     acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
   };
 #pragma unroll 1
@@ -919,7 +920,18 @@ void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, cons
   if (T < 1 || T > kGemvMaxTokens) throw ConfigErr("gemv: 1..6 tokens");
   if (!W.w_tf) throw ConfigErr("gemv: decode (tile-fragment) weight layout missing");
   switch (W.fmt) {
-    case kFP16: return dispatch_fmt<kFP16>(W, pro, epi, x, T, gamma, eps, y, st);
+    case kFP16:
+      if (T > 4 && size_t(kGemvMaxTokens) * 2 * W.k > 120 * 1024) {
+        // FP16, 5-6 tokens, large K: the 6-column activation stage leaves a
+        // 2-stage ring, and the 6-real-token case returned stale rows in ~5-45%
+        // of runs (scripts/repro_gemv_t6.py; root cause open).
+        // Run it as 4 + (T - 4) tokens (both clean over 100+ runs).
+        const size_t yrow = epi == kEpiSwiglu ? size_t(W.n / 2) : size_t(W.n);
+        dispatch_fmt<kFP16>(W, pro, epi, x, 4, gamma, eps, y, st);
+        return dispatch_fmt<kFP16>(W, pro, epi, x + size_t(4) * W.k, T - 4, gamma, eps,
+                                   y + 4 * yrow, st);
+      }
+      return dispatch_fmt<kFP16>(W, pro, epi, x, T, gamma, eps, y, st);
     case kINT8: return dispatch_fmt<kINT8>(W, pro, epi, x, T, gamma, eps, y, st);
     case kW4:
       if (T > 1 && size_t(kGemvMaxTokens) * 4 * W.k > 120 * 1024) {
