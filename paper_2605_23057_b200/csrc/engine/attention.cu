@@ -8,6 +8,7 @@
 // KV layout per layer: [block][kv_head][16 tokens][head_dim] fp16, so one
 // (block, kv head) is a contiguous 16*D*2-byte run (4 KB at D=128).
 #include "kernels.cuh"
+#include "mma_frag.cuh"
 
 namespace msw {
 #ifdef MSW_TRACE
@@ -296,6 +297,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 // the 4-warp / 64-position version spent 6.5 of its 17.8 us per layer in the
 // fence + atomic + last-CTA split merge; scripts/attn_timeline.py.)
 constexpr int kDecWarps = 8;
+#ifndef MSW_ATTN_MMA
+#define MSW_ATTN_MMA 1  // decode attention tile on mma.sync (0: scalar FMA loops)
+#endif
 constexpr int kDecMinChunk = 256;
 __device__ __forceinline__ int split_chunk_dec(int ctx, int nsplit) {
   const int c = (ctx + nsplit - 1) / nsplit;
@@ -422,6 +426,115 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     }
   }
   const float scale = rsqrtf(float(D));
+#if MSW_ATTN_MMA
+  // Tensor-pipe tile (mma.sync m16n8k16, fp32 accumulate): rows = the G query
+  // heads (16-row A tile, rows >= G zero), QK over 4 n-tiles of 8 positions,
+  // P (fp16, FA2 register reuse) x V with V fragments from ldmatrix.trans.
+  constexpr int KS = D / 16, DT = D / 8;
+  const int g = lane >> 2, tq = lane & 3;
+  uint32_t qa[KS][2];
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const int k0 = kk * 16 + 2 * tq;
+    qa[kk][0] = g < G ? h22u(__floats2half2_rn(qs[g < G ? g : 0][k0], qs[g < G ? g : 0][k0 + 1])) : 0u;
+    qa[kk][1] = g < G ? h22u(__floats2half2_rn(qs[g < G ? g : 0][k0 + 8], qs[g < G ? g : 0][k0 + 9])) : 0u;
+  }
+  float mrow = -INFINITY, lrow = 0.0f;
+  float acc[DT][4];
+#pragma unroll
+  for (int dt = 0; dt < DT; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.0f;
+#pragma unroll 1
+  for (int base = first; base < end; base += kDecWarps * 32) {
+    if (base != first) {
+      __syncwarp();
+      stage_tile(base);
+    }
+    cp_async_wait_all();
+    const int p = base + lane;
+    if (p == p_self) {  // the new token's row comes from smem, not the cache
+#pragma unroll 1
+      for (int c = 0; c < D / 8; ++c) {
+        *reinterpret_cast<uint4*>(sK + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(knew + c * 8);
+        *reinterpret_cast<uint4*>(sV + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(vnew + c * 8);
+      }
+    } else if (p >= end) {  // P = 0 there, but 0 x stale-NaN V would poison the MMA
+#pragma unroll 1
+      for (int c = 0; c < D / 8; ++c)
+        *reinterpret_cast<uint4*>(sV + lane * RS + c * 8) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncwarp();
+    float sc[4][2];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      float c4[4] = {0.f, 0.f, 0.f, 0.f};
+      const half* kr = sK + (nt * 8 + g) * RS + 2 * tq;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + kk * 16);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 8);
+        const uint32_t a4[4] = {qa[kk][0], 0u, qa[kk][1], 0u};
+        mma_f16(c4, a4, b0, b1);
+      }
+#pragma unroll
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const int pp = base + nt * 8 + 2 * tq + e2;
+        sc[nt][e2] = pp < end ? c4[e2] * scale : -INFINITY;
+      }
+    }
+    float mt = fmaxf(fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1])),
+                     fmaxf(fmaxf(sc[2][0], sc[2][1]), fmaxf(sc[3][0], sc[3][1])));
+    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
+    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+    const float mn = fmaxf(mrow, mt);
+    const float corr = __expf(mrow - mn);
+    float ls = 0.0f;
+    uint32_t pa[2][2];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const float e0 = sc[nt][0] == -INFINITY ? 0.0f : __expf(sc[nt][0] - mn);
+      const float e1 = sc[nt][1] == -INFINITY ? 0.0f : __expf(sc[nt][1] - mn);
+      ls += e0 + e1;
+      pa[nt >> 1][nt & 1] = h22u(__floats2half2_rn(e0, e1));
+    }
+    ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+    ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+    lrow = lrow * corr + ls;
+    mrow = mn;
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+      acc[dt][0] *= corr;
+      acc[dt][1] *= corr;
+    }
+    const int n_here = min(32, end - base);
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      if (ks * 16 >= n_here) break;  // warp-uniform
+      const uint32_t a4[4] = {g < G ? pa[ks][0] : 0u, 0u, g < G ? pa[ks][1] : 0u, 0u};
+      const half* vrow = sV + (ks * 16 + (lane & 15)) * RS;
+#pragma unroll
+      for (int dt = 0; dt < DT; ++dt) {
+        uint32_t b0, b1;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                     : "=r"(b0), "=r"(b1)
+                     : "r"(smem_u32(vrow + dt * 8)));
+        mma_f16(acc[dt], a4, b0, b1);
+      }
+    }
+  }
+  // per-warp (m, l, acc) -> shared, rows g < G held by the tq lanes
+  if (g < G) {
+    if (tq == 0) {
+      wm[warp][g < G ? g : 0] = mrow;
+      wl[warp][g < G ? g : 0] = lrow;
+    }
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+      wacc[warp][g < G ? g : 0][dt * 8 + 2 * tq] = acc[dt][0];
+      wacc[warp][g < G ? g : 0][dt * 8 + 2 * tq + 1] = acc[dt][1];
+    }
+  }
+#else
+  const float scale = rsqrtf(float(D));
   float m[G], l[G], acc[G][DPL];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -497,7 +610,6 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       }
     }
   }
-  ATT_TP(3);
   // merge the warps of this CTA
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -508,6 +620,8 @@ __global__ void __launch_bounds__(kDecWarps * 32)
 #pragma unroll
     for (int d = 0; d < DPL; ++d) wacc[warp][g][lane * DPL + d] = acc[g][d];
   }
+#endif
+  ATT_TP(3);
   __syncthreads();
 #pragma unroll 1
   for (int i = threadIdx.x; i < G * D; i += blockDim.x) {

@@ -1,4 +1,4 @@
-for t in 6 5; do timeout -s KILL 300 python scripts/repro_gemv_t6.py 4096 200 $t > gpurun_out/repro_$t.txt 2>&1; done
-timeout -s KILL 300 python scripts/repro_gemv_t6.py 256 300 6 >> gpurun_out/repro_6.txt 2>&1
 timeout -s KILL 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "EXIT $?" >> gpurun_out/gpu_tests.log
-timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "EXIT $?" >> gpurun_out/smoke.log
+for m in 2 1 0; do timeout -s KILL 200 python scripts/decode_once.py --mode $m --new 129 --reps 2 > gpurun_out/dec_m$m.txt 2>&1; done
+timeout -s KILL 200 python scripts/decode_once.py --mode 2 --prompt 900 --new 129 --reps 1 > gpurun_out/dec_m2_long.txt 2>&1
+timeout -s KILL 300 python scripts/attn_timeline.py 2 200 > gpurun_out/attn_tl.txt 2>&1
