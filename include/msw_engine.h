@@ -41,6 +41,8 @@ enum {
   MSW_MODE_INT8 = 1,
   MSW_MODE_GPTQ4 = 2,
   MSW_MODE_SPECULATIVE = 4,
+  MSW_MODE_CHUNKED_PREFILL = 6, /* FP16, prefill in 512-token chunks (screening mode) */
+  MSW_MODE_CUDA_GRAPHS = 8,     /* FP16, graph-replayed decode (screening mode) */
   MSW_MODE_GPTQ_PREFIX_CACHING = 10,
   MSW_MODE_INT8_CONT_BATCHING = 11
 };

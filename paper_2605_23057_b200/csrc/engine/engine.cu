@@ -27,12 +27,15 @@ namespace {
 thread_local std::string g_last_error;
 
 constexpr int kPrefillChunk = 2048;
+constexpr int kChunkedPrefillTokens = 512;  // ChunkedPrefill screening mode
 constexpr int kMaxLogitRows = 64;
 
 int fmt_of_mode(int mode) {
   switch (mode) {
     case MSW_MODE_FP16:
     case MSW_MODE_SPECULATIVE:
+    case MSW_MODE_CHUNKED_PREFILL:
+    case MSW_MODE_CUDA_GRAPHS:
       return kFP16;
     case MSW_MODE_INT8:
     case MSW_MODE_INT8_CONT_BATCHING:
@@ -314,7 +317,8 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
   if (is_draft) {
     m.fmt_on[kFP16] = true;
   } else {
-    m.fmt_on[kFP16] = mm & ((1u << MSW_MODE_FP16) | (1u << MSW_MODE_SPECULATIVE));
+    m.fmt_on[kFP16] = mm & ((1u << MSW_MODE_FP16) | (1u << MSW_MODE_SPECULATIVE) |
+                            (1u << MSW_MODE_CHUNKED_PREFILL) | (1u << MSW_MODE_CUDA_GRAPHS));
     m.fmt_on[kINT8] = mm & ((1u << MSW_MODE_INT8) | (1u << MSW_MODE_INT8_CONT_BATCHING));
     m.fmt_on[kW4] = mm & ((1u << MSW_MODE_GPTQ4) | (1u << MSW_MODE_GPTQ_PREFIX_CACHING));
   }
@@ -616,10 +620,10 @@ void release_sequence(Model& m, const SeqBlocks& sb) {
 // Prefill tokens [from, plen) of one sequence (block-table row `row`), in
 // chunks; the last chunk yields logits/argmax for the last prompt token.
 void prefill(msw_engine* e, Model& m, int fmt, int row, const int32_t* prompt, int from, int plen,
-             const SeqBlocks& sb) {
+             const SeqBlocks& sb, int chunk = kPrefillChunk) {
   Scratch& s = e->sc;
-  for (int c0 = from; c0 < plen; c0 += kPrefillChunk) {
-    const int T = std::min(kPrefillChunk, plen - c0);
+  for (int c0 = from; c0 < plen; c0 += chunk) {
+    const int T = std::min(chunk, plen - c0);
     int* st_tok = s.stage;
     int* st_pos = s.stage + T;
     int* st_slot = s.stage + 2 * T;
@@ -877,10 +881,13 @@ void run_single(msw_engine* e, const msw_request& r, msw_result& res) {
   SeqBlocks sb = map_sequence(m, 0, r.prompt_len + n_new, r.prompt_ids, r.prompt_len, prefix, fmt,
                               e->st, e->sc.stage);
   const bool want_logits = res.logits != nullptr;
-  const bool graphs = e->cfg.use_graphs && !want_logits;
+  // CudaGraphs screening mode: graph-replayed decode even when the engine was
+  // configured eager (cfg.use_graphs = 0); ChunkedPrefill: 512-token prefill chunks
+  const bool graphs = (e->cfg.use_graphs || r.mode == MSW_MODE_CUDA_GRAPHS) && !want_logits;
   try {
     MSW_CUDA(cudaEventRecord(e->ev[0], e->st));
-    prefill(e, m, fmt, 0, r.prompt_ids, sb.hit_tokens, r.prompt_len, sb);
+    prefill(e, m, fmt, 0, r.prompt_ids, sb.hit_tokens, r.prompt_len, sb,
+            r.mode == MSW_MODE_CHUNKED_PREFILL ? kChunkedPrefillTokens : kPrefillChunk);
     if (want_logits) copy_logits_row(e, res.logits, 0);
     start_decode(e, m, e->sc.next, r.prompt_len - 1, 0);
     MSW_CUDA(cudaEventRecord(e->ev[1], e->st));

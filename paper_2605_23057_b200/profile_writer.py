@@ -24,8 +24,8 @@ import json
 
 import numpy as np
 
-from .configs import (MODE_FP16, MODE_GPTQ4, MODE_GPTQ_PC, MODE_INT8, MODE_INT8_CB, MODE_NAMES,
-                      MODE_SPEC)
+from .configs import (MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_FP16, MODE_GPTQ4, MODE_GPTQ_PC,
+                      MODE_INT8, MODE_INT8_CB, MODE_NAMES, MODE_SPEC)
 from .controller import FAMILIES
 
 # family_nominal_shape (workload.cpp:9-23): prompt, output, shared_prefix, memory_pressure
@@ -34,7 +34,8 @@ NOMINAL = {
     "SyntheticLL": (1024, 128), "SharedPrefixChat": (1024, 128),
     "MemoryPressureLongContext": (2048, 64), "MMLUPro": (400, 16), "GSM8K": (250, 256),
     "TruthfulQA": (200, 64), "GPQA": (500, 16), "MLU": (300, 16)}
-PROFILE_MODES = (MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_SPEC, MODE_GPTQ_PC, MODE_INT8_CB)
+PROFILE_MODES = (MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_SPEC, MODE_GPTQ_PC, MODE_INT8_CB,
+                 MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS)
 CB_COHORT = 4  # co-scheduled requests for the continuous-batching cells (batch_pressure 4)
 PREFIX_LEN = 768  # shared tokens of SharedPrefixChat requests
 

@@ -15,16 +15,18 @@ import numpy as np
 import pytest
 
 import oracle as O
-from paper_2605_23057_b200 import (MODE_FP16, MODE_GPTQ4, MODE_GPTQ_PC, MODE_INT8, MODE_INT8_CB,
-                                   MODE_SPEC, engine_cfg, model_cfg)
+from paper_2605_23057_b200 import (MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_FP16, MODE_GPTQ4,
+                                   MODE_GPTQ_PC, MODE_INT8, MODE_INT8_CB, MODE_SPEC, engine_cfg,
+                                   model_cfg)
 from paper_2605_23057_b200._capi import MswError
 from paper_2605_23057_b200.engine import Engine
 
 pytestmark = pytest.mark.gpu
 
 TOL = {MODE_FP16: 2e-3, MODE_INT8: 1e-2, MODE_GPTQ4: 1e-2, MODE_GPTQ_PC: 1e-2, MODE_INT8_CB: 1e-2,
-       MODE_SPEC: 2e-3}
-ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_GPTQ_PC: 2, MODE_INT8_CB: 1}
+       MODE_SPEC: 2e-3, MODE_CHUNKED_PREFILL: 2e-3, MODE_CUDA_GRAPHS: 2e-3}
+ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_GPTQ_PC: 2, MODE_INT8_CB: 1,
+               MODE_CHUNKED_PREFILL: 0, MODE_CUDA_GRAPHS: 0}
 
 
 def prompt(seed, n, vocab):
@@ -47,7 +49,8 @@ def _check_logits(gpu, ref, tol):
     assert err.max() < tol, f"logit error {err.max():.3g} >= {tol}"
 
 
-@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4])
+@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_CHUNKED_PREFILL,
+                                  MODE_CUDA_GRAPHS])
 @pytest.mark.parametrize("plen,n_new", [(1, 4), (37, 24), (130, 9)])
 def test_batch1_modes_match_oracle(pair, mode, plen, n_new):
     _, eng, orc, _ = pair
@@ -171,3 +174,34 @@ def test_continuous_batching_more_requests_than_rows(long_pair):
     for i, r in enumerate(res):
         toks, _ = orc.generate(1, prompts[i], nnew[i])
         assert np.array_equal(r.tokens, toks), i
+
+
+def test_chunked_prefill_mode_512_token_chunks(long_pair):
+    # ChunkedPrefill screening mode: a 1300-token prompt prefilled as 512+512+276,
+    # each chunk attending to the earlier chunks' paged K/V
+    eng, orc = long_pair
+    p = prompt(4242, 1300, eng.vocab)
+    r = eng.run(MODE_CHUNKED_PREFILL, p, 8, want_logits=True)
+    toks, lg = orc.generate(0, p, 8, want_logits=True)
+    assert np.array_equal(r.tokens, toks)
+    _check_logits(r.logits, lg, TOL[MODE_CHUNKED_PREFILL])
+    assert np.array_equal(eng.run(MODE_FP16, p, 8).tokens, toks)
+
+
+def test_cuda_graphs_mode_on_eager_engine(cuda_ok):
+    # engine configured eager: FP16 decodes with per-kernel launches, the
+    # CudaGraphs screening mode replays the captured decode graph; same tokens
+    cfg = engine_cfg(target="tiny", draft=None, modes=(MODE_FP16, MODE_CUDA_GRAPHS), seed=5,
+                     kv_blocks=256, max_seq_len=512, use_graphs=False)
+    eng = Engine(cfg)
+    try:
+        orc = O.OracleModel(model_cfg("tiny"), seed=5, max_ctx=512)
+        p = prompt(31337, 40, eng.vocab)
+        toks, _ = orc.generate(0, p, 30)
+        rg = eng.run(MODE_CUDA_GRAPHS, p, 30)
+        re_ = eng.run(MODE_FP16, p, 30)
+        assert np.array_equal(rg.tokens, toks)
+        assert np.array_equal(re_.tokens, toks)
+        assert not eng.has_mode(MODE_INT8)
+    finally:
+        eng.close()

@@ -8,7 +8,8 @@ import subprocess
 
 import pytest
 
-from paper_2605_23057_b200.configs import MODE_FP16, MODE_GPTQ4, MODE_INT8, MODE_INT8_CB, MODE_SPEC
+from paper_2605_23057_b200.configs import (MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_FP16,
+                                           MODE_GPTQ4, MODE_INT8, MODE_INT8_CB, MODE_SPEC)
 from paper_2605_23057_b200.profile_writer import NOMINAL, build_profile, fit_baseline, write_profile
 
 REF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
@@ -20,7 +21,7 @@ def _fake_measurements():
     for i, (fam, (p, o)) in enumerate(NOMINAL.items()):
         base = 20.0 + 0.4 * p + 11.5 * o  # the reference's default FP16 cost model (profile.cpp:281-291)
         for mode, sp in ((MODE_FP16, 1.0), (MODE_INT8, 1.3), (MODE_GPTQ4, 1.5), (MODE_SPEC, 1.2),
-                         (MODE_INT8_CB, 0.9)):
+                         (MODE_INT8_CB, 0.9), (MODE_CHUNKED_PREFILL, 0.98), (MODE_CUDA_GRAPHS, 1.02)):
             meas[(mode, fam)] = {"latency_ms": base / sp, "tokens": o, "prompt": p,
                                  "energy_j_per_token": 3.0 / sp, "mem_bytes": 16e9 / sp}
     return meas
@@ -35,7 +36,8 @@ def test_fit_recovers_linear_cost_model():
 def test_profile_schema_and_ratios():
     prof = build_profile(_fake_measurements(), 3.0, 16384.0)
     assert set(prof) == {"baseline_costs", "cells"}
-    assert len(prof["cells"]) == 5 * len(NOMINAL)
+    assert len(prof["cells"]) == 7 * len(NOMINAL)
+    assert {c["mode"] for c in prof["cells"]} >= {"chunked_prefill", "cuda_graphs"}
     fp16 = [c for c in prof["cells"] if c["mode"] == "fp16"]
     assert all(c["latency_speedup"] == 1.0 and c["energy_ratio"] == 1.0 for c in fp16)
     g4 = next(c for c in prof["cells"] if c["mode"] == "gptq4" and c["family"] == "GSM8K")
