@@ -488,6 +488,12 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
   if (T <= kMaxLogitRows) nsplit = std::max(1, std::min(m.nsplit, (2 * kNumSMs) / (T * Hk)));
   long long& n = e->launches;
 
+  LinearW head;
+  head.fmt = kFP16;
+  head.n = c.vocab;
+  head.k = H;
+  head.w = m.lm_head;
+  head.w_tf = m.lm_head_tf;
   launch_embed(m.embed, s.tok, T, H, s.h, st);
   ++n;
   for (int l = 0; l < c.n_layers; ++l) {
@@ -496,7 +502,8 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
     half* vc = m.vc + m.kv_layer_elems * l;
     // attention block
     if (small) {
-      if (!diag_skip("qkv")) launch_gemv(ly.qkv[fmt], kProNorm, kEpiStore, s.h, T, ly.attn_norm, eps, s.qkv, st);
+      if (!diag_skip("qkv"))
+        launch_gemv(ly.qkv[fmt], kProNorm, kEpiStore, s.h, T, ly.attn_norm, eps, s.qkv, st, &ly.o[fmt]);
       ++n;
     } else {
       launch_prep_act(fmt, s.h, T, H, ly.attn_norm, eps, s.xh, s.xq, s.xscale, st);
@@ -519,9 +526,14 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       }
     }
     if (small) {
-      if (!diag_skip("o,") && !diag_skip("oonly")) launch_gemv(ly.o[fmt], kProPlain, kEpiResid, s.o, T, nullptr, eps, s.h, st);
-      if (!diag_skip("gu")) launch_gemv(ly.gu[fmt], kProNorm, kEpiSwiglu, s.h, T, ly.ffn_norm, eps, s.act, st);
-      if (!diag_skip("down")) launch_gemv(ly.down[fmt], kProPlain, kEpiResid, s.act, T, nullptr, eps, s.h, st);
+      // each GEMV prefetches the head of the next one's weight stream into L2
+      const LinearW* after_down = l + 1 < c.n_layers ? &m.layers[l + 1].qkv[fmt] : &head;
+      if (!diag_skip("o,") && !diag_skip("oonly"))
+        launch_gemv(ly.o[fmt], kProPlain, kEpiResid, s.o, T, nullptr, eps, s.h, st, &ly.gu[fmt]);
+      if (!diag_skip("gu"))
+        launch_gemv(ly.gu[fmt], kProNorm, kEpiSwiglu, s.h, T, ly.ffn_norm, eps, s.act, st, &ly.down[fmt]);
+      if (!diag_skip("down"))
+        launch_gemv(ly.down[fmt], kProPlain, kEpiResid, s.act, T, nullptr, eps, s.h, st, after_down);
       n += 3;
     } else {
       launch_prep_act(fmt, s.o, T, Hq * D, nullptr, eps, s.xh, s.xq, s.xscale, st);
@@ -541,12 +553,6 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
     hrows = s.hsel;
     ++n;
   }
-  LinearW head;
-  head.fmt = kFP16;
-  head.n = c.vocab;
-  head.k = H;
-  head.w = m.lm_head;
-  head.w_tf = m.lm_head_tf;
   if (n_logits <= kGemvMaxTokens) {
     if (!diag_skip("head")) launch_gemv(head, kProNorm, kEpiStore, hrows, n_logits, m.final_norm, eps, s.logits, st);
     ++n;

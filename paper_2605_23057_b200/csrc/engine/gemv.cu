@@ -35,6 +35,28 @@ constexpr int kConsumers = 16;
 constexpr int kThreads = (kConsumers + 2) * 32;  // + producer warp + epilogue warp
 constexpr int kConsThreads = kConsumers * 32;
 constexpr int kChunkBytes = 512;
+
+// The head of the NEXT decode linear's weight stream, per CTA: once a CTA's
+// producer has issued its last ring stage it prefetches into L2 the first
+// w_bytes of the slice CTA blockIdx.x of the next GEMV will stream (and that
+// CTA's scale block), so the next kernel's ring starts on L2 hits instead of
+// a cold HBM round trip. The bytes are the ones the next kernel reads anyway:
+// no extra HBM traffic, only earlier.
+struct L2Next {
+  const uint8_t* w = nullptr;
+  const uint8_t* s = nullptr;
+  uint32_t w_stride = 0, w_bytes = 0, w_total = 0;
+  uint32_t s_stride = 0, s_bytes = 0, s_total = 0;
+  int ncta = 0;
+};
+
+__device__ __forceinline__ void l2_next_prefetch(const L2Next& nx) {
+  if (int(blockIdx.x) >= nx.ncta) return;
+  const uint32_t wo = blockIdx.x * nx.w_stride;
+  if (nx.w_bytes && wo < nx.w_total) prefetch_l2(nx.w + wo, min(nx.w_bytes, nx.w_total - wo));
+  const uint32_t so = blockIdx.x * nx.s_stride;
+  if (nx.s_bytes && so < nx.s_total) prefetch_l2(nx.s + so, min(nx.s_bytes, nx.s_total - so));
+}
 constexpr int kMaxStages = 8;
 constexpr int kSmemBudget = 190 * 1024;
 
@@ -251,7 +273,7 @@ template <int FMT, int PRO, int EPI, int NT, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_tf_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
                    const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
-                   float* __restrict__ y, int n_stages) {
+                   float* __restrict__ y, int n_stages, const L2Next nx) {
   using Acc = typename std::conditional<FMT == kINT8, int, float>::type;
   constexpr int CK = TF<FMT>::kChunkK;
   constexpr int CPW = (S / kConsumers) > TF<FMT>::kMinChunksPerWarp ? (S / kConsumers)
@@ -320,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
+      l2_next_prefetch(nx);
     }
     pdl_wait();
     pdl_trigger();
@@ -515,7 +538,7 @@ template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_w4_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
                    const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
-                   float* __restrict__ y, int n_stages, uint32_t /*unused*/) {
+                   float* __restrict__ y, int n_stages, const L2Next nx) {
   constexpr int WPG = kConsumers / GW;  // warps sharing one stage
   constexpr int CPW = S / WPG;          // chunks per warp per stage
   static_assert(CPW == 4, "two 128-k groups per warp per stage");
@@ -578,6 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       MSW_TP(2);  // last stage issued
+      l2_next_prefetch(nx);
     }
     pdl_wait();
     pdl_trigger();
@@ -790,6 +814,45 @@ __global__ void repack_tf_kernel(int fmt, const uint8_t* __restrict__ src, int n
   }
 }
 
+// L2 prefetch descriptor of the linear launched after the current one; set by
+// launch_gemv for the duration of one launch (host-thread local, the launch
+// captures it by value, so graph capture records it too).
+thread_local L2Next t_next;
+
+// Enabled behind W4 GEMVs only (128 KB per CTA: W4 decode 1.620 -> 1.588
+// ms/token). FP16 and INT8 already run near the HBM rate, where the early
+// bytes compete with the current stream: FP16 2.668 -> 2.72 ms, INT8 flat at
+// 32 KB and worse above (scripts/l2next_ab.sh). MSW_L2NEXT_KB overrides.
+L2Next make_l2_next(int cur_fmt, const LinearW* nw) {
+  L2Next nx;
+  static const long env_kb = [] {
+    const char* v = std::getenv("MSW_L2NEXT_KB");
+    return v ? std::atol(v) : -1L;
+  }();
+  const long kb = env_kb >= 0 ? env_kb : (cur_fmt == kW4 ? 128L : 0L);
+  if (!nw || !nw->w_tf || kb <= 0) return nx;
+  const int ck = nw->fmt == kFP16 ? 16 : (nw->fmt == kINT8 ? 32 : 64);
+  const int ntiles = nw->n / 16;
+  const int grid = std::max(1, std::min(ntiles, kNumSMs));
+  const int per_cta = (ntiles + grid - 1) / grid;
+  const size_t tile_bytes = size_t(nw->k / ck) * kChunkBytes;
+  const size_t w_total = size_t(ntiles) * tile_bytes;
+  if (w_total >= (size_t(1) << 32)) return nx;  // 32-bit offsets
+  nx.w = static_cast<const uint8_t*>(nw->w_tf);
+  nx.w_stride = uint32_t(per_cta * tile_bytes);
+  nx.w_bytes = uint32_t(std::min<size_t>(size_t(kb) * 1024, per_cta * tile_bytes));
+  nx.w_total = uint32_t(w_total);
+  const size_t srow = nw->fmt == kW4 ? size_t(nw->k / kW4Group) * 2 : (nw->fmt == kINT8 ? 4 : 0);
+  if (srow && nw->s) {
+    nx.s = static_cast<const uint8_t*>(nw->s);
+    nx.s_stride = uint32_t(per_cta * 16 * srow);
+    nx.s_bytes = nx.s_stride;
+    nx.s_total = uint32_t(size_t(nw->n) * srow);
+  }
+  nx.ncta = grid;
+  return nx;
+}
+
 template <int FMT, int PRO, int EPI, int NT, int S>
 void launch_tf_s(const LinearW& W, const float* x, int T, const half* gamma, float eps, float* y,
                  cudaStream_t st) {
@@ -815,7 +878,8 @@ void launch_tf_s(const LinearW& W, const float* x, int T, const half* gamma, flo
     attr_done = true;
   }
   launch_pdl(gemv_tf_kernel<FMT, PRO, EPI, NT, S>, dim3(grid), dim3(kThreads), smem, st,
-             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages);
+             static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages,
+             t_next);
 }
 
 template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
@@ -841,7 +905,7 @@ void launch_w4(const LinearW& W, const float* x, int T, const half* gamma, float
   }
   launch_pdl(gemv_w4_kernel<PRO, EPI, NT, S, GW, XREG>, dim3(grid), dim3(kThreads), smem, st,
              static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages,
-             uint32_t(1u << 24));
+             t_next);
 }
 
 template <int FMT, int PRO, int EPI, int NT>
@@ -914,8 +978,23 @@ extern "C" int msw_trace_set(void* buf) {
 }
 #endif
 
+void launch_gemv_(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
+                  float eps, float* y, cudaStream_t st);
+
 void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
-                 float eps, float* y, cudaStream_t st) {
+                 float eps, float* y, cudaStream_t st, const LinearW* next) {
+  t_next = make_l2_next(W.fmt, next);
+  try {
+    launch_gemv_(W, pro, epi, x, T, gamma, eps, y, st);
+  } catch (...) {
+    t_next = L2Next();
+    throw;
+  }
+  t_next = L2Next();
+}
+
+void launch_gemv_(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
+                  float eps, float* y, cudaStream_t st) {
   if (W.n % 16 != 0 || W.k % 128 != 0) throw ConfigErr("gemv: n % 16, k % 128 required");
   if (T < 1 || T > kGemvMaxTokens) throw ConfigErr("gemv: 1..6 tokens");
   if (!W.w_tf) throw ConfigErr("gemv: decode (tile-fragment) weight layout missing");

@@ -48,7 +48,8 @@ enum Epilogue { kEpiStore = 0, kEpiResid = 1, kEpiSwiglu = 2 };
 // x is fp32 [T, k], 1 <= T <= kGemvMaxTokens; y rows are per token.
 constexpr int kGemvMaxTokens = 6;
 void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
-                 float eps, float* y, cudaStream_t st);
+                 float eps, float* y, cudaStream_t st,
+                 const LinearW* next = nullptr);
 void launch_gemv_i8_acc(const int8_t* w, const int8_t* x, int n, int k, int* acc, cudaStream_t st);
 // row-major weights (FP16 half / INT8 int8 / W4 row-packed words) -> the
 // tile-fragment layout the decode GEMV streams (same byte count)
