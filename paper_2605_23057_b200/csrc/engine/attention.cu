@@ -97,6 +97,16 @@ __device__ __forceinline__ int split_chunk(int ctx, int nsplit) {
 // fp32 qkv row; the split-0 CTA appends k/v to the paged cache, and every CTA
 // uses the fresh k/v from shared memory for the query's own position instead
 // of reading the cache (no cross-CTA ordering needed).
+constexpr int kKvPad = 8;  // halves of padding per staged K/V row (bank-conflict free LDS.128)
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 template <int D, int G, bool FUSED>
 __global__ void __launch_bounds__(kAttnWarps * 32)
     attention_kernel(const half* __restrict__ q, const float* __restrict__ qkv,
@@ -170,7 +180,24 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     for (int d = 0; d < DPL; ++d) acc[g][d] = 0.0f;
   }
 
+  // per-warp K tile in shared memory, staged with coalesced 16-byte pieces
+  // (2 rows per warp instruction for D = 128) instead of lane = position loads
+  constexpr int RS = D + kKvPad, CPR = D / 8, RPI = 32 / CPR;
+  extern __shared__ __align__(16) half ks_smem[];
+  half* sK = ks_smem + size_t(warp) * 32 * RS;
   for (int base = begin + warp * 32; base < end; base += kAttnWarps * 32) {
+    __syncwarp();  // the previous tile's rows are consumed
+#pragma unroll 4
+    for (int i = 0; i < 32 / RPI; ++i) {
+      const int r = i * RPI + lane / CPR;
+      const int pr = base + r;
+      if (pr < end && !(FUSED && pr == p_self)) {
+        const int sl = bt[pr >> 4] * kKvBlock + (pr & 15);
+        cp_async16(sK + r * RS + (lane % CPR) * 8, kc + kv_off(sl, hk, Hk, D) + (lane % CPR) * 8);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
     const int p = base + lane;
     float s[G];
     if (p < end) {
@@ -183,8 +210,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
           for (int g = 0; g < G; ++g) dot[g] = fmaf(qs[g][d], knew[d], dot[g]);
         }
       } else {
-        const int sl = bt[p >> 4] * kKvBlock + (p & 15);
-        const uint4* kr = reinterpret_cast<const uint4*>(kc + kv_off(sl, hk, Hk, D));
+        const uint4* kr = reinterpret_cast<const uint4*>(sK + lane * RS);
 #pragma unroll 4
         for (int c = 0; c < D / 8; ++c) {
           const uint4 kv = kr[c];
@@ -318,15 +344,6 @@ __device__ __forceinline__ int split_chunk_dec(int ctx, int nsplit) {
 //  * splits are merged in-kernel: every split writes (m, l, acc) partials and
 //    the last CTA to finish (atomic counter) combines them, so there is no
 //    separate combine launch.
-constexpr int kKvPad = 8;  // halves of padding per staged K/V row (bank-conflict free LDS.128)
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
 
 template <int D, int G>
 __global__ void __launch_bounds__(kDecWarps * 32)
@@ -716,11 +733,19 @@ void attn_d(int G, dim3 grid, const half* q, const float* qkv, const float* inv_
             half* vc, int Hq, int Hk, int nsplit, float* po, float* pml, float* o,
             cudaStream_t st) {
   const dim3 thr(kAttnWarps * 32);
+  const size_t smem = size_t(kAttnWarps) * 32 * (D + kKvPad) * sizeof(half);
 #define MSW_ATT(GG)                                                                              \
-  case GG:                                                                                       \
-    launch_pdl(attention_kernel<D, GG, FUSED>, grid, thr, 0, st, q, qkv, inv_freq, pos, slot,   \
+  case GG: {                                                                                     \
+    static bool attr = false;                                                                    \
+    if (!attr) {                                                                                 \
+      MSW_CUDA(cudaFuncSetAttribute(attention_kernel<D, GG, FUSED>,                              \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));    \
+      attr = true;                                                                               \
+    }                                                                                            \
+    launch_pdl(attention_kernel<D, GG, FUSED>, grid, thr, smem, st, q, qkv, inv_freq, pos, slot, \
                seq_of, bt, maxb, kc, vc, Hq, Hk, nsplit, po, pml, o);                            \
-    break;
+    break;                                                                                       \
+  }
   switch (G) {
     MSW_ATT(1)
     MSW_ATT(2)
