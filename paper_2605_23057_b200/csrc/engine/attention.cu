@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       acc[dt][1] *= corr;
     }
     const int n_here = min(32, end - base);
+    if (base == first && active == 1) ATT_TP(5);  // warp 0: QK + softmax done (single split)
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       if (ks * 16 >= n_here) break;  // warp-uniform

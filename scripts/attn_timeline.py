@@ -33,7 +33,7 @@ t = t[live]
 t0 = t[:, 0].min()
 print(f"ctx {prompt + 2}: {live.sum()} CTAs recorded")
 for e, nm in enumerate(["entry", "past pdl wait", "rope done", "positions done", "partial written",
-                        "merge done", "tile 0 staged", "idle exit"]):
+                        "merge|QK done", "tile 0 staged", "idle exit"]):
     col = t[:, e]
     col = col[col > 0]
     if len(col):
