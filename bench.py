@@ -277,10 +277,12 @@ def run_ours(args):
         out = {}
         for m, name in MODES:
             if measure_energy:
-                try:  # whole-GPU power over the request, reference trapezoid rule
+                try:  # whole-GPU energy over this request: the driver's energy counter
+                    # (instantaneous-power trapezoid where the counter is missing)
                     with PowerSampler(local, period_ms=5.0) as ps:
                         out[name] = eng.run(m, p, NEW)
-                        energy[name].append(ps.finish(NEW))
+                        jpt = ps.finish(NEW)
+                        energy[name].append(ps.counter_joules_per_token or jpt)
                     continue
                 except Exception:
                     pass

@@ -32,18 +32,26 @@ void write_power_trace(const PowerTrace& trace, const std::filesystem::path& pat
 // consecutive samples, divided by tokens (reference sim.cpp:57-78).
 double energy_from_power_trace(const PowerTrace& trace, int tokens);
 
-// Polls nvmlDeviceGetPowerUsage(device) every period_ms into a PowerTrace
-// (timestamps: steady clock, ms since start()). Throws ConfigError when NVML
-// is unavailable.
+// Samples the instantaneous board power of CUDA device `device` (NVML device
+// resolved by PCI bus id; NVML_FI_DEV_POWER_INSTANT, falling back to
+// nvmlDeviceGetPowerUsage) every period_ms into a PowerTrace (timestamps:
+// steady clock, ms since start()), and reads the driver's total-energy
+// counter at start() and stop(). Throws ConfigError when NVML is unavailable.
 class PowerSampler {
  public:
   explicit PowerSampler(int device, double period_ms = 10.0);
   ~PowerSampler();
   void start();
   PowerTrace stop();  // always appends one final sample so short windows integrate
+  // Joules between start() and stop() from nvmlDeviceGetTotalEnergyConsumption
+  // (the driver's integrated counter); -1 when the device does not expose it.
+  double counter_joules() const;
 
  private:
   void sample_once();
+  bool read_energy_mj(unsigned long long* mj);
+  bool have_energy_ = false;
+  unsigned long long e0_ = 0, e1_ = 0;
   int device_;
   double period_ms_;
   void* dev_handle_ = nullptr;

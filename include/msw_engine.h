@@ -142,6 +142,15 @@ int msw_linear_decode(int32_t wtype, const void* w_tf, const void* scales, int32
  * 16-row tiles of 512-byte mma.sync A-fragment chunks; same byte count. */
 int msw_repack_decode(int32_t wtype, const void* w, int32_t n, int32_t k, void* out, void* stream);
 
+/* The W8A8 PRODUCTION kernels' raw int32 accumulators: w int8 [n,k]
+ * row-major, x fp32 [t,k] quantised per token exactly as in the engine
+ * (absmax/127, RNE), acc int32 [t,n] = sum_k w[n,k] * q(x)[t,k] before any
+ * scale. t <= 6 runs the decode GEMV (gemv_tf_kernel<INT8>, mma.sync s8),
+ * t > 6 the tcgen05 kind::i8 GEMM including its split-K combine. With
+ * integer x and max|x[t]| = 127 the quantisation is the identity. */
+int msw_linear_i8_raw(const int8_t* w, int32_t n, int32_t k, const float* x, int32_t t,
+                      int32_t* acc, void* stream);
+
 /* INT8 core on identical operands: acc[n] = sum_k w[n,k]*x[k] (int32 exact). */
 int msw_gemv_i8_acc(const int8_t* w, const int8_t* x, int32_t n, int32_t k,
                     int32_t* acc, void* stream);
@@ -158,6 +167,10 @@ int msw_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* packed,
                       uint16_t* scales, void* stream);
 
 int msw_device_sync(void);
+
+/* PCI bus id ("0000:1b:00.0") of CUDA device `device`, for resolving the
+ * matching NVML handle (energy sampling) independent of CUDA_VISIBLE_DEVICES. */
+int msw_device_pci_bus_id(int32_t device, char* buf, int32_t len);
 
 #ifdef __cplusplus
 }

@@ -144,15 +144,18 @@ int msw_write_decisions_csv(const char* ndjson, const msw_exec_row* rows, int32_
                             const char* path);
 
 /* Energy (include/modeswitch/energy.hpp; reference sim.hpp:14-31, sim.cpp:10-78).
- * msw_power_start: NVML power polling of `device` every period_ms in a host
- * thread. msw_power_stop: stops, optionally writes the trace as the reference's
+ * msw_power_start: NVML instantaneous-power polling of CUDA device `device`
+ * (NVML handle resolved by PCI bus id) every period_ms in a host thread.
+ * msw_power_stop: stops, optionally writes the trace as the reference's
  * "timestamp_ms,power_w" CSV, returns joules per token (tokens >= 1) by the
- * reference's trapezoid rule and the sample count; frees the sampler.
+ * reference's trapezoid rule, the sample count and (counter_joules, optional)
+ * the joules of the driver's total-energy counter over the same window, or -1
+ * when unsupported; frees the sampler.
  * msw_energy_from_trace: the same integration over a CSV trace on disk. */
 typedef struct msw_power_sampler msw_power_sampler;
 int msw_power_start(int32_t device, double period_ms, msw_power_sampler** out);
 int msw_power_stop(msw_power_sampler* s, const char* csv_path, int32_t tokens,
-                   double* joules_per_token, int32_t* n_samples);
+                   double* joules_per_token, int32_t* n_samples, double* counter_joules);
 int msw_energy_from_trace(const char* csv_path, int32_t tokens, double* joules_per_token);
 
 const char* msw_host_last_error(void);

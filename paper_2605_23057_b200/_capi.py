@@ -135,11 +135,13 @@ def engine_lib() -> C.CDLL:
         lib.msw_engine_reset_prefix_cache.argtypes = [vp]
         lib.msw_linear.argtypes = [i32, vp, vp, i32, i32, vp, i32, vp, vp]
         lib.msw_gemv_i8_acc.argtypes = [vp, vp, i32, i32, vp, vp]
+        lib.msw_linear_i8_raw.argtypes = [vp, i32, i32, vp, i32, vp, vp]
         lib.msw_linear_decode.argtypes = [i32, vp, vp, i32, i32, vp, i32, vp, vp]
         lib.msw_repack_decode.argtypes = [i32, vp, i32, i32, vp, vp]
         lib.msw_fill_fp16.argtypes = [vp, i64, i64, C.c_uint64, C.c_uint64, i32, vp]
         lib.msw_quant_int8_rows.argtypes = [vp, i32, i32, vp, vp, vp]
         lib.msw_quant_w4_rows.argtypes = [vp, i32, i32, vp, vp, vp]
+        lib.msw_device_pci_bus_id.argtypes = [i32, C.c_char_p, i32]
         _engine = lib
     return _engine
 
@@ -165,7 +167,7 @@ def host_lib() -> C.CDLL:
         lib.msw_write_decisions_csv.argtypes = [C.c_char_p, C.POINTER(ExecRow), C.c_int32, C.c_char_p]
         lib.msw_power_start.argtypes = [C.c_int32, C.c_double, C.POINTER(C.c_void_p)]
         lib.msw_power_stop.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.POINTER(C.c_double),
-                                       C.POINTER(C.c_int32)]
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_double)]
         lib.msw_energy_from_trace.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_double)]
         lib.msw_host_last_error.restype = C.c_char_p
         _host = lib

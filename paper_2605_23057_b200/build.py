@@ -19,7 +19,31 @@ ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "lib")
 INC = os.path.join(ROOT, "include")
 CSRC = os.path.join(PKG, "csrc")
-NLOHMANN = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+# nlohmann/json 3.11.3 (the version the reference's byte-exact NDJSON goldens
+# were generated with). MSW_NLOHMANN_INCLUDE names a directory holding
+# json.hpp; otherwise the copy vendored by cudnn_frontend in this image.
+NLOHMANN_CANDIDATES = [
+    os.environ.get("MSW_NLOHMANN_INCLUDE", ""),
+    "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann",
+    "/usr/include/nlohmann",
+]
+NLOHMANN_VERSION = (3, 11, 3)
+
+
+def nlohmann_dir() -> str:
+    import re
+    for d in NLOHMANN_CANDIDATES:
+        f = os.path.join(d, "json.hpp") if d else ""
+        if not f or not os.path.exists(f):
+            continue
+        txt = open(f, errors="replace").read(200_000)
+        ver = tuple(int(re.search(rf"#define NLOHMANN_JSON_VERSION_{k} (\d+)", txt).group(1))
+                    for k in ("MAJOR", "MINOR", "PATCH"))
+        if ver != NLOHMANN_VERSION:
+            raise RuntimeError(f"{f}: nlohmann/json {ver}, need {NLOHMANN_VERSION} "
+                               "(byte-exact NDJSON goldens); set MSW_NLOHMANN_INCLUDE")
+        return d
+    raise RuntimeError("nlohmann/json.hpp 3.11.3 not found; set MSW_NLOHMANN_INCLUDE")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -98,7 +122,7 @@ def build_host(force: bool = False) -> str:
     deps = srcs + _headers() + [ENGINE_SO]
     if force or _stale(HOST_SO, deps):
         _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra",
-              "-I", INC, "-I", NLOHMANN, *srcs, "-o", HOST_SO,
+              "-I", INC, "-I", nlohmann_dir(), *srcs, "-o", HOST_SO,
               "-L", LIB, "-lmsw_engine", "-Wl,-rpath,$ORIGIN", "-lpthread", "-ldl"])
     return HOST_SO
 

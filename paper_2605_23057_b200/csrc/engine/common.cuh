@@ -190,6 +190,18 @@ __device__ __forceinline__ void prefetch_l2_range(const void* p, size_t bytes, i
   }
 }
 
+// A/B experiment switches (MSW_NO_PDL, MSW_L2NEXT_KB, MSW_GEMV_W4_GENERIC,
+// MSW_SKIP) are read only by the diagnostics build (-DMSW_TRACE); the product
+// library ignores the environment.
+inline const char* diag_env(const char* name) {
+#ifdef MSW_TRACE
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 // Launch with the programmatic-stream-serialization attribute (PDL).
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -202,7 +214,7 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  static const bool pdl_off = std::getenv("MSW_NO_PDL") != nullptr;  // A/B experiments
+  static const bool pdl_off = diag_env("MSW_NO_PDL") != nullptr;  // A/B experiments
   cfg.attrs = attr;
   cfg.numAttrs = pdl_off ? 0 : 1;
   MSW_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));

@@ -174,10 +174,6 @@ struct Model {
   std::vector<void*> allocations;
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
   int graph_nodes[3] = {0, 0, 0};
-  // persistent decode step (decode_mk.cu), built on first use per format
-  bool mk_ready[3] = {false, false, false};
-  MkParams mk[3];
-  size_t mk_smem[3] = {0, 0, 0};
 
   size_t weight_bytes(int fmt) const {
     size_t b = size_t(c.vocab) * c.hidden * 2;  // fp16 lm_head in every mode
@@ -213,6 +209,7 @@ struct Scratch {
   int* hist = nullptr;
   int* stage = nullptr;  // pinned host staging
   size_t stage_ints = 0;
+  GemmWs gw;  // tcgen05 split-K workspace (deterministic combine)
 };
 
 }  // namespace
@@ -452,6 +449,11 @@ void alloc_scratch(msw_engine* e) {
   MSW_CUDA(cudaMemset(s.amax_ws, 0, sizeof(unsigned long long) * 2 * kMaxLogitRows));
   s.step = dalloc<int>(1);
   s.hist = dalloc<int>(size_t(e->cfg.max_seq_len) + 64);
+  s.gw.part = dalloc<uint32_t>(kGemmWsPartElems);
+  s.gw.part_elems = kGemmWsPartElems;
+  s.gw.cnt = dalloc<int>(kGemmWsTiles);
+  s.gw.cnt_n = kGemmWsTiles;
+  MSW_CUDA(cudaMemset(s.gw.cnt, 0, sizeof(int) * kGemmWsTiles));
   s.stage_ints = size_t(T) * 4 + 256;
   MSW_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.stage), s.stage_ints * sizeof(int),
                          cudaHostAllocDefault));
@@ -459,7 +461,7 @@ void alloc_scratch(msw_engine* e) {
                   (void*)s.xq, (void*)s.xscale, (void*)s.hsel, (void*)s.logits, (void*)s.part_o,
                   (void*)s.part_ml, (void*)s.tok, (void*)s.pos, (void*)s.slot, (void*)s.seq_of,
                   (void*)s.logit_rows, (void*)s.split_cnt, (void*)s.next, (void*)s.amax_ws, (void*)s.step,
-                  (void*)s.hist})
+                  (void*)s.hist, (void*)s.gw.part, (void*)s.gw.cnt})
     e->owned.push_back(p);
 }
 
@@ -467,13 +469,18 @@ void alloc_scratch(msw_engine* e) {
 // Runs T tokens (inputs already in sc.tok/pos/slot/seq_of) through model m in
 // format fmt; logits + argmax for the n_logits rows listed in sc.logit_rows
 // (rows == nullptr means rows 0..n_logits-1 == all T rows).
-// Diagnostics only: MSW_SKIP="attn,qkv,o,gu,down,head,argmax" drops those
-// launches from the step (outputs become meaningless) to attribute in-graph
-// step time per kernel class. Never set on a product path.
+// Diagnostics build only (-DMSW_TRACE, libmsw_engine_trace.so):
+// MSW_SKIP="attn,qkv,o,gu,down,head,argmax" drops those launches from the step
+// (outputs become meaningless) to attribute in-graph step time per kernel
+// class. The product library compiles this to a constant false.
+#ifdef MSW_TRACE
 bool diag_skip(const char* what) {
   static const char* env = std::getenv("MSW_SKIP");
   return env && std::strstr(env, what);
 }
+#else
+constexpr bool diag_skip(const char*) { return false; }
+#endif
 
 void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_identity,
              bool tokens_independent) {
@@ -507,7 +514,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       ++n;
     } else {
       launch_prep_act(fmt, s.h, T, H, ly.attn_norm, eps, s.xh, s.xq, s.xscale, st);
-      launch_gemm(ly.qkv[fmt], kEpiStore, s.xh, s.xq, s.xscale, T, s.qkv, st);
+      launch_gemm(ly.qkv[fmt], kEpiStore, s.xh, s.xq, s.xscale, T, s.qkv, s.gw, st);
       n += 2;
     }
     if (tokens_independent) {  // decode / CB: RoPE + KV append fused into attention
@@ -516,7 +523,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       n += 1;
     } else {
       launch_rope_append(s.qkv, T, s.pos, s.slot, m.rope, m.ash, s.q16, kc, vc, st);
-      if (T > kMaxLogitRows && !std::getenv("MSW_SCALAR_PREFILL_ATTN")) {
+      if (T > kMaxLogitRows) {
         launch_attention_prefill(s.q16, T, s.pos, s.seq_of, m.block_table, kc, vc, m.ash, s.o, st);
         n += 2;
       } else {
@@ -537,11 +544,11 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       n += 3;
     } else {
       launch_prep_act(fmt, s.o, T, Hq * D, nullptr, eps, s.xh, s.xq, s.xscale, st);
-      launch_gemm(ly.o[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, st);
+      launch_gemm(ly.o[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, s.gw, st);
       launch_prep_act(fmt, s.h, T, H, ly.ffn_norm, eps, s.xh, s.xq, s.xscale, st);
-      launch_gemm(ly.gu[fmt], kEpiSwiglu, s.xh, s.xq, s.xscale, T, s.act, st);
+      launch_gemm(ly.gu[fmt], kEpiSwiglu, s.xh, s.xq, s.xscale, T, s.act, s.gw, st);
       launch_prep_act(fmt, s.act, T, F, nullptr, eps, s.xh, s.xq, s.xscale, st);
-      launch_gemm(ly.down[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, st);
+      launch_gemm(ly.down[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, s.gw, st);
       n += 6;
     }
     (void)Hk;
@@ -558,7 +565,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
     ++n;
   } else {
     launch_prep_act(kFP16, hrows, n_logits, H, m.final_norm, eps, s.xh, s.xq, s.xscale, st);
-    launch_gemm(head, kEpiStore, s.xh, s.xq, s.xscale, n_logits, s.logits, st);
+    launch_gemm(head, kEpiStore, s.xh, s.xq, s.xscale, n_logits, s.logits, s.gw, st);
     n += 2;
   }
   if (!diag_skip("argmax")) launch_argmax(s.logits, n_logits, c.vocab, s.next, s.amax_ws, st);
@@ -723,94 +730,9 @@ void prefill_packed(msw_engine* e, Model& m, int fmt, const std::vector<PackSeq>
   }
 }
 
-// The persistent decode step's parameters for (m, fmt): device layer table,
-// barrier words, shared-memory plan. Returns false if the shape is outside
-// what decode_mk.cu covers (the per-kernel path below then runs).
-bool ensure_mk(msw_engine* e, Model& m, int fmt) {
-  static const bool on = std::getenv("MSW_MK") != nullptr;  // opt-in while it is tuned
-  if (!on) return false;
-  if (m.mk_ready[fmt]) return true;
-  Scratch& s = e->sc;
-  const msw_model_cfg& c = m.c;
-  MkParams P;
-  P.n_layers = c.n_layers;
-  P.H = c.hidden;
-  P.Hq = c.n_heads;
-  P.Hk = c.n_kv_heads;
-  P.D = c.head_dim;
-  P.F = c.ffn;
-  P.eps = c.rms_eps;
-  if (!mk_supported(P)) return false;
-  std::vector<MkLayer> ly(c.n_layers);
-  auto lin = [](const LinearW& W) {
-    MkLinear L;
-    L.w_tf = W.w_tf;
-    L.s = W.s;
-    L.n = W.n;
-    L.k = W.k;
-    return L;
-  };
-  for (int l = 0; l < c.n_layers; ++l) {
-    const Layer& src = m.layers[l];
-    ly[l].qkv = lin(src.qkv[fmt]);
-    ly[l].o = lin(src.o[fmt]);
-    ly[l].gu = lin(src.gu[fmt]);
-    ly[l].down = lin(src.down[fmt]);
-    ly[l].attn_norm = src.attn_norm;
-    ly[l].ffn_norm = src.ffn_norm;
-    ly[l].kc = m.kc + m.kv_layer_elems * l;
-    ly[l].vc = m.vc + m.kv_layer_elems * l;
-  }
-  MkLayer* d_ly = model_alloc<MkLayer>(m, ly.size());
-  MSW_CUDA(cudaMemcpy(d_ly, ly.data(), sizeof(MkLayer) * ly.size(), cudaMemcpyHostToDevice));
-  unsigned* sync = model_alloc<unsigned>(m, 2 + 64);  // bar, epoch, attn counters
-  MSW_CUDA(cudaMemset(sync, 0, sizeof(unsigned) * (2 + 64)));
-  P.layers = d_ly;
-  P.embed = m.embed;
-  P.head.w_tf = m.lm_head_tf;
-  P.head.n = c.vocab;
-  P.head.k = c.hidden;
-  P.final_norm = m.final_norm;
-  P.rope = m.rope;
-  P.block_table = m.block_table;
-  P.tok = s.tok;
-  P.pos = s.pos;
-  P.slot = s.slot;
-  P.step = s.step;
-  P.hist = s.hist;
-  P.next = s.next;
-  P.h = s.h;
-  P.qkv = s.qkv;
-  P.o = s.o;
-  P.act = s.act;
-  P.logits = s.logits;
-  P.part_o = s.part_o;
-  P.part_ml = s.part_ml;
-  P.bar = sync;
-  P.epoch = sync + 1;
-  P.attn_cnt = reinterpret_cast<int*>(sync + 2);
-  P.amax = s.amax_ws + (2 * kMaxLogitRows - 1);  // never touched by launch_argmax (T <= 64)
-  P.nsplit_max = std::max(1, std::min(32, kNumSMs / c.n_kv_heads));
-  P.one = 1;
-  m.mk_smem[fmt] = mk_smem_plan(P, fmt);
-  if (const char* ns = std::getenv("MSW_MK_SLOTS")) {  // ring-depth experiments
-    const int want = std::max(2, std::min(P.n_slots, std::atoi(ns)));
-    m.mk_smem[fmt] -= size_t(P.n_slots - want) * 32 * 1024;
-    P.n_slots = want;
-  }
-  m.mk[fmt] = P;
-  m.mk_ready[fmt] = true;
-  return true;
-}
-
 // One batch-1 decode step for model m / fmt, as a graph or eagerly.
 void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph) {
   Scratch& s = e->sc;
-  if (ensure_mk(e, m, fmt)) {  // one persistent launch: forward + argmax + advance
-    launch_decode_mk(fmt, m.mk[fmt], m.mk_smem[fmt], e->st);
-    ++e->launches;
-    return;
-  }
   auto body = [&]() {
     forward(e, m, fmt, 1, 1, true, true);
     launch_advance(s.next, s.tok, s.pos, s.slot, s.step, s.hist, m.block_table, e->st);
@@ -1087,6 +1009,15 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
       std::vector<Live> adm;
       while (next_req < n && !free_rows.empty()) {
         const msw_request& r = reqs[next_req];
+        // KV admission: a sequence is admitted only when the pool holds all of
+        // its blocks (prompt + max_new); otherwise wait for live sequences to
+        // retire. Only a request that cannot fit an empty pool is an error.
+        const int need = (r.prompt_len + r.max_new_tokens + kKvBlock - 1) / kKvBlock;
+        if (need > m.pool.available()) {
+          if (live.empty() && adm.empty())
+            throw DataErr("request needs more KV blocks than the pool holds");
+          break;
+        }
         Live L;
         L.req = next_req;
         L.row = free_rows.back();
@@ -1310,38 +1241,67 @@ int msw_engine_reset_prefix_cache(msw_engine* e) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+// Test entry shared by msw_linear and msw_linear_i8_raw: the production
+// dispatch (decode GEMV on the tile-fragment layout for t <= 6, prep_act +
+// tcgen05 GEMM otherwise) on row-major weights, with temporary buffers.
+void run_linear_entry(int32_t wtype, const void* w, const void* scales, int32_t n, int32_t k,
+                      const float* x, int32_t t, float* y, int epi, cudaStream_t st) {
+  LinearW W;
+  W.fmt = wtype;
+  W.n = n;
+  W.k = k;
+  W.w = w;
+  W.s = scales;
+  if (t <= kGemvMaxTokens) {
+    // weights arrive row-major; build the decode layout first
+    uint8_t* tf = dalloc<uint8_t>(tf_bytes(wtype, n, k));
+    launch_repack_tf(wtype, w, n, k, tf, st);
+    // the GEMV's producer streams weights BEFORE griddepcontrol.wait (PDL), so
+    // freshly repacked weights must be complete before it launches
+    MSW_CUDA(cudaStreamSynchronize(st));
+    W.w_tf = tf;
+    launch_gemv(W, kProPlain, epi, x, t, nullptr, 1e-5f, y, st);
+    MSW_CUDA(cudaStreamSynchronize(st));
+    cudaFree(tf);
+  } else {
+    half* xh = dalloc<half>(size_t(t) * k);
+    int8_t* xq = dalloc<int8_t>(size_t(t) * k);
+    float* xs = dalloc<float>(t);
+    GemmWs gw;
+    gw.part = dalloc<uint32_t>(kGemmWsPartElems);
+    gw.part_elems = kGemmWsPartElems;
+    gw.cnt = dalloc<int>(kGemmWsTiles);
+    gw.cnt_n = kGemmWsTiles;
+    MSW_CUDA(cudaMemsetAsync(gw.cnt, 0, sizeof(int) * kGemmWsTiles, st));
+    launch_prep_act(wtype, x, t, k, nullptr, 1e-5f, xh, xq, xs, st);
+    launch_gemm(W, epi, xh, xq, xs, t, y, gw, st);
+    MSW_CUDA(cudaStreamSynchronize(st));
+    cudaFree(xh);
+    cudaFree(xq);
+    cudaFree(xs);
+    cudaFree(gw.part);
+    cudaFree(gw.cnt);
+  }
+}
+}  // namespace
+
+extern "C" {
+
 int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n, int32_t k,
                const float* x, int32_t t, float* y, void* stream) {
   return guarded([&] {
-    LinearW W;
-    W.fmt = wtype;
-    W.n = n;
-    W.k = k;
-    W.w = w;
-    W.s = scales;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (t <= kGemvMaxTokens) {
-      // test entry: weights arrive row-major; build the decode layout first
-      uint8_t* tf = dalloc<uint8_t>(tf_bytes(wtype, n, k));
-      launch_repack_tf(wtype, w, n, k, tf, st);
-      // the GEMV's producer streams weights BEFORE griddepcontrol.wait (PDL), so
-      // freshly repacked weights must be complete before it launches
-      MSW_CUDA(cudaStreamSynchronize(st));
-      W.w_tf = tf;
-      launch_gemv(W, kProPlain, kEpiStore, x, t, nullptr, 1e-5f, y, st);
-      MSW_CUDA(cudaStreamSynchronize(st));
-      cudaFree(tf);
-    } else {
-      half* xh = dalloc<half>(size_t(t) * k);
-      int8_t* xq = dalloc<int8_t>(size_t(t) * k);
-      float* xs = dalloc<float>(t);
-      launch_prep_act(wtype, x, t, k, nullptr, 1e-5f, xh, xq, xs, st);
-      launch_gemm(W, kEpiStore, xh, xq, xs, t, y, st);
-      MSW_CUDA(cudaStreamSynchronize(st));
-      cudaFree(xh);
-      cudaFree(xq);
-      cudaFree(xs);
-    }
+    run_linear_entry(wtype, w, scales, n, k, x, t, y, kEpiStore, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int msw_linear_i8_raw(const int8_t* w, int32_t n, int32_t k, const float* x, int32_t t,
+                      int32_t* acc, void* stream) {
+  return guarded([&] {
+    run_linear_entry(kINT8, w, nullptr, n, k, x, t, reinterpret_cast<float*>(acc), kEpiRaw,
+                     static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -1393,6 +1353,13 @@ int msw_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* packed, 
 
 int msw_device_sync(void) {
   return guarded([&] { MSW_CUDA(cudaDeviceSynchronize()); });
+}
+
+int msw_device_pci_bus_id(int32_t device, char* buf, int32_t len) {
+  return guarded([&] {
+    if (!buf || len < 13) throw ConfigErr("msw_device_pci_bus_id: buffer too small");
+    MSW_CUDA(cudaDeviceGetPCIBusId(buf, len, device));
+  });
 }
 
 }  // extern "C"

@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int n = n0 + tx * 4 + j;
-      if (FMT == kINT8) {
+      if (EPI == kEpiRaw) {
+        v[j] = __int_as_float(int(acc[i][j]));
+      } else if (FMT == kINT8) {
         v[j] = n < N ? (float(acc[i][j]) * xscale[m]) * static_cast<const float*>(ws)[n] : 0.0f;
       } else {
         v[j] = float(acc[i][j]);
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < 4; j += 2) {
       const int n = n0 + tx * 4 + j;
       if (n >= N) continue;
-      if (EPI == kEpiStore) {
+      if (EPI == kEpiStore || EPI == kEpiRaw) {
         y[size_t(m) * N + n] = v[j];
         y[size_t(m) * N + n + 1] = v[j + 1];
       } else if (EPI == kEpiResid) {
@@ -154,8 +156,12 @@ void gemm_fmt(const LinearW& W, int epi, const half* xh, const int8_t* xq, const
     gemm_tiled_kernel<FMT, kEpiStore><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
   else if (epi == kEpiResid)
     gemm_tiled_kernel<FMT, kEpiResid><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
-  else
+  else if (epi == kEpiSwiglu)
     gemm_tiled_kernel<FMT, kEpiSwiglu><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
+  else if (FMT == kINT8 && epi == kEpiRaw)
+    gemm_tiled_kernel<FMT, kEpiRaw><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
+  else
+    throw ConfigErr("gemm: bad epilogue");
   MSW_LAUNCH_CHECK();
 }
 
@@ -168,8 +174,8 @@ void launch_prep_act(int fmt, const float* x, int T, int K, const half* gamma, f
 }
 
 void launch_gemm(const LinearW& W, int epi, const half* xh, const int8_t* xq, const float* xscale,
-                 int T, float* y, cudaStream_t st) {
-  if (gemm_tc_supported(W)) return launch_gemm_tc(W, epi, xh, xq, xscale, T, y, st);
+                 int T, float* y, const GemmWs& gw, cudaStream_t st) {
+  if (gemm_tc_supported(W)) return launch_gemm_tc(W, epi, xh, xq, xscale, T, y, gw, st);
   if (W.k % BK != 0 || W.n % 2 != 0) throw ConfigErr("gemm: bad shape");
   switch (W.fmt) {
     case kFP16: return gemm_fmt<kFP16>(W, epi, xh, xq, xscale, T, y, st);

@@ -20,6 +20,7 @@
 #include <cuda.h>
 
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 
 #include "kernels.cuh"
@@ -125,8 +126,10 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int N, int K, int T, const void* __restrict__ wscale,
                    const float* __restrict__ xscale, const uint32_t* __restrict__ w4,
-                   float* __restrict__ y, int ksplit) {
+                   float* __restrict__ y, int ksplit, uint32_t* __restrict__ ws_part,
+                   int* __restrict__ tile_cnt) {
   using C = TcCfg<FMT, BN>;
+  using Acc32 = typename std::conditional<FMT == kINT8, int, float>::type;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kTileM, t0 = blockIdx.y * BN;
-  // split-K: blockIdx.z owns k-tiles [kb0, kb0 + nk); partial sums are added atomically
+  // split-K: blockIdx.z owns k-tiles [kb0, kb0 + nk) (combined in the epilogue)
   const int nk_all = K / C::kTileK;
   const int nk_per = (nk_all + ksplit - 1) / ksplit;
   const int kb0 = blockIdx.z * nk_per;
@@ -232,30 +235,80 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   if (warp < 4) {
     mbar_wait(done, 0);
     tc_fence_after();
-    const int n = n0 + warp * 32 + lane;
+    const int row = warp * 32 + lane;
+    const int n = n0 + row;
     const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
     float ws = 1.0f;
     if (FMT == kINT8) ws = static_cast<const float*>(wscale)[n];
+    // Split-K is deterministic: every split stores its raw partial tile
+    // (INT8: the int32 accumulators themselves) to ws_part[z][tile][BN][128];
+    // the CTA that completes a tile's count sums the ksplit partials in z
+    // order and runs the epilogue once, so the INT8 result is the exact int32
+    // sum scaled once, and fp32 results do not depend on CTA arrival order.
+    const int tile_id = blockIdx.y * gridDim.x + blockIdx.x;
+    const size_t tile_stride = size_t(BN) * kTileM;
+    const size_t z_stride = size_t(gridDim.x) * gridDim.y * tile_stride;
+    bool last = true;
+    if (ksplit > 1) {
+      uint32_t* mine = ws_part + blockIdx.z * z_stride + tile_id * tile_stride + row;
 #pragma unroll 1
-    for (int j0 = 0; j0 < BN; j0 += 16) {
-      uint32_t r[16];
-      tmem_ld16(trow + j0, r);
+      for (int j0 = 0; j0 < BN; j0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(trow + j0, r);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int t = t0 + j0 + j;
-        float v;
-        if (FMT == kINT8) {
-          v = (float(int(r[j])) * (t < T ? xscale[t] : 0.0f)) * ws;
+        for (int j = 0; j < 16; ++j) mine[size_t(j0 + j) * kTileM] = nk > 0 ? r[j] : 0u;
+      }
+      __threadfence();
+      named_sync(1, 128);
+      __shared__ int s_last;
+      if (threadIdx.x == 0) {
+        const int old = atomicAdd(&tile_cnt[tile_id], 1);
+        s_last = old == ksplit - 1;
+        if (s_last) tile_cnt[tile_id] = 0;  // self-resetting for the next launch
+      }
+      named_sync(1, 128);
+      last = s_last != 0;
+      __threadfence();
+    }
+    if (last) {
+      const uint32_t* parts = ws_part + tile_id * tile_stride + row;
+#pragma unroll 1
+      for (int j0 = 0; j0 < BN; j0 += 16) {
+        uint32_t r[16];
+        if (ksplit > 1) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            Acc32 a = 0;
+            for (int z = 0; z < ksplit; ++z) {
+              const uint32_t u = __ldcg(parts + z * z_stride + size_t(j0 + j) * kTileM);
+              if (FMT == kINT8) a += Acc32(int(u));
+              else a += Acc32(__uint_as_float(u));
+            }
+            r[j] = FMT == kINT8 ? uint32_t(int(a)) : __float_as_uint(float(a));
+          }
         } else {
-          v = __uint_as_float(r[j]);
+          tmem_ld16(trow + j0, r);
         }
-        if (EPI == kEpiSwiglu) {  // never split (nonlinear)
-          const float up = __shfl_xor_sync(0xffffffffu, v, 1);
-          if (t < T && (lane & 1) == 0) y[size_t(t) * (N / 2) + (n >> 1)] = silu(v) * up;
-        } else if (t < T) {
-          if (ksplit > 1) atomicAdd(&y[size_t(t) * N + n], v);  // STORE targets are pre-zeroed
-          else if (EPI == kEpiStore) y[size_t(t) * N + n] = v;
-          else y[size_t(t) * N + n] += v;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int t = t0 + j0 + j;
+          if (EPI == kEpiRaw) {  // INT8 test entry: the int32 accumulator itself
+            if (t < T) reinterpret_cast<uint32_t*>(y)[size_t(t) * N + n] = r[j];
+            continue;
+          }
+          float v;
+          if (FMT == kINT8) {
+            v = (float(int(r[j])) * (t < T ? xscale[t] : 0.0f)) * ws;
+          } else {
+            v = __uint_as_float(r[j]);
+          }
+          if (EPI == kEpiSwiglu) {  // never split (nonlinear)
+            const float up = __shfl_xor_sync(0xffffffffu, v, 1);
+            if (t < T && (lane & 1) == 0) y[size_t(t) * (N / 2) + (n >> 1)] = silu(v) * up;
+          } else if (t < T) {
+            if (EPI == kEpiStore) y[size_t(t) * N + n] = v;
+            else y[size_t(t) * N + n] += v;
+          }
         }
       }
     }
@@ -307,7 +360,7 @@ CUtensorMap make_map(const void* base, int elt_bytes, uint64_t rows, uint64_t k,
 
 template <int FMT, int BN, int EPI>
 void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, float* y,
-               cudaStream_t st) {
+               const GemmWs& gw, cudaStream_t st) {
   using C = TcCfg<FMT, BN>;
   static bool attr = false;
   if (!attr) {
@@ -320,35 +373,44 @@ void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, f
   if (FMT != kW4) ta = make_map(W.w, elt, W.n, W.k, kTileM);
   const CUtensorMap tb = make_map(xact, elt, T, W.k, BN);
   // small grids (continuous-batching steps: T <= 64, n = 4096) leave most SMs
-  // idle; split K across CTAs and accumulate partials atomically
+  // idle; split K across CTAs (deterministic combine in the epilogue)
   const int tiles = (W.n / kTileM) * ((T + BN - 1) / BN);
   const int nk = W.k / C::kTileK;
   int ksplit = 1;
   if (EPI != kEpiSwiglu)
     while (tiles * ksplit * 2 <= kNumSMs && nk / (ksplit * 2) >= 8) ksplit *= 2;
-  if (ksplit > 1 && EPI == kEpiStore)
-    MSW_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * size_t(T) * W.n, st));
+  if (ksplit > 1) {
+    const int per = (nk + ksplit - 1) / ksplit;
+    ksplit = (nk + per - 1) / per;  // every split owns >= 1 k-tile
+  }
+  if (ksplit > 1 && (size_t(ksplit) * tiles * BN * kTileM > gw.part_elems || tiles > gw.cnt_n))
+    ksplit = 1;  // workspace too small for this shape: unsplit (still exact)
   const dim3 grid(W.n / kTileM, (T + BN - 1) / BN, ksplit);
   gemm_tc_kernel<FMT, BN, EPI><<<grid, C::kThreads, C::kSmem, st>>>(
-      ta, tb, W.n, W.k, T, W.s, xscale, static_cast<const uint32_t*>(W.w), y, ksplit);
+      ta, tb, W.n, W.k, T, W.s, xscale, static_cast<const uint32_t*>(W.w), y, ksplit, gw.part,
+      gw.cnt);
   MSW_LAUNCH_CHECK();
 }
 
 template <int FMT, int EPI>
 void launch_fmt_epi(const LinearW& W, const void* x, const float* xs, int T, float* y,
-                    cudaStream_t st) {
-  if (T <= 16) return launch_bn<FMT, 16, EPI>(W, x, xs, T, y, st);
-  if (T <= 32) return launch_bn<FMT, 32, EPI>(W, x, xs, T, y, st);
-  if (T <= 64) return launch_bn<FMT, 64, EPI>(W, x, xs, T, y, st);
-  return launch_bn<FMT, 128, EPI>(W, x, xs, T, y, st);
+                    const GemmWs& gw, cudaStream_t st) {
+  if (T <= 16) return launch_bn<FMT, 16, EPI>(W, x, xs, T, y, gw, st);
+  if (T <= 32) return launch_bn<FMT, 32, EPI>(W, x, xs, T, y, gw, st);
+  if (T <= 64) return launch_bn<FMT, 64, EPI>(W, x, xs, T, y, gw, st);
+  return launch_bn<FMT, 128, EPI>(W, x, xs, T, y, gw, st);
 }
 
 template <int FMT>
 void launch_fmt(const LinearW& W, int epi, const void* x, const float* xs, int T, float* y,
-                cudaStream_t st) {
-  if (epi == kEpiStore) return launch_fmt_epi<FMT, kEpiStore>(W, x, xs, T, y, st);
-  if (epi == kEpiResid) return launch_fmt_epi<FMT, kEpiResid>(W, x, xs, T, y, st);
-  return launch_fmt_epi<FMT, kEpiSwiglu>(W, x, xs, T, y, st);
+                const GemmWs& gw, cudaStream_t st) {
+  if (epi == kEpiStore) return launch_fmt_epi<FMT, kEpiStore>(W, x, xs, T, y, gw, st);
+  if (epi == kEpiResid) return launch_fmt_epi<FMT, kEpiResid>(W, x, xs, T, y, gw, st);
+  if (epi == kEpiSwiglu) return launch_fmt_epi<FMT, kEpiSwiglu>(W, x, xs, T, y, gw, st);
+  if constexpr (FMT == kINT8) {
+    if (epi == kEpiRaw) return launch_fmt_epi<FMT, kEpiRaw>(W, x, xs, T, y, gw, st);
+  }
+  throw ConfigErr("gemm_tc: bad epilogue for this format");
 }
 
 }  // namespace
@@ -358,12 +420,12 @@ bool gemm_tc_supported(const LinearW& W) {
 }
 
 void launch_gemm_tc(const LinearW& W, int epi, const half* xh, const int8_t* xq,
-                    const float* xscale, int T, float* y, cudaStream_t st) {
+                    const float* xscale, int T, float* y, const GemmWs& gw, cudaStream_t st) {
   if (!gemm_tc_supported(W)) throw ConfigErr("gemm_tc: n must be a multiple of 128, k of 128");
   switch (W.fmt) {
-    case kFP16: return launch_fmt<kFP16>(W, epi, xh, xscale, T, y, st);
-    case kINT8: return launch_fmt<kINT8>(W, epi, xq, xscale, T, y, st);
-    case kW4: return launch_fmt<kW4>(W, epi, xh, xscale, T, y, st);
+    case kFP16: return launch_fmt<kFP16>(W, epi, xh, xscale, T, y, gw, st);
+    case kINT8: return launch_fmt<kINT8>(W, epi, xq, xscale, T, y, gw, st);
+    case kW4: return launch_fmt<kW4>(W, epi, xh, xscale, T, y, gw, st);
     default: throw ConfigErr("gemm_tc: bad format");
   }
 }

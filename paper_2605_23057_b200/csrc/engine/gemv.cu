@@ -374,6 +374,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             i0 += int(part[b][w2][row][col]);
             i1 += int(part[b][w2][row + 1][col]);
           }
+          if (EPI == kEpiRaw) {  // test entry: the int32 accumulators themselves
+            if (col < T) {
+              reinterpret_cast<int*>(y)[size_t(col) * n + tile * 16 + row] = i0;
+              reinterpret_cast<int*>(y)[size_t(col) * n + tile * 16 + row + 1] = i1;
+            }
+            continue;
+          }
           v0 = float(i0);
           v1 = float(i1);
         } else {
@@ -826,7 +833,7 @@ thread_local L2Next t_next;
 L2Next make_l2_next(int cur_fmt, const LinearW* nw) {
   L2Next nx;
   static const long env_kb = [] {
-    const char* v = std::getenv("MSW_L2NEXT_KB");
+    const char* v = diag_env("MSW_L2NEXT_KB");
     return v ? std::atol(v) : -1L;
   }();
   const long kb = env_kb >= 0 ? env_kb : (cur_fmt == kW4 ? 128L : 0L);
@@ -913,7 +920,7 @@ void launch_tf(const LinearW& W, const float* x, int T, const half* gamma, float
                cudaStream_t st) {
   const int chunks_tile = W.k / TF<FMT>::kChunkK;
   if constexpr (FMT == kW4 && NT == 1) {  // the GPTQ modes decode batch-1
-    static const bool generic = std::getenv("MSW_GEMV_W4_GENERIC") != nullptr;  // A/B switch
+    static const bool generic = diag_env("MSW_GEMV_W4_GENERIC") != nullptr;  // A/B switch
     if (!generic) {
     if (chunks_tile == 64) return launch_w4<PRO, EPI, NT, 64, 1, true>(W, x, T, gamma, eps, y, st);
     if (chunks_tile % 64 == 0) return launch_w4<PRO, EPI, NT, 64, 1, false>(W, x, T, gamma, eps, y, st);
@@ -938,6 +945,9 @@ void dispatch_nt(const LinearW& W, int pro, int epi, const float* x, int T, cons
   MSW_GEMV_CASE(kProNorm, kEpiStore)
   MSW_GEMV_CASE(kProNorm, kEpiResid)
   MSW_GEMV_CASE(kProNorm, kEpiSwiglu)
+  if constexpr (FMT == kINT8) {
+    MSW_GEMV_CASE(kProPlain, kEpiRaw)
+  }
 #undef MSW_GEMV_CASE
   throw ConfigErr("gemv: bad prologue/epilogue");
 }
@@ -1000,11 +1010,13 @@ void launch_gemv_(const LinearW& W, int pro, int epi, const float* x, int T, con
   if (!W.w_tf) throw ConfigErr("gemv: decode (tile-fragment) weight layout missing");
   switch (W.fmt) {
     case kFP16:
-      if (T > 4 && size_t(kGemvMaxTokens) * 2 * W.k > 120 * 1024) {
-        // FP16, 5-6 tokens, large K: the 6-column activation stage leaves a
-        // 2-stage ring, and the 6-real-token case returned stale rows in ~5-45%
-        // of runs (scripts/repro_gemv_t6.py; root cause open).
-        // Run it as 4 + (T - 4) tokens (both clean over 100+ runs).
+      if (T == 6 && size_t(kGemvMaxTokens) * 2 * W.k > 120 * 1024 &&
+          !diag_env("MSW_GEMV_NO_SPLIT")) {
+        // FP16, 6 real tokens, large K: the 6-column activation stage leaves a
+        // 2-stage ring, and this case returned stale rows in ~5-45% of runs
+        // (scripts/repro_gemv_t6.py). No engine path issues it
+        // (speculative verify is T = k + 1 = 5, which runs in one launch);
+        // run it as 4 + 2 tokens.
         const size_t yrow = epi == kEpiSwiglu ? size_t(W.n / 2) : size_t(W.n);
         dispatch_fmt<kFP16>(W, pro, epi, x, 4, gamma, eps, y, st);
         return dispatch_fmt<kFP16>(W, pro, epi, x + size_t(4) * W.k, T - 4, gamma, eps,

@@ -41,10 +41,12 @@ void launch_interleave_rows(const void* a, const void* b, int n, size_t row_byte
 
 // ---- gemv.cu: batch-1 decode GEMV ----------------------------------------
 enum Prologue { kProPlain = 0, kProNorm = 1 };
-enum Epilogue { kEpiStore = 0, kEpiResid = 1, kEpiSwiglu = 2 };
+enum Epilogue { kEpiStore = 0, kEpiResid = 1, kEpiSwiglu = 2, kEpiRaw = 3 };
 // x: fp32 [k]. kProNorm: x <- x * rsqrt(mean(x^2)+eps) * gamma before the
 // format's activation handling (fp16 rounding, or int8 absmax quantisation).
 // kEpiStore: y[n] = v; kEpiResid: y[n] += v; kEpiSwiglu: y[i] = silu(v[2i]) * v[2i+1].
+// kEpiRaw (INT8 only, test entry msw_linear_i8_raw): y holds the int32
+// accumulators themselves, before any scale.
 // x is fp32 [T, k], 1 <= T <= kGemvMaxTokens; y rows are per token.
 constexpr int kGemvMaxTokens = 6;
 void launch_gemv(const LinearW& W, int pro, int epi, const float* x, int T, const half* gamma,
@@ -61,13 +63,24 @@ void launch_repack_tf(int fmt, const void* src, int n, int k, void* dst, cudaStr
 // quantisation (xq + per-token scale).
 void launch_prep_act(int fmt, const float* x, int T, int K, const half* gamma, float eps,
                      half* xh, int8_t* xq, float* xscale, cudaStream_t st);
+// Split-K workspace of the tcgen05 GEMM (owned by the caller, one per stream):
+// part holds per-split raw partial tiles, cnt per-tile arrival counters
+// (zeroed once at allocation, self-resetting).
+struct GemmWs {
+  uint32_t* part = nullptr;
+  size_t part_elems = 0;
+  int* cnt = nullptr;
+  int cnt_n = 0;
+};
+constexpr size_t kGemmWsPartElems = size_t(kNumSMs) * 128 * 128;  // >= ksplit*tiles*BN*128
+constexpr int kGemmWsTiles = kNumSMs;
 void launch_gemm(const LinearW& W, int epi, const half* xh, const int8_t* xq, const float* xscale,
-                 int T, float* y, cudaStream_t st);
+                 int T, float* y, const GemmWs& gw, cudaStream_t st);
 
 // ---- gemm_tc.cu: tcgen05/TMEM/TMA tensor-core path (n % 128 == 0, k % 128 == 0)
 bool gemm_tc_supported(const LinearW& W);
 void launch_gemm_tc(const LinearW& W, int epi, const half* xh, const int8_t* xq,
-                    const float* xscale, int T, float* y, cudaStream_t st);
+                    const float* xscale, int T, float* y, const GemmWs& gw, cudaStream_t st);
 
 // ---- attention.cu -----------------------------------------------------------
 struct AttnShape {
@@ -113,48 +126,5 @@ void launch_gather_rows(const float* src, const int* rows, int n, int width, flo
 // step += 1, pos += 1, slot from block-table row 0
 void launch_advance(const int* next, int* tok, int* pos, int* slot, int* step, int* history,
                     const int* block_table, cudaStream_t st);
-
-// ---- decode_mk.cu: persistent batch-1 decode step (one launch per token) ----
-struct MkLinear {
-  const void* w_tf = nullptr;  // tile-fragment weights
-  const void* s = nullptr;     // INT8: float [n]; W4: half [n][k/128]; FP16: unused
-  int n = 0, k = 0;
-};
-struct MkLayer {
-  MkLinear qkv, o, gu, down;
-  const half* attn_norm = nullptr;
-  const half* ffn_norm = nullptr;
-  half* kc = nullptr;  // this layer's paged K / V pool
-  half* vc = nullptr;
-};
-struct MkParams {
-  const MkLayer* layers = nullptr;  // device array [n_layers]
-  int n_layers = 0;
-  int H = 0, Hq = 0, Hk = 0, D = 0, F = 0;
-  float eps = 1e-5f;
-  const half* embed = nullptr;
-  MkLinear head;  // fp16 lm_head (tile-fragment), n = vocab
-  const half* final_norm = nullptr;
-  const float2* rope = nullptr;
-  const int* block_table = nullptr;  // row 0
-  // batch-1 decode state (advanced in-kernel: tok = hist[step] = next, pos += 1, slot)
-  int *tok = nullptr, *pos = nullptr, *slot = nullptr, *step = nullptr, *hist = nullptr,
-      *next = nullptr;
-  // scratch
-  float *h = nullptr, *qkv = nullptr, *o = nullptr, *act = nullptr, *logits = nullptr;
-  float *part_o = nullptr, *part_ml = nullptr;  // [Hq][nsplit_max][D], [Hq][nsplit_max][2]
-  int* attn_cnt = nullptr;                      // [Hk], self-resetting
-  unsigned* bar = nullptr;                      // grid-barrier arrivals (monotonic)
-  unsigned* epoch = nullptr;                    // launches completed
-  unsigned long long* amax = nullptr;           // argmax key, self-resetting
-  int nsplit_max = 1;
-  int xs_bytes = 0, sc_bytes = 0, n_slots = 0;  // shared-memory plan (mk_smem_plan)
-  uint32_t one = 1;                             // runtime 1 (keeps mul.hi shifts on the FMA pipe)
-};
-constexpr size_t kMkSmemMax = 223 * 1024;
-// Fills P.xs_bytes / sc_bytes / n_slots for format fmt; returns the dynamic smem bytes.
-size_t mk_smem_plan(MkParams& P, int fmt);
-bool mk_supported(const MkParams& P);
-void launch_decode_mk(int fmt, const MkParams& P, size_t smem, cudaStream_t st);
 
 }  // namespace msw

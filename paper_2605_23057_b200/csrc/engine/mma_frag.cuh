@@ -1,5 +1,4 @@
-// mma.sync fragment helpers shared by the decode GEMV (gemv.cu) and the
-// persistent decode step (decode_mk.cu).
+// mma.sync fragment helpers for the decode GEMV (gemv.cu).
 #pragma once
 
 #include "common.cuh"

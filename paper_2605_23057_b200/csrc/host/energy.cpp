@@ -10,6 +10,7 @@
 #include <string>
 
 #include "modeswitch/domain.hpp"
+#include "msw_engine.h"
 
 namespace modeswitch {
 
@@ -64,22 +65,46 @@ double energy_from_power_trace(const PowerTrace& trace, int tokens) {
 
 // ---- NVML, resolved at run time (no link dependency on the driver library)
 namespace {
+struct NvmlField {  // nvmlFieldValue_t (nvml.h)
+  unsigned field_id, scope_id;
+  long long timestamp, latency_usec;
+  int value_type, nvml_return;
+  union {
+    double d;
+    unsigned ui;
+    unsigned long ul;
+    unsigned long long ull;
+    long long sll;
+    int si;
+  } value;
+};
+constexpr unsigned kFieldPowerInstant = 186;  // NVML_FI_DEV_POWER_INSTANT (mW)
+
 struct Nvml {
   using InitFn = int (*)();
-  using HandleFn = int (*)(unsigned, void**);
+  using HandleIdxFn = int (*)(unsigned, void**);
+  using HandleBusFn = int (*)(const char*, void**);
   using PowerFn = int (*)(void*, unsigned*);
+  using FieldsFn = int (*)(void*, int, NvmlField*);
+  using EnergyFn = int (*)(void*, unsigned long long*);
   InitFn init = nullptr;
-  HandleFn handle = nullptr;
+  HandleIdxFn handle_idx = nullptr;
+  HandleBusFn handle_bus = nullptr;
   PowerFn power = nullptr;
+  FieldsFn fields = nullptr;
+  EnergyFn energy = nullptr;
   bool ok = false;
   Nvml() {
     void* lib = dlopen("libnvidia-ml.so.1", RTLD_LAZY | RTLD_LOCAL);
     if (!lib) lib = dlopen("libnvidia-ml.so", RTLD_LAZY | RTLD_LOCAL);
     if (!lib) return;
     init = reinterpret_cast<InitFn>(dlsym(lib, "nvmlInit_v2"));
-    handle = reinterpret_cast<HandleFn>(dlsym(lib, "nvmlDeviceGetHandleByIndex_v2"));
-    power = reinterpret_cast<PowerFn>(dlsym(lib, "nvmlDeviceGetPowerUsage"));  // milliwatts
-    ok = init && handle && power && init() == 0;
+    handle_idx = reinterpret_cast<HandleIdxFn>(dlsym(lib, "nvmlDeviceGetHandleByIndex_v2"));
+    handle_bus = reinterpret_cast<HandleBusFn>(dlsym(lib, "nvmlDeviceGetHandleByPciBusId_v2"));
+    power = reinterpret_cast<PowerFn>(dlsym(lib, "nvmlDeviceGetPowerUsage"));  // 1 s average on Ampere+
+    fields = reinterpret_cast<FieldsFn>(dlsym(lib, "nvmlDeviceGetFieldValues"));
+    energy = reinterpret_cast<EnergyFn>(dlsym(lib, "nvmlDeviceGetTotalEnergyConsumption"));  // mJ
+    ok = init && (handle_bus || handle_idx) && (power || fields) && init() == 0;
   }
 };
 Nvml& nvml() {
@@ -94,8 +119,23 @@ double now_ms() {
 
 PowerSampler::PowerSampler(int device, double period_ms) : device_(device), period_ms_(period_ms) {
   if (!nvml().ok) throw ConfigError("NVML unavailable: cannot sample GPU power");
-  if (nvml().handle(unsigned(device), &dev_handle_) != 0)
-    throw ConfigError("NVML: no handle for device " + std::to_string(device));
+  // CUDA ordinals and NVML indices differ under CUDA_VISIBLE_DEVICES or a
+  // non-PCI enumeration order: resolve the NVML device by the CUDA device's
+  // PCI bus id (libmsw_engine.so asks the CUDA runtime).
+  char bus[32] = {0};
+  int rc = -1;
+  if (nvml().handle_bus && msw_device_pci_bus_id(device, bus, int(sizeof(bus))) == 0)
+    rc = nvml().handle_bus(bus, &dev_handle_);
+  if (rc != 0 && nvml().handle_idx) rc = nvml().handle_idx(unsigned(device), &dev_handle_);
+  if (rc != 0) throw ConfigError("NVML: no handle for device " + std::to_string(device));
+}
+
+bool PowerSampler::read_energy_mj(unsigned long long* mj) {
+  return nvml().energy && nvml().energy(dev_handle_, mj) == 0;
+}
+
+double PowerSampler::counter_joules() const {
+  return have_energy_ ? double(e1_ - e0_) / 1000.0 : -1.0;
 }
 
 PowerSampler::~PowerSampler() {
@@ -103,17 +143,30 @@ PowerSampler::~PowerSampler() {
 }
 
 void PowerSampler::sample_once() {
-  unsigned mw = 0;
-  if (nvml().power(dev_handle_, &mw) != 0) return;
+  // instantaneous board power (NVML_FI_DEV_POWER_INSTANT); the legacy
+  // nvmlDeviceGetPowerUsage is a 1 s moving average on Ampere and newer, which
+  // would smear the previous request's power into a short window
+  double watts = -1.0;
+  if (nvml().fields) {
+    NvmlField f{};
+    f.field_id = kFieldPowerInstant;
+    if (nvml().fields(dev_handle_, 1, &f) == 0 && f.nvml_return == 0) watts = f.value.ui / 1000.0;
+  }
+  if (watts < 0.0 && nvml().power) {
+    unsigned mw = 0;
+    if (nvml().power(dev_handle_, &mw) == 0) watts = mw / 1000.0;
+  }
+  if (watts < 0.0) return;
   const double t = now_ms() - t0_;
   std::lock_guard<std::mutex> lk(mu_);
   if (!trace_.samples.empty() && !(t > trace_.samples.back().timestamp_ms)) return;
-  trace_.samples.push_back({t, mw / 1000.0});
+  trace_.samples.push_back({t, watts});
 }
 
 void PowerSampler::start() {
   if (running_) return;
   trace_.samples.clear();
+  have_energy_ = read_energy_mj(&e0_);
   t0_ = now_ms();
   sample_once();
   running_ = true;
@@ -131,6 +184,7 @@ PowerTrace PowerSampler::stop() {
     thread_.join();
   }
   sample_once();
+  if (have_energy_) have_energy_ = read_energy_mj(&e1_);
   std::lock_guard<std::mutex> lk(mu_);
   return trace_;
 }

@@ -295,11 +295,12 @@ int msw_power_start(int32_t device, double period_ms, msw_power_sampler** out) {
 }
 
 int msw_power_stop(msw_power_sampler* s, const char* csv_path, int32_t tokens,
-                   double* joules_per_token, int32_t* n_samples) {
+                   double* joules_per_token, int32_t* n_samples, double* counter_joules) {
   return guarded([&] {
     if (!s) throw ms::ConfigError("msw_power_stop: sampler is NULL");
     std::unique_ptr<msw_power_sampler> own(s);
     const ms::PowerTrace tr = own->impl.stop();
+    if (counter_joules) *counter_joules = own->impl.counter_joules();
     if (n_samples) *n_samples = int32_t(tr.samples.size());
     if (csv_path && *csv_path) ms::write_power_trace(tr, csv_path);
     if (joules_per_token) *joules_per_token = ms::energy_from_power_trace(tr, tokens);

@@ -24,6 +24,7 @@ class PowerSampler:
         self.device, self.period_ms, self.csv_path = device, period_ms, csv_path
         self._h = None
         self.joules_per_token = None
+        self.counter_joules_per_token = None
         self.samples = 0
 
     def __enter__(self):
@@ -33,11 +34,15 @@ class PowerSampler:
         return self
 
     def finish(self, tokens: int) -> float:
-        j, n = C.c_double(), C.c_int32()
+        """J/token by the reference's trapezoid rule over the recorded trace.
+        `counter_joules_per_token` is the same window from the driver's
+        total-energy counter (None where unsupported)."""
+        j, n, cj = C.c_double(), C.c_int32(), C.c_double()
         h, self._h = self._h, None
         check_host(host_lib().msw_power_stop(h, self.csv_path.encode() if self.csv_path else None,
-                                             int(tokens), C.byref(j), C.byref(n)))
+                                             int(tokens), C.byref(j), C.byref(n), C.byref(cj)))
         self.joules_per_token, self.samples = j.value, n.value
+        self.counter_joules_per_token = cj.value / tokens if cj.value >= 0 else None
         return j.value
 
     def __exit__(self, *exc):

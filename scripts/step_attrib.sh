@@ -4,6 +4,6 @@ mode=${1:-2}
 out=gpurun_out/step_attrib_m${mode}.txt
 : > $out
 for sk in "" attn argmax head "qkv" "o,oonly" gu down "qkv,o,oonly,gu,down" "qkv,o,oonly,gu,down,attn,head,argmax"; do
-  r=$(MSW_SKIP="$sk" timeout 300 python scripts/decode_once.py --mode $mode --new 129 --reps 2 2>&1 | tail -1)
+  r=$(MSW_ENGINE_SO=libmsw_engine_trace.so MSW_SKIP="$sk" timeout 300 python scripts/decode_once.py --mode $mode --new 129 --reps 2 2>&1 | tail -1)
   echo "skip=[$sk] $r" >> $out
 done

@@ -23,6 +23,9 @@ def test_power_trace_round_trip(cuda_ok, tmp_path):
     with open(path) as f:
         assert f.readline().strip() == "timestamp_ms,power_w"
     assert energy_from_trace(path, 20 * 40) == pytest.approx(jpt, rel=1e-12)
+    # instantaneous-power trace vs the driver's energy counter over the same window
+    if ps.counter_joules_per_token is not None:
+        assert ps.counter_joules_per_token == pytest.approx(jpt, rel=0.3)
 
 
 def test_profile_writer_measures_tiny_engine(cuda_ok, tmp_path):

@@ -205,3 +205,40 @@ def test_cuda_graphs_mode_on_eager_engine(cuda_ok):
         assert not eng.has_mode(MODE_INT8)
     finally:
         eng.close()
+
+
+def test_continuous_batching_bitwise_deterministic(long_pair):
+    # 40 live rows run the tcgen05 kind::i8 GEMM with split-K every step; the
+    # split partials are combined in a fixed order (int32), so logits repeat
+    # bit for bit across runs
+    eng, _ = long_pair
+    rng = np.random.default_rng(8)
+    plens = [int(x) for x in rng.integers(20, 200, size=40)]
+    nnew = [int(x) for x in rng.integers(3, 16, size=40)]
+    prompts = [prompt(7000 + i, plens[i], eng.vocab) for i in range(40)]
+    runs = [eng.run_batch(MODE_INT8_CB, prompts, nnew, want_logits=True) for _ in range(3)]
+    for rr in runs[1:]:
+        for a, b in zip(runs[0], rr):
+            assert np.array_equal(a.tokens, b.tokens)
+            assert np.array_equal(a.logits.view(np.uint32), b.logits.view(np.uint32))
+
+
+def test_continuous_batching_waits_for_kv_blocks(cuda_ok):
+    # a 12-block pool holds 2 of these 5-6-block sequences at a time:
+    # admission waits for retirements instead of failing the cohort
+    cfg = engine_cfg(target="tiny", draft=None, modes=(MODE_INT8, MODE_INT8_CB), seed=9,
+                     kv_blocks=12, max_seq_len=256)
+    eng = Engine(cfg)
+    try:
+        orc = O.OracleModel(model_cfg("tiny"), seed=9, max_ctx=256)
+        prompts = [prompt(100 + i, 60 + i, eng.vocab) for i in range(12)]
+        nnew = [12] * 12
+        res = eng.run_batch(MODE_INT8_CB, prompts, nnew)
+        for i, r in enumerate(res):
+            toks, _ = orc.generate(1, prompts[i], nnew[i])
+            assert np.array_equal(r.tokens, toks), i
+        with pytest.raises(MswError) as e:  # one request larger than the whole pool
+            eng.run_batch(MODE_INT8_CB, [prompt(1, 200, eng.vocab)], [50])
+        assert e.value.code == 3
+    finally:
+        eng.close()

@@ -6,9 +6,11 @@ BIT-EXACT; FP16 / W4 / W8A8 linears (decode GEMV for t <= 6, tcgen05 GEMM
 for t > 6 and n % 128 == 0, CUDA-core tile GEMM otherwise) within the stated
 relative tolerance
 (max |gpu - oracle| / max |oracle|):  FP16 2e-5 (GEMV) / 1e-4 (tcgen05
-accumulation over K up to 14336), W8A8 2e-5 (int32 exact, the
-only fp ops are two scale multiplies), W4 2e-3 (fp16 partial sums of <= 4
-products by contract)."""
+accumulation over K up to 14336), W4 2e-3 (fp16 partial sums of <= 4
+products by contract). W8A8 linears are BIT-EXACT end to end
+(same per-token quantisation, exact int32 accumulators, the same two scale
+multiplies), and msw_linear_i8_raw exposes the production kernels' int32
+accumulators for a direct comparison."""
 import ctypes as C
 
 import numpy as np
@@ -110,7 +112,7 @@ def test_linear_formats_vs_oracle(cuda_ok, t, n, k):
     q8, s8 = O.quant_int8_rows(w)
     y = _run_linear(_capi.W_INT8, torch.from_numpy(q8).cuda(), torch.from_numpy(s8).cuda(), n, k, x)
     ref = O.linear(_capi.W_INT8, q8, s8, x)
-    assert np.abs(y - ref).max() / np.abs(ref).max() < 2e-5
+    assert np.array_equal(y, ref)  # exact int32 accumulators, identical scale multiplies
     # W4 g128
     q4, s4 = O.quant_w4_rows(w)
     packed = _pack_w4_host(q4)
@@ -118,3 +120,47 @@ def test_linear_formats_vs_oracle(cuda_ok, t, n, k):
                     torch.from_numpy(s4.view(np.int16)).cuda(), n, k, x)
     ref = O.linear(_capi.W_W4, q4, s4, x)
     assert np.abs(y - ref).max() / np.abs(ref).max() < 2e-3
+
+
+def _i8_raw(w, x):
+    torch = _torch()
+    n, k = w.shape
+    t = x.shape[0]
+    dw = torch.from_numpy(np.ascontiguousarray(w)).cuda()
+    dx = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+    acc = torch.empty((t, n), dtype=torch.int32, device="cuda")
+    check_engine(engine_lib().msw_linear_i8_raw(dw.data_ptr(), n, k, dx.data_ptr(), t, acc.data_ptr(), None))
+    torch.cuda.synchronize()
+    return acc.cpu().numpy()
+
+
+@pytest.mark.parametrize("t", [1, 2, 5, 6, 7, 64, 300])
+@pytest.mark.parametrize("n,k", [(4096, 4096), (1024, 14336), (256, 4096), (96, 512)])
+def test_int8_production_accumulators_bit_exact(cuda_ok, t, n, k):
+    """The W8A8 product kernels (decode GEMV t<=6, tcgen05 kind::i8 GEMM with
+    its deterministic split-K t>6, tile GEMM for n % 128 != 0) return int32
+    accumulators identical to the oracle's exact integer dot products."""
+    rng = np.random.default_rng(t * 7919 + n + k)
+    w = rng.integers(-127, 128, size=(n, k), dtype=np.int8)
+    w[0, :] = 127  # row at the int32 extreme: 127*127*k
+    xi = rng.integers(-127, 128, size=(t, k)).astype(np.int8)
+    xi[:, 0] = 127  # absmax 127 -> per-token scale 1, quantisation is the identity
+    xi[0, :] = 127
+    got = _i8_raw(w, xi.astype(np.float32))
+    ref = np.stack([O.gemv_i8_acc(w, xi[i]) for i in range(t)])
+    assert np.array_equal(got, ref)
+
+
+def test_int8_split_k_linear_deterministic(cuda_ok):
+    """The tcgen05 INT8 linear at a continuous-batching shape (T=64, split-K 4)
+    is bitwise identical across repeated launches and equals the oracle."""
+    torch = _torch()
+    n, k, t = 4096, 4096, 64
+    w = O.fill_fp16(n, k, 5, 4242, 6)
+    q8, s8 = O.quant_int8_rows(w)
+    x = np.random.default_rng(1).standard_normal((t, k)).astype(np.float32)
+    dq, ds = torch.from_numpy(q8).cuda(), torch.from_numpy(s8).cuda()
+    outs = [_run_linear(_capi.W_INT8, dq, ds, n, k, x) for _ in range(8)]
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+    assert np.array_equal(outs[0], O.linear(_capi.W_INT8, q8, s8, x))
