@@ -210,6 +210,8 @@ struct Scratch {
   int* stage = nullptr;  // pinned host staging
   size_t stage_ints = 0;
   GemmWs gw;  // tcgen05 split-K workspace (deterministic combine)
+  SpecState* spec = nullptr;  // speculative-decoding round state (device)
+  int* spec_out = nullptr;    // emitted tokens of the running spec request
 };
 
 }  // namespace
@@ -224,6 +226,8 @@ struct msw_engine {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   long long launches = 0;
   std::vector<void*> owned;
+  cudaGraphExec_t spec_graph = nullptr;  // WHILE(tokens to emit) { spec round }
+  int spec_round_nodes = 0;
 };
 
 namespace msw {
@@ -454,14 +458,21 @@ void alloc_scratch(msw_engine* e) {
   s.gw.cnt = dalloc<int>(kGemmWsTiles);
   s.gw.cnt_n = kGemmWsTiles;
   MSW_CUDA(cudaMemset(s.gw.cnt, 0, sizeof(int) * kGemmWsTiles));
-  s.stage_ints = size_t(T) * 4 + 256;
+  s.spec = dalloc<SpecState>(1);
+  s.spec_out = dalloc<int>(size_t(e->cfg.max_seq_len) + 64);
+  {
+    SpecState init{};
+    init.out = s.spec_out;
+    MSW_CUDA(cudaMemcpy(s.spec, &init, sizeof(init), cudaMemcpyHostToDevice));
+  }
+  s.stage_ints = std::max<size_t>(size_t(T) * 4 + 256, sizeof(SpecState) / sizeof(int) + 8);
   MSW_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.stage), s.stage_ints * sizeof(int),
                          cudaHostAllocDefault));
   for (void* p : {(void*)s.h, (void*)s.qkv, (void*)s.q16, (void*)s.o, (void*)s.act, (void*)s.xh,
                   (void*)s.xq, (void*)s.xscale, (void*)s.hsel, (void*)s.logits, (void*)s.part_o,
                   (void*)s.part_ml, (void*)s.tok, (void*)s.pos, (void*)s.slot, (void*)s.seq_of,
                   (void*)s.logit_rows, (void*)s.split_cnt, (void*)s.next, (void*)s.amax_ws, (void*)s.step,
-                  (void*)s.hist, (void*)s.gw.part, (void*)s.gw.cnt})
+                  (void*)s.hist, (void*)s.gw.part, (void*)s.gw.cnt, (void*)s.spec, (void*)s.spec_out})
     e->owned.push_back(p);
 }
 
@@ -845,13 +856,73 @@ void run_single(msw_engine* e, const msw_request& r, msw_result& res) {
 
 // Speculative decoding: FP16 target + FP16 draft, k greedy proposals, one
 // batched verify of k+1 tokens; emitted tokens are the target's greedy tokens.
+// Everything after the two prefills runs on the device: one round is the
+// draft's T=2 step (re-running position n-2 so the round shape is fixed), its
+// k-1 T=1 steps, the target's (k+1)-token verify and the accept kernel, which
+// commits the tokens to the device state and sets the condition of the CUDA
+// graph WHILE node that repeats the round. A request's whole decode is one
+// graph launch with no host synchronisation; the host reads the tokens and
+// counters once at the end.
+void spec_round(msw_engine* e, cudaGraphConditionalHandle cond, bool use_cond) {
+  Scratch& s = e->sc;
+  Model& dr = e->draft;
+  Model& tg = e->target;
+  const int k = e->cfg.spec_k;
+  cudaStream_t st = e->st;
+  launch_spec_draft_setup(s.spec, s.tok, s.pos, s.slot, s.seq_of, s.logit_rows, dr.block_table, st);
+  forward(e, dr, kFP16, 2, 1, /*rows_identity=*/false, /*tokens_independent=*/false);
+  for (int i = 1; i < k; ++i) {
+    launch_spec_draft_next(s.spec, i, s.next, s.tok, s.pos, s.slot, s.seq_of, dr.block_table, st);
+    forward(e, dr, kFP16, 1, 1, true, true);
+  }
+  launch_spec_verify_setup(s.spec, k, s.next, s.tok, s.pos, s.slot, s.seq_of, tg.block_table, st);
+  forward(e, tg, kFP16, k + 1, k + 1, true, false);
+  launch_spec_accept(s.spec, k, s.next, s.logits, tg.c.vocab, cond, use_cond, st);
+  e->launches += 4 + k;
+}
+
+void build_spec_graph(msw_engine* e) {
+  cudaGraph_t g;
+  MSW_CUDA(cudaGraphCreate(&g, 0));
+  try {
+    cudaGraphConditionalHandle h;
+    MSW_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    MSW_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &p));
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    const long long before = e->launches;
+    MSW_CUDA(cudaStreamBeginCaptureToGraph(e->st, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    try {
+      spec_round(e, h, true);
+    } catch (...) {
+      cudaGraph_t dummy;
+      cudaStreamEndCapture(e->st, &dummy);
+      throw;
+    }
+    MSW_CUDA(cudaStreamEndCapture(e->st, &body));
+    e->spec_round_nodes = int(e->launches - before);
+    e->launches = before;
+    MSW_CUDA(cudaGraphInstantiate(&e->spec_graph, g, 0));
+  } catch (...) {
+    cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraphDestroy(g);
+}
+
 void run_spec(msw_engine* e, const msw_request& r, msw_result& res) {
   if (!e->cfg.has_draft) throw ConfigErr("speculative decoding needs a draft model");
   Model& tg = e->target;
   Model& dr = e->draft;
   if (!tg.fmt_on[kFP16]) throw ConfigErr("speculative decoding needs the FP16 target");
   const int k = e->cfg.spec_k;
-  if (k < 1 || k + 1 > kGemvMaxTokens) throw ConfigErr("spec_k must be in [1, 5]");
+  if (k < 1 || k + 1 > kGemvMaxTokens || k > kSpecMaxK) throw ConfigErr("spec_k must be in [1, 5]");
   check_request(e, r, k + 2);
   Scratch& s = e->sc;
   const int plen = r.prompt_len, n_new = r.max_new_tokens, V = tg.c.vocab;
@@ -865,111 +936,59 @@ void run_spec(msw_engine* e, const msw_request& r, msw_result& res) {
     release_sequence(tg, tb);
     throw;
   }
-  const bool want_logits = res.logits != nullptr;
   const bool graphs = e->cfg.use_graphs != 0;
-  std::vector<int32_t> seq(r.prompt_ids, r.prompt_ids + plen);
-  seq.reserve(npos + 8);
-  int rounds = 0, proposed = 0, accepted = 0;
+  float* lg_dev = nullptr;
+  SpecState fin{};
   float prefill_ms = 0, decode_ms = 0;
   try {
+    if (res.logits) lg_dev = dalloc<float>(size_t(n_new) * V);
+    if (graphs && !e->spec_graph) build_spec_graph(e);
     MSW_CUDA(cudaEventRecord(e->ev[0], e->st));
     prefill(e, dr, kFP16, 0, r.prompt_ids, 0, plen, db);
     prefill(e, tg, kFP16, 0, r.prompt_ids, 0, plen, tb);
-    int first = 0;
-    MSW_CUDA(cudaMemcpyAsync(s.stage, s.next, sizeof(int), cudaMemcpyDeviceToHost, e->st));
-    if (want_logits) copy_logits_row(e, res.logits, 0);
+    launch_spec_init(s.spec, s.next, plen, n_new, r.prompt_ids[plen - 1], lg_dev, e->st);
+    if (lg_dev)
+      MSW_CUDA(cudaMemcpyAsync(lg_dev, s.logits, sizeof(float) * V, cudaMemcpyDeviceToDevice, e->st));
+    e->launches += 1;
     MSW_CUDA(cudaEventRecord(e->ev[1], e->st));
-    MSW_CUDA(cudaStreamSynchronize(e->st));
-    first = s.stage[0];
-    seq.push_back(first);
-    res.out_ids[0] = first;
-    int emitted = 1;
-    int dlen = plen;  // positions present in the draft cache
-    std::vector<int> props(k), g(k + 1);
-    while (emitted < n_new) {
-      const int n = int(seq.size());
-      // draft catch-up (only after a fully accepted round): positions dlen .. n-2
-      if (dlen < n - 1) {
-        const int T = n - 1 - dlen;
-        for (int i = 0; i < T; ++i) {
-          const int p = dlen + i;
-          s.stage[i] = seq[p];
-          s.stage[T + i] = p;
-          s.stage[2 * T + i] = db.blocks[p / kKvBlock] * kKvBlock + p % kKvBlock;
-          s.stage[3 * T + i] = 0;
-        }
-        MSW_CUDA(cudaMemcpyAsync(s.tok, s.stage, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-        MSW_CUDA(cudaMemcpyAsync(s.pos, s.stage + T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-        MSW_CUDA(cudaMemcpyAsync(s.slot, s.stage + 2 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-        MSW_CUDA(cudaMemcpyAsync(s.seq_of, s.stage + 3 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-        if (T > 1) {
-          s.stage[4 * T] = T - 1;
-          MSW_CUDA(cudaMemcpyAsync(s.logit_rows, s.stage + 4 * T, sizeof(int), cudaMemcpyHostToDevice, e->st));
-        }
-        forward(e, dr, kFP16, T, 1, T == 1, T == 1);
-        MSW_CUDA(cudaStreamSynchronize(e->st));
-        dlen = n - 1;
-      }
-      // k greedy draft proposals from seq[n-1] at position n-1 (device-resident loop)
-      s.stage[0] = seq[n - 1];
-      MSW_CUDA(cudaMemcpyAsync(s.next, s.stage, sizeof(int), cudaMemcpyHostToDevice, e->st));
-      start_decode(e, dr, s.next, n - 2, 0);  // tok = seq[n-1], pos = n-1, hist[0] = seq[n-1]
-      for (int i = 0; i < k; ++i) decode_step(e, dr, kFP16, graphs);
-      // hist[1..k] are the proposals
-      MSW_CUDA(cudaMemcpyAsync(s.stage + 8, s.hist + 1, sizeof(int) * k, cudaMemcpyDeviceToHost, e->st));
-      MSW_CUDA(cudaStreamSynchronize(e->st));
-      for (int i = 0; i < k; ++i) props[i] = s.stage[8 + i];
-      dlen = n - 1 + k;
-      // target verify: [seq[n-1], d_1..d_k] at positions n-1 .. n-1+k
-      const int T = k + 1;
-      for (int i = 0; i < T; ++i) {
-        const int p = n - 1 + i;
-        s.stage[i] = i == 0 ? seq[n - 1] : props[i - 1];
-        s.stage[T + i] = p;
-        s.stage[2 * T + i] = tb.blocks[p / kKvBlock] * kKvBlock + p % kKvBlock;
-        s.stage[3 * T + i] = 0;
-      }
-      MSW_CUDA(cudaMemcpyAsync(s.tok, s.stage, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-      MSW_CUDA(cudaMemcpyAsync(s.pos, s.stage + T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-      MSW_CUDA(cudaMemcpyAsync(s.slot, s.stage + 2 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-      MSW_CUDA(cudaMemcpyAsync(s.seq_of, s.stage + 3 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-      forward(e, tg, kFP16, T, T, true, false);
-      MSW_CUDA(cudaMemcpyAsync(s.stage + 8, s.next, sizeof(int) * T, cudaMemcpyDeviceToHost, e->st));
-      MSW_CUDA(cudaStreamSynchronize(e->st));
-      for (int i = 0; i < T; ++i) g[i] = s.stage[8 + i];
-      int j = 0;
-      while (j < k && props[j] == g[j]) ++j;
-      ++rounds;
-      proposed += k;
-      accepted += j;
-      for (int i = 0; i <= j && emitted < n_new; ++i) {
-        seq.push_back(g[i]);
-        res.out_ids[emitted] = g[i];
-        if (want_logits) {
-          copy_logits_row(e, res.logits + size_t(emitted) * V, i);
+    if (n_new > 1) {
+      if (graphs) {
+        MSW_CUDA(cudaGraphLaunch(e->spec_graph, e->st));
+      } else {
+        int* emitted = s.stage;
+        do {
+          spec_round(e, 0, false);
+          MSW_CUDA(cudaMemcpyAsync(emitted, &s.spec->emitted, sizeof(int), cudaMemcpyDeviceToHost, e->st));
           MSW_CUDA(cudaStreamSynchronize(e->st));
-        }
-        ++emitted;
+        } while (*emitted < n_new);
       }
-      dlen = std::min(dlen, int(seq.size()) - 1);
     }
     MSW_CUDA(cudaEventRecord(e->ev[2], e->st));
+    MSW_CUDA(cudaMemcpyAsync(res.out_ids, s.spec_out, sizeof(int) * n_new, cudaMemcpyDeviceToHost, e->st));
+    MSW_CUDA(cudaMemcpyAsync(s.stage, s.spec, sizeof(SpecState), cudaMemcpyDeviceToHost, e->st));
+    if (lg_dev)
+      MSW_CUDA(cudaMemcpyAsync(res.logits, lg_dev, sizeof(float) * size_t(n_new) * V,
+                               cudaMemcpyDeviceToHost, e->st));
     MSW_CUDA(cudaStreamSynchronize(e->st));
+    std::memcpy(&fin, s.stage, sizeof(SpecState));
     MSW_CUDA(cudaEventElapsedTime(&prefill_ms, e->ev[0], e->ev[1]));
     MSW_CUDA(cudaEventElapsedTime(&decode_ms, e->ev[1], e->ev[2]));
   } catch (...) {
+    if (lg_dev) cudaFree(lg_dev);
     release_sequence(tg, tb);
     release_sequence(dr, db);
     throw;
   }
+  if (lg_dev) cudaFree(lg_dev);
   release_sequence(tg, tb);
   release_sequence(dr, db);
+  if (graphs) e->launches += (long long)fin.rounds * e->spec_round_nodes;
   res.n_out = n_new;
   res.prefill_ms = prefill_ms;
   res.decode_ms = decode_ms;
-  res.spec_rounds = rounds;
-  res.spec_proposed = proposed;
-  res.spec_accepted = accepted;
+  res.spec_rounds = fin.rounds;
+  res.spec_proposed = fin.proposed;
+  res.spec_accepted = fin.accepted;
   res.total_ms = now_ms() - t0;
 }
 
@@ -1213,6 +1232,7 @@ void msw_engine_destroy(msw_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->st);
+  if (e->spec_graph) cudaGraphExecDestroy(e->spec_graph);
   free_model(e->target);
   free_model(e->draft);
   for (void* p : e->owned) cudaFree(p);
@@ -1300,8 +1320,19 @@ int msw_linear(int32_t wtype, const void* w, const void* scales, int32_t n, int3
 int msw_linear_i8_raw(const int8_t* w, int32_t n, int32_t k, const float* x, int32_t t,
                       int32_t* acc, void* stream) {
   return guarded([&] {
-    run_linear_entry(kINT8, w, nullptr, n, k, x, t, reinterpret_cast<float*>(acc), kEpiRaw,
-                     static_cast<cudaStream_t>(stream));
+    // the kernels stage / read the per-row scales in every epilogue (the raw
+    // one ignores them): give them a valid array
+    float* ones = dalloc<float>(size_t(n));
+    std::vector<float> h(size_t(n), 1.0f);
+    try {
+      MSW_CUDA(cudaMemcpy(ones, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice));
+      run_linear_entry(kINT8, w, ones, n, k, x, t, reinterpret_cast<float*>(acc), kEpiRaw,
+                       static_cast<cudaStream_t>(stream));
+    } catch (...) {
+      cudaFree(ones);
+      throw;
+    }
+    cudaFree(ones);
   });
 }
 

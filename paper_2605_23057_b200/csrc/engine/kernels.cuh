@@ -127,4 +127,29 @@ void launch_gather_rows(const float* src, const int* rows, int n, int width, flo
 void launch_advance(const int* next, int* tok, int* pos, int* slot, int* step, int* history,
                     const int* block_table, cudaStream_t st);
 
+// ---- speculative decoding state (device) and round kernels (misc.cu) ----------
+constexpr int kSpecMaxK = 8;
+struct SpecState {
+  int n;         // committed sequence length (prompt + emitted)
+  int emitted;   // tokens emitted so far
+  int n_new;     // tokens to emit
+  int rounds, proposed, accepted;
+  int last;      // seq[n-1]
+  int prev;      // seq[n-2]
+  int props[kSpecMaxK];  // this round's draft proposals
+  int* out;             // emitted tokens [n_new]
+  float* logits_out;    // optional [n_new, V] logits of the emitted tokens
+};
+void launch_spec_init(SpecState* ss, const int* next, int plen, int n_new, int prompt_last,
+                      float* logits_out, cudaStream_t st);
+void launch_spec_draft_setup(const SpecState* ss, int* tok, int* pos, int* slot, int* seq_of,
+                             int* logit_rows, const int* block_table, cudaStream_t st);
+void launch_spec_draft_next(SpecState* ss, int i, const int* next, int* tok, int* pos, int* slot,
+                            int* seq_of, const int* block_table, cudaStream_t st);
+void launch_spec_verify_setup(SpecState* ss, int k, const int* next, int* tok, int* pos, int* slot,
+                              int* seq_of, const int* block_table, cudaStream_t st);
+// two launches (logits copy, accept); use_cond: accept sets the enclosing WHILE node's condition
+void launch_spec_accept(SpecState* ss, int k, const int* g, const float* logits, int V,
+                        cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t st);
+
 }  // namespace msw

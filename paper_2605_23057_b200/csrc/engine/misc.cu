@@ -102,6 +102,130 @@ __global__ void advance_kernel(const int* next, int* tok, int* pos, int* slot, i
   slot[0] = block_table[p >> 4] * kKvBlock + (p & 15);
 }
 
+
+// ---- speculative decoding, device side (one round = draft T=2 step, k-1
+// draft T=1 steps, target verify of k+1 tokens, accept) --------------------
+// Draft step 0 re-runs position n-2 with the token already there (same
+// token, same position: the KV it rewrites is the same value up to
+// summation order) together with the newest committed token at n-1, so the
+// round's shape never depends on how many proposals the previous round
+// accepted (the host loop needed a variable-length catch-up after a fully
+// accepted round).
+__global__ void spec_draft_setup_kernel(const SpecState* __restrict__ ss, int* tok, int* pos,
+                                        int* slot, int* seq_of, int* logit_rows,
+                                        const int* __restrict__ block_table) {
+  pdl_wait();
+  pdl_trigger();
+  const int t = threadIdx.x;
+  if (t >= 2) return;
+  const int n = ss->n;
+  const int p = n - 2 + t;
+  tok[t] = t == 0 ? ss->prev : ss->last;
+  pos[t] = p;
+  slot[t] = block_table[p >> 4] * kKvBlock + (p & 15);
+  seq_of[t] = 0;
+  if (t == 0) logit_rows[0] = 1;
+}
+
+// proposal i-1 (from the previous draft step's argmax) becomes the input of
+// draft step i at position n-1+i
+__global__ void spec_draft_next_kernel(SpecState* ss, int i, const int* __restrict__ next,
+                                       int* tok, int* pos, int* slot, int* seq_of,
+                                       const int* __restrict__ block_table) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x != 0) return;
+  const int d = next[0];
+  ss->props[i - 1] = d;
+  const int p = ss->n - 1 + i;
+  tok[0] = d;
+  pos[0] = p;
+  slot[0] = block_table[p >> 4] * kKvBlock + (p & 15);
+  seq_of[0] = 0;
+}
+
+// target verify input: [last, d_1 .. d_k] at positions n-1 .. n-1+k
+__global__ void spec_verify_setup_kernel(SpecState* ss, int k, const int* __restrict__ next,
+                                         int* tok, int* pos, int* slot, int* seq_of,
+                                         const int* __restrict__ block_table) {
+  pdl_wait();
+  pdl_trigger();
+  const int t = threadIdx.x;
+  if (t > k) return;
+  if (t == k) ss->props[k - 1] = next[0];  // the last draft step's argmax
+  const int d = t == 0 ? ss->last : (t == k ? next[0] : ss->props[t - 1]);
+  const int p = ss->n - 1 + t;
+  tok[t] = d;
+  pos[t] = p;
+  slot[t] = block_table[p >> 4] * kKvBlock + (p & 15);
+  seq_of[t] = 0;
+}
+
+// Accept the longest prefix where the target's greedy token equals the
+// draft's proposal, plus the target's own next token; emitted tokens are
+// appended to the request's output. Single thread: k <= 8 compares. With
+// `cond` the enclosing WHILE node's condition becomes "tokens still to emit".
+__device__ __forceinline__ int spec_matched(const SpecState* ss, int k, const int* g) {
+  int j = 0;
+  while (j < k && ss->props[j] == g[j]) ++j;
+  return j;
+}
+
+// Logits rows of the tokens this round will emit -> the request's logits
+// output (only when requested). Runs BEFORE spec_accept_kernel and reads the
+// state without modifying it, so all CTAs see the same round.
+__global__ void spec_copy_logits_kernel(const SpecState* __restrict__ ss, int k,
+                                        const int* __restrict__ g,
+                                        const float* __restrict__ logits, int V) {
+  pdl_wait();
+  pdl_trigger();
+  float* lg = ss->logits_out;
+  if (!lg) return;
+  const int j = spec_matched(ss, k, g);
+  const int emitted = ss->emitted;
+  const int ne = min(j + 1, ss->n_new - emitted);
+  const long long total = (long long)ne * V;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    lg[(long long)emitted * V + i] = logits[i];
+}
+
+__global__ void spec_accept_kernel(SpecState* ss, int k, const int* __restrict__ g,
+                                   cudaGraphConditionalHandle cond, int use_cond) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x != 0) return;
+  const int j = spec_matched(ss, k, g);
+  const int emitted = ss->emitted;
+  const int ne = min(j + 1, ss->n_new - emitted);  // committed this round: g[0 .. ne-1]
+  for (int i = 0; i < ne; ++i) ss->out[emitted + i] = g[i];
+  ss->prev = ne >= 2 ? g[ne - 2] : ss->last;
+  ss->last = g[ne - 1];
+  ss->n += ne;
+  ss->emitted = emitted + ne;
+  ss->rounds += 1;
+  ss->proposed += k;
+  ss->accepted += j;
+  if (use_cond) cudaGraphSetConditional(cond, emitted + ne < ss->n_new ? 1u : 0u);
+}
+
+// first token (target prefill argmax) -> state
+__global__ void spec_init_kernel(SpecState* ss, const int* __restrict__ next, int plen, int n_new,
+                                 int prompt_last, float* logits_out) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x != 0) return;
+  const int t = next[0];
+  ss->n = plen + 1;
+  ss->prev = prompt_last;
+  ss->last = t;
+  ss->emitted = 1;
+  ss->n_new = n_new;
+  ss->rounds = ss->proposed = ss->accepted = 0;
+  ss->out[0] = t;
+  ss->logits_out = logits_out;
+}
+
 }  // namespace
 
 void launch_embed(const half* emb, const int* tok, int T, int H, float* h, cudaStream_t st) {
@@ -123,6 +247,36 @@ void launch_advance(const int* next, int* tok, int* pos, int* slot, int* step, i
                     const int* block_table, cudaStream_t st) {
   launch_pdl(advance_kernel, dim3(1), dim3(32), 0, st, next, tok, pos, slot, step, history,
              block_table);
+}
+
+void launch_spec_init(SpecState* ss, const int* next, int plen, int n_new, int prompt_last,
+                      float* logits_out, cudaStream_t st) {
+  launch_pdl(spec_init_kernel, dim3(1), dim3(32), 0, st, ss, next, plen, n_new, prompt_last,
+             logits_out);
+}
+
+void launch_spec_draft_setup(const SpecState* ss, int* tok, int* pos, int* slot, int* seq_of,
+                             int* logit_rows, const int* block_table, cudaStream_t st) {
+  launch_pdl(spec_draft_setup_kernel, dim3(1), dim3(32), 0, st, ss, tok, pos, slot, seq_of,
+             logit_rows, block_table);
+}
+
+void launch_spec_draft_next(SpecState* ss, int i, const int* next, int* tok, int* pos, int* slot,
+                            int* seq_of, const int* block_table, cudaStream_t st) {
+  launch_pdl(spec_draft_next_kernel, dim3(1), dim3(32), 0, st, ss, i, next, tok, pos, slot, seq_of,
+             block_table);
+}
+
+void launch_spec_verify_setup(SpecState* ss, int k, const int* next, int* tok, int* pos, int* slot,
+                              int* seq_of, const int* block_table, cudaStream_t st) {
+  launch_pdl(spec_verify_setup_kernel, dim3(1), dim3(32), 0, st, ss, k, next, tok, pos, slot,
+             seq_of, block_table);
+}
+
+void launch_spec_accept(SpecState* ss, int k, const int* g, const float* logits, int V,
+                        cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t st) {
+  launch_pdl(spec_copy_logits_kernel, dim3(2 * kNumSMs), dim3(256), 0, st, ss, k, g, logits, V);
+  launch_pdl(spec_accept_kernel, dim3(1), dim3(32), 0, st, ss, k, g, cond, use_cond ? 1 : 0);
 }
 
 }  // namespace msw

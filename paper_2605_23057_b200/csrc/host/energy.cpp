@@ -150,7 +150,19 @@ void PowerSampler::sample_once() {
   if (nvml().fields) {
     NvmlField f{};
     f.field_id = kFieldPowerInstant;
-    if (nvml().fields(dev_handle_, 1, &f) == 0 && f.nvml_return == 0) watts = f.value.ui / 1000.0;
+    if (nvml().fields(dev_handle_, 1, &f) == 0 && f.nvml_return == 0) {
+      double mw = -1.0;  // nvmlValueType_t: 0 double, 1 uint, 2 ulong, 3 ull, 4 sll, 5 int
+      switch (f.value_type) {
+        case 0: mw = f.value.d; break;
+        case 1: mw = double(f.value.ui); break;
+        case 2: mw = double(f.value.ul); break;
+        case 3: mw = double(f.value.ull); break;
+        case 4: mw = double(f.value.sll); break;
+        case 5: mw = double(f.value.si); break;
+        default: break;
+      }
+      if (mw >= 0.0) watts = mw / 1000.0;
+    }
   }
   if (watts < 0.0 && nvml().power) {
     unsigned mw = 0;

@@ -84,6 +84,36 @@ def test_speculative_matches_target_greedy(pair):
     assert np.array_equal(r.tokens, greedy)
 
 
+@pytest.mark.parametrize("plen,n_new", [(1, 1), (1, 2), (3, 9), (45, 60), (200, 33)])
+def test_speculative_device_loop(pair, plen, n_new):
+    """The graph path (no logits requested: one WHILE-node graph launch per
+    request, accept on the device) emits the target's greedy tokens with the
+    oracle's round / accept counts, including n_new = 1 (no round) and 2."""
+    _, eng, orc, drf = pair
+    p = prompt(plen * 13 + n_new, plen, eng.vocab)
+    r = eng.run(MODE_SPEC, p, n_new)
+    toks, _, st = O.spec_generate(orc, drf, 4, p, n_new)
+    assert np.array_equal(r.tokens, toks)
+    assert (r.spec_rounds, r.spec_proposed, r.spec_accepted) == (st["rounds"], st["proposed"], st["accepted"])
+    r2 = eng.run(MODE_SPEC, p, n_new)  # replay is stateless across requests
+    assert np.array_equal(r2.tokens, toks) and r2.spec_rounds == r.spec_rounds
+
+
+def test_speculative_eager_engine(cuda_ok):
+    """use_graphs = 0: the same device round runs eagerly with a host check per round."""
+    shape = "tiny"
+    eng = Engine(engine_cfg(target=shape, draft="tiny_draft", seed=5, kv_blocks=256,
+                            max_seq_len=512, use_graphs=0))
+    orc = O.OracleModel(model_cfg(shape), seed=5, max_ctx=512)
+    drf = O.OracleModel(model_cfg("tiny_draft"), seed=5, is_draft=True, max_ctx=512)
+    p = prompt(71, 30, eng.vocab)
+    r = eng.run(MODE_SPEC, p, 41)
+    toks, _, st = O.spec_generate(orc, drf, 4, p, 41)
+    eng.close()
+    assert np.array_equal(r.tokens, toks)
+    assert (r.spec_rounds, r.spec_accepted) == (st["rounds"], st["accepted"])
+
+
 def test_prefix_caching_reuses_blocks_and_keeps_tokens(pair):
     _, eng, orc, _ = pair
     eng.reset_prefix_cache()
