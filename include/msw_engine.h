@@ -166,6 +166,20 @@ int msw_quant_int8_rows(const uint16_t* w, int32_t n, int32_t k, int8_t* q,
 int msw_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* packed,
                       uint16_t* scales, void* stream);
 
+/* Decode / continuous-batching attention (attn_decode_kernel, the engine's
+ * kernel): T query tokens, each the newest token of its own sequence.
+ * qkv fp32 [T, (Hq+2Hk)*D] (pre-RoPE); rope float2 [max_pos][D/2] (cos, sin);
+ * pos / slot / seq_of int32 [T]; block_table int32 [rows, max_blocks];
+ * kc / vc fp16 paged cache [nblk][Hk][16][D] (one layer). RoPE is applied to
+ * q and the new k, k / v are appended at slot[t], and o fp32 [T, Hq, D] is
+ * softmax(q k^T / sqrt(D)) v over positions [0, pos[t]], split over nsplit
+ * CTAs per (token, kv head) and merged in-kernel. */
+int msw_attention_decode(const float* qkv, const void* rope, int32_t T, const int32_t* pos,
+                         const int32_t* slot, const int32_t* seq_of, const int32_t* block_table,
+                         int32_t max_blocks, uint16_t* kc, uint16_t* vc, int32_t n_heads,
+                         int32_t n_kv_heads, int32_t head_dim, int32_t nsplit, float* o,
+                         void* stream);
+
 int msw_device_sync(void);
 
 /* PCI bus id ("0000:1b:00.0") of CUDA device `device`, for resolving the

@@ -142,6 +142,8 @@ def engine_lib() -> C.CDLL:
         lib.msw_quant_int8_rows.argtypes = [vp, i32, i32, vp, vp, vp]
         lib.msw_quant_w4_rows.argtypes = [vp, i32, i32, vp, vp, vp]
         lib.msw_device_pci_bus_id.argtypes = [i32, C.c_char_p, i32]
+        lib.msw_attention_decode.argtypes = [vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32,
+                                             i32, vp, vp]
         _engine = lib
     return _engine
 

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <list>
+#include <map>
 #include <memory>
 #include <unordered_map>
 #include <vector>
@@ -209,9 +210,10 @@ struct Scratch {
   int* hist = nullptr;
   int* stage = nullptr;  // pinned host staging
   size_t stage_ints = 0;
-  GemmWs gw;  // tcgen05 split-K workspace (deterministic combine)
   SpecState* spec = nullptr;  // speculative-decoding round state (device)
   int* spec_out = nullptr;    // emitted tokens of the running spec request
+  int* cb_hbase = nullptr;    // continuous batching: per live row, history base
+  int* cb_hist = nullptr;     // continuous batching: generated tokens [max_batch][max_seq_len]
 };
 
 }  // namespace
@@ -228,6 +230,7 @@ struct msw_engine {
   std::vector<void*> owned;
   cudaGraphExec_t spec_graph = nullptr;  // WHILE(tokens to emit) { spec round }
   int spec_round_nodes = 0;
+  std::map<int, std::pair<cudaGraphExec_t, int>> cb_graphs;  // live-batch size -> (step graph, nodes)
 };
 
 namespace msw {
@@ -446,6 +449,7 @@ void alloc_scratch(msw_engine* e) {
   s.slot = dalloc<int>(T);
   s.seq_of = dalloc<int>(T);
   s.logit_rows = dalloc<int>(kMaxLogitRows);
+  MSW_CUDA(cudaMemset(s.logit_rows, 0, sizeof(int) * kMaxLogitRows));
   s.split_cnt = dalloc<int>(tsplit * 64);
   MSW_CUDA(cudaMemset(s.split_cnt, 0, sizeof(int) * tsplit * 64));
   s.next = dalloc<int>(kMaxLogitRows);
@@ -453,11 +457,8 @@ void alloc_scratch(msw_engine* e) {
   MSW_CUDA(cudaMemset(s.amax_ws, 0, sizeof(unsigned long long) * 2 * kMaxLogitRows));
   s.step = dalloc<int>(1);
   s.hist = dalloc<int>(size_t(e->cfg.max_seq_len) + 64);
-  s.gw.part = dalloc<uint32_t>(kGemmWsPartElems);
-  s.gw.part_elems = kGemmWsPartElems;
-  s.gw.cnt = dalloc<int>(kGemmWsTiles);
-  s.gw.cnt_n = kGemmWsTiles;
-  MSW_CUDA(cudaMemset(s.gw.cnt, 0, sizeof(int) * kGemmWsTiles));
+  s.cb_hbase = dalloc<int>(T);
+  s.cb_hist = dalloc<int>(size_t(std::max(1, e->cfg.max_batch)) * e->cfg.max_seq_len);
   s.spec = dalloc<SpecState>(1);
   s.spec_out = dalloc<int>(size_t(e->cfg.max_seq_len) + 64);
   {
@@ -465,14 +466,15 @@ void alloc_scratch(msw_engine* e) {
     init.out = s.spec_out;
     MSW_CUDA(cudaMemcpy(s.spec, &init, sizeof(init), cudaMemcpyHostToDevice));
   }
-  s.stage_ints = std::max<size_t>(size_t(T) * 4 + 256, sizeof(SpecState) / sizeof(int) + 8);
+  s.stage_ints = std::max<size_t>(size_t(T) * 6 + 256, sizeof(SpecState) / sizeof(int) + 8);
   MSW_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.stage), s.stage_ints * sizeof(int),
                          cudaHostAllocDefault));
   for (void* p : {(void*)s.h, (void*)s.qkv, (void*)s.q16, (void*)s.o, (void*)s.act, (void*)s.xh,
                   (void*)s.xq, (void*)s.xscale, (void*)s.hsel, (void*)s.logits, (void*)s.part_o,
                   (void*)s.part_ml, (void*)s.tok, (void*)s.pos, (void*)s.slot, (void*)s.seq_of,
                   (void*)s.logit_rows, (void*)s.split_cnt, (void*)s.next, (void*)s.amax_ws, (void*)s.step,
-                  (void*)s.hist, (void*)s.gw.part, (void*)s.gw.cnt, (void*)s.spec, (void*)s.spec_out})
+                  (void*)s.hist, (void*)s.spec, (void*)s.spec_out,
+                  (void*)s.cb_hbase, (void*)s.cb_hist})
     e->owned.push_back(p);
 }
 
@@ -525,7 +527,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       ++n;
     } else {
       launch_prep_act(fmt, s.h, T, H, ly.attn_norm, eps, s.xh, s.xq, s.xscale, st);
-      launch_gemm(ly.qkv[fmt], kEpiStore, s.xh, s.xq, s.xscale, T, s.qkv, s.gw, st);
+      launch_gemm(ly.qkv[fmt], kEpiStore, s.xh, s.xq, s.xscale, T, s.qkv, st);
       n += 2;
     }
     if (tokens_independent) {  // decode / CB: RoPE + KV append fused into attention
@@ -555,11 +557,11 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       n += 3;
     } else {
       launch_prep_act(fmt, s.o, T, Hq * D, nullptr, eps, s.xh, s.xq, s.xscale, st);
-      launch_gemm(ly.o[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, s.gw, st);
+      launch_gemm(ly.o[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, st);
       launch_prep_act(fmt, s.h, T, H, ly.ffn_norm, eps, s.xh, s.xq, s.xscale, st);
-      launch_gemm(ly.gu[fmt], kEpiSwiglu, s.xh, s.xq, s.xscale, T, s.act, s.gw, st);
+      launch_gemm(ly.gu[fmt], kEpiSwiglu, s.xh, s.xq, s.xscale, T, s.act, st);
       launch_prep_act(fmt, s.act, T, F, nullptr, eps, s.xh, s.xq, s.xscale, st);
-      launch_gemm(ly.down[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, s.gw, st);
+      launch_gemm(ly.down[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, st);
       n += 6;
     }
     (void)Hk;
@@ -576,7 +578,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
     ++n;
   } else {
     launch_prep_act(kFP16, hrows, n_logits, H, m.final_norm, eps, s.xh, s.xq, s.xscale, st);
-    launch_gemm(head, kEpiStore, s.xh, s.xq, s.xscale, n_logits, s.logits, s.gw, st);
+    launch_gemm(head, kEpiStore, s.xh, s.xq, s.xscale, n_logits, s.logits, st);
     n += 2;
   }
   if (!diag_skip("argmax")) launch_argmax(s.logits, n_logits, c.vocab, s.next, s.amax_ws, st);
@@ -663,8 +665,9 @@ void prefill(msw_engine* e, Model& m, int fmt, int row, const int32_t* prompt, i
     MSW_CUDA(cudaMemcpyAsync(s.pos, st_pos, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
     MSW_CUDA(cudaMemcpyAsync(s.slot, st_slot, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
     MSW_CUDA(cudaMemcpyAsync(s.seq_of, st_seq, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-    const bool last = c0 + T >= plen;
-    if (last && T > 1) {
+    // every chunk's head runs on its last token (only the last chunk's result
+    // is used; the row must be valid either way)
+    if (T > 1) {
       int* st_rows = s.stage + 4 * T;
       st_rows[0] = T - 1;
       MSW_CUDA(cudaMemcpyAsync(s.logit_rows, st_rows, sizeof(int), cudaMemcpyHostToDevice, e->st));
@@ -726,8 +729,9 @@ void prefill_packed(msw_engine* e, Model& m, int fmt, const std::vector<PackSeq>
     MSW_CUDA(cudaMemcpyAsync(s.pos, st_pos, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
     MSW_CUDA(cudaMemcpyAsync(s.slot, st_slot, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
     MSW_CUDA(cudaMemcpyAsync(s.seq_of, st_seq, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-    if (nl > 0)
-      MSW_CUDA(cudaMemcpyAsync(s.logit_rows, st_rows, sizeof(int) * nl, cudaMemcpyHostToDevice, e->st));
+    if (nl == 0) st_rows[0] = T - 1;  // no sequence ends here: head on a valid (unused) row
+    MSW_CUDA(cudaMemcpyAsync(s.logit_rows, st_rows, sizeof(int) * std::max(nl, 1),
+                             cudaMemcpyHostToDevice, e->st));
     const bool ident = nl == T;  // every token is some sequence's last
     forward(e, m, fmt, T, std::max(nl, 1), ident, false);
     int* got = s.stage + 4 * kPrefillChunk + kMaxLogitRows;
@@ -995,8 +999,51 @@ void run_spec(msw_engine* e, const msw_request& r, msw_result& res) {
 // INT8 + continuous batching: iteration-level scheduling of a co-scheduled
 // cohort. Up to max_batch live sequences; each engine step decodes one token
 // for every live sequence (ragged positions, one block-table row each);
-// finished sequences retire and queued ones are admitted (prefilled) before
-// the next step. Per-request latency = its admission to its last token.
+// finished sequences retire and queued ones are admitted (prefilled, packed)
+// before the next step. Per-request latency = its admission to its last token.
+//
+// The step state (input token, position, KV slot, row, history base of every
+// live sequence) stays on the device and the step's own cb_advance kernel
+// moves it forward, so between scheduling events (a retirement, which frees a
+// row and KV blocks for admission) the host issues the steps back to back —
+// one CUDA graph per live-batch size T — and synchronises only at the event.
+// The host knows when the next event is: min over live sequences of the
+// tokens they still have to generate.
+void cb_step(msw_engine* e, Model& m, int T, bool use_graph) {
+  Scratch& s = e->sc;
+  auto body = [&]() {
+    forward(e, m, kINT8, T, T, true, true);
+    launch_cb_advance(s.next, T, s.tok, s.pos, s.slot, s.seq_of, s.cb_hbase, s.cb_hist,
+                      m.block_table, m.max_blocks, e->st);
+    ++e->launches;
+  };
+  if (!use_graph) {
+    body();
+    return;
+  }
+  auto it = e->cb_graphs.find(T);
+  if (it == e->cb_graphs.end()) {
+    const long long before = e->launches;
+    cudaGraph_t g;
+    MSW_CUDA(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
+    try {
+      body();
+    } catch (...) {
+      cudaStreamEndCapture(e->st, &g);
+      throw;
+    }
+    MSW_CUDA(cudaStreamEndCapture(e->st, &g));
+    cudaGraphExec_t x;
+    const cudaError_t rc = cudaGraphInstantiate(&x, g, 0);
+    cudaGraphDestroy(g);
+    MSW_CUDA(rc);
+    it = e->cb_graphs.emplace(T, std::make_pair(x, int(e->launches - before))).first;
+    e->launches = before;
+  }
+  MSW_CUDA(cudaGraphLaunch(it->second.first, e->st));
+  e->launches += it->second.second;
+}
+
 void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
   Model& m = e->target;
   const int fmt = kINT8;
@@ -1007,6 +1054,9 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
     check_request(e, reqs[i], 1);
   }
   Scratch& s = e->sc;
+  const int hstride = e->cfg.max_seq_len;  // device history ints per batch row
+  const int V = m.c.vocab;
+  const bool graphs = e->cfg.use_graphs != 0;
   struct Live {
     int req;
     int row;
@@ -1019,9 +1069,17 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
   std::vector<int> free_rows;
   for (int r = maxb - 1; r >= 0; --r) free_rows.push_back(r);
   int next_req = 0;
-  const double t0 = now_ms();
-  double decode_time = 0, prefill_time = 0;
-  std::vector<int> step_tok(maxb);
+  auto retire = [&](Live& L) {
+    msw_result& rr = res[L.req];
+    if (L.generated > 1)
+      MSW_CUDA(cudaMemcpy(rr.out_ids + 1, s.cb_hist + size_t(L.row) * hstride + 1,
+                          sizeof(int) * (L.generated - 1), cudaMemcpyDeviceToHost));
+    release_sequence(m, L.sb);
+    free_rows.push_back(L.row);
+    rr.n_out = L.generated;
+    rr.total_ms = now_ms() - L.t_admit;
+    rr.decode_ms = rr.total_ms - rr.prefill_ms;
+  };
   try {
     while (next_req < n || !live.empty()) {
       // admission: map every request that fits, then prefill them packed
@@ -1070,7 +1128,6 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
           throw;
         }
         const double tdone = now_ms();
-        prefill_time += tdone - tp;
         for (size_t j = 0; j < adm.size(); ++j) {
           Live& L = adm[j];
           msw_result& rr = res[L.req];
@@ -1079,52 +1136,50 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
           L.generated = 1;
           rr.prefill_ms = tdone - tp;
           if (L.generated >= reqs[L.req].max_new_tokens) {
-            release_sequence(m, L.sb);
-            free_rows.push_back(L.row);
-            rr.n_out = L.generated;
-            rr.total_ms = now_ms() - L.t_admit;
+            retire(L);
           } else {
             live.push_back(std::move(L));
           }
         }
       }
       if (live.empty()) continue;
-      // one decode step for every live sequence
+      // load the device step state of the live set (after any admission the
+      // packed prefill has reused these scratch arrays)
       const int T = int(live.size());
+      int steps = 1 << 30;
       for (int i = 0; i < T; ++i) {
         const Live& L = live[i];
-        const int p = reqs[L.req].prompt_len + L.generated - 1;
+        const msw_request& r = reqs[L.req];
+        const int p = r.prompt_len + L.generated - 1;
         s.stage[i] = L.last_tok;
         s.stage[T + i] = p;
         s.stage[2 * T + i] = L.sb.blocks[p / kKvBlock] * kKvBlock + p % kKvBlock;
         s.stage[3 * T + i] = L.row;
+        s.stage[4 * T + i] = L.row * hstride - r.prompt_len + 1;  // hist index of the output = hbase + p
+        steps = std::min(steps, r.max_new_tokens - L.generated);
       }
-      const double ts = now_ms();
       MSW_CUDA(cudaMemcpyAsync(s.tok, s.stage, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
       MSW_CUDA(cudaMemcpyAsync(s.pos, s.stage + T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
       MSW_CUDA(cudaMemcpyAsync(s.slot, s.stage + 2 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
       MSW_CUDA(cudaMemcpyAsync(s.seq_of, s.stage + 3 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
-      forward(e, m, fmt, T, T, true, true);
-      MSW_CUDA(cudaMemcpyAsync(s.stage + 4 * T, s.next, sizeof(int) * T, cudaMemcpyDeviceToHost, e->st));
-      for (int i = 0; i < T; ++i) {
-        msw_result& rr = res[live[i].req];
-        if (rr.logits) copy_logits_row(e, rr.logits + size_t(live[i].generated) * m.c.vocab, i);
+      MSW_CUDA(cudaMemcpyAsync(s.cb_hbase, s.stage + 4 * T, sizeof(int) * T, cudaMemcpyHostToDevice, e->st));
+      // steps until the next retirement, back to back on the device
+      for (int k = 0; k < steps; ++k) {
+        cb_step(e, m, T, graphs);
+        for (int i = 0; i < T; ++i) {
+          msw_result& rr = res[live[i].req];
+          if (rr.logits) copy_logits_row(e, rr.logits + size_t(live[i].generated + k) * V, i);
+        }
       }
+      MSW_CUDA(cudaMemcpyAsync(s.stage + 5 * T, s.tok, sizeof(int) * T, cudaMemcpyDeviceToHost, e->st));
       MSW_CUDA(cudaStreamSynchronize(e->st));
-      decode_time += now_ms() - ts;
-      // retire / advance
       std::vector<Live> still;
       for (int i = 0; i < T; ++i) {
         Live& L = live[i];
-        msw_result& rr = res[L.req];
-        L.last_tok = s.stage[4 * T + i];
-        rr.out_ids[L.generated++] = L.last_tok;
+        L.generated += steps;
+        L.last_tok = s.stage[5 * T + i];
         if (L.generated >= reqs[L.req].max_new_tokens) {
-          release_sequence(m, L.sb);
-          free_rows.push_back(L.row);
-          rr.n_out = L.generated;
-          rr.total_ms = now_ms() - L.t_admit;
-          rr.decode_ms = rr.total_ms - rr.prefill_ms;
+          retire(L);
         } else {
           still.push_back(std::move(L));
         }
@@ -1135,9 +1190,6 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
     for (Live& L : live) release_sequence(m, L.sb);
     throw;
   }
-  (void)t0;
-  (void)decode_time;
-  (void)prefill_time;
 }
 
 template <typename F>
@@ -1233,6 +1285,7 @@ void msw_engine_destroy(msw_engine* e) {
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->st);
   if (e->spec_graph) cudaGraphExecDestroy(e->spec_graph);
+  for (auto& kv : e->cb_graphs) cudaGraphExecDestroy(kv.second.first);
   free_model(e->target);
   free_model(e->draft);
   for (void* p : e->owned) cudaFree(p);
@@ -1290,20 +1343,12 @@ void run_linear_entry(int32_t wtype, const void* w, const void* scales, int32_t 
     half* xh = dalloc<half>(size_t(t) * k);
     int8_t* xq = dalloc<int8_t>(size_t(t) * k);
     float* xs = dalloc<float>(t);
-    GemmWs gw;
-    gw.part = dalloc<uint32_t>(kGemmWsPartElems);
-    gw.part_elems = kGemmWsPartElems;
-    gw.cnt = dalloc<int>(kGemmWsTiles);
-    gw.cnt_n = kGemmWsTiles;
-    MSW_CUDA(cudaMemsetAsync(gw.cnt, 0, sizeof(int) * kGemmWsTiles, st));
     launch_prep_act(wtype, x, t, k, nullptr, 1e-5f, xh, xq, xs, st);
-    launch_gemm(W, epi, xh, xq, xs, t, y, gw, st);
+    launch_gemm(W, epi, xh, xq, xs, t, y, st);
     MSW_CUDA(cudaStreamSynchronize(st));
     cudaFree(xh);
     cudaFree(xq);
     cudaFree(xs);
-    cudaFree(gw.part);
-    cudaFree(gw.cnt);
   }
 }
 }  // namespace
@@ -1379,6 +1424,38 @@ int msw_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* packed, 
   return guarded([&] {
     launch_quant_w4(reinterpret_cast<const half*>(w), n, k, reinterpret_cast<uint32_t*>(packed),
                     reinterpret_cast<half*>(scales), static_cast<cudaStream_t>(stream));
+  });
+}
+
+int msw_attention_decode(const float* qkv, const void* rope, int32_t T, const int32_t* pos,
+                         const int32_t* slot, const int32_t* seq_of, const int32_t* block_table,
+                         int32_t max_blocks, uint16_t* kc, uint16_t* vc, int32_t n_heads,
+                         int32_t n_kv_heads, int32_t head_dim, int32_t nsplit, float* o,
+                         void* stream) {
+  return guarded([&] {
+    if (T < 1 || nsplit < 1 || nsplit > 64 || n_kv_heads < 1 || n_heads % n_kv_heads)
+      throw ConfigErr("msw_attention_decode: bad shape");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t parts = size_t(T) * n_heads * nsplit;
+    float* part_o = dalloc<float>(parts * head_dim);
+    float* part_ml = dalloc<float>(parts * 2);
+    int* cnt = dalloc<int>(size_t(T) * n_kv_heads);
+    try {
+      MSW_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * size_t(T) * n_kv_heads, st));
+      const AttnShape a{n_heads, n_kv_heads, head_dim, max_blocks};
+      launch_attention_decode(qkv, static_cast<const float2*>(rope), T, pos, slot, seq_of,
+                              block_table, reinterpret_cast<half*>(kc), reinterpret_cast<half*>(vc),
+                              a, nsplit, part_o, part_ml, cnt, o, st);
+      MSW_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaFree(part_o);
+      cudaFree(part_ml);
+      cudaFree(cnt);
+      throw;
+    }
+    cudaFree(part_o);
+    cudaFree(part_ml);
+    cudaFree(cnt);
   });
 }
 

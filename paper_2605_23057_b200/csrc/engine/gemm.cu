@@ -174,8 +174,8 @@ void launch_prep_act(int fmt, const float* x, int T, int K, const half* gamma, f
 }
 
 void launch_gemm(const LinearW& W, int epi, const half* xh, const int8_t* xq, const float* xscale,
-                 int T, float* y, const GemmWs& gw, cudaStream_t st) {
-  if (gemm_tc_supported(W)) return launch_gemm_tc(W, epi, xh, xq, xscale, T, y, gw, st);
+                 int T, float* y, cudaStream_t st) {
+  if (gemm_tc_supported(W)) return launch_gemm_tc(W, epi, xh, xq, xscale, T, y, st);
   if (W.k % BK != 0 || W.n % 2 != 0) throw ConfigErr("gemm: bad shape");
   switch (W.fmt) {
     case kFP16: return gemm_fmt<kFP16>(W, epi, xh, xq, xscale, T, y, st);

@@ -7,16 +7,23 @@
 // feature, column = token). This keeps M at 128 for any token count, so small
 // continuous-batching steps (T = 16..64) still run full-width UMMAs.
 //
-// Per CTA (one 128 x BN output tile):
+// Per CTA (one 128 x BN output tile, or one K-slice of it):
 //   warp 0 (one lane) : TMA producer, 4-stage smem ring (SWIZZLE_128B tiles)
 //   warp 1 (one lane) : MMA issuer (tcgen05.mma, commit -> empty barrier)
 //   warp 2            : TMEM allocation owner
+//   warp 3 (one lane, W4) : TMA producer of the packed weights, 8-stage ring
 //   warps 0-3         : epilogue, tcgen05.ld 32x32b, fused store / residual
 //                       add / SwiGLU / W8A8 rescale
-//   warps 4-7 (W4)    : dequantisers: packed uint4b8 + fp16 group scale ->
-//                       fp16 (q-8)*s written in the SW128 K-major layout the
-//                       UMMA descriptor reads (no int4 UMMA on sm_100a)
+//   warps 4-7 (W4)    : dequantisers: packed uint4b8 (smem) + fp16 group
+//                       scale -> fp16 (q-8)*s written in the SW128 K-major
+//                       layout the UMMA descriptor reads (no int4 UMMA on sm_100a)
 // kind::f16 for FP16 and W4, kind::i8 (int32 accumulate, exact) for W8A8.
+//
+// Small token counts leave most SMs idle with one CTA per 128-row tile (a
+// continuous-batching step or a 128-token prefill of a 4096-row projection is
+// 32 tiles), so K is split over up to 8 CTAs that form a thread-block cluster
+// and reduce their partial tiles through distributed shared memory, in a
+// fixed order (deterministic; exact int32 for W8A8).
 #include <cuda.h>
 
 #include <mutex>
@@ -107,6 +114,11 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t
   return d;
 }
 
+// Split-K CTAs of one output tile form a thread-block cluster along z; the
+// partial tiles are reduced through distributed shared memory (below).
+constexpr int kMaxSplit = 8;  // portable cluster size
+constexpr int kPkStages = 8;  // W4: packed-weight ring depth (4 KB stages)
+
 template <int FMT, int BN>
 struct TcCfg {
   static constexpr bool kIsW4 = FMT == kW4;
@@ -115,33 +127,55 @@ struct TcCfg {
   static constexpr int kUmmaK = FMT == kINT8 ? 32 : 16;       // elements per UMMA
   static constexpr int kABytes = kTileM * kTileKBytes;        // 16 KB
   static constexpr int kBBytes = BN * kTileKBytes;
-  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kPkBytes = kIsW4 ? kTileM * 32 : 0;    // 128 rows x 8 packed words
   static constexpr int kThreads = kIsW4 ? 256 : 128;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kRingBytes = kStages * (kABytes + kBBytes) + kPkStages * kPkBytes;
+  static constexpr int kSmem = kRingBytes + 1024 /*align*/ + 256 /*barriers*/;
+  // split-K partial tile [BN][128] (fp32 / int32), staged in the A ring once
+  // every MMA has completed
+  static_assert(BN * kTileM * 4 <= kStages * kABytes, "partial tile must fit the A ring");
 };
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// 32-bit load from the same smem offset in cluster CTA `rank` (DSMEM)
+__device__ __forceinline__ uint32_t ld_dsmem(const void* local, uint32_t rank) {
+  uint32_t remote, v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote) : "memory");
+  return v;
+}
 
 template <int FMT, int BN, int EPI>
 __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int N, int K, int T, const void* __restrict__ wscale,
-                   const float* __restrict__ xscale, const uint32_t* __restrict__ w4,
-                   float* __restrict__ y, int ksplit, uint32_t* __restrict__ ws_part,
-                   int* __restrict__ tile_cnt) {
+                   const float* __restrict__ xscale, float* __restrict__ y, int ksplit) {
   using C = TcCfg<FMT, BN>;
   using Acc32 = typename std::conditional<FMT == kINT8, int, float>::type;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * C::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
+  uint8_t* sP = sB + kStages * C::kBBytes;  // W4 packed ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kRingBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* done = empty + kStages;
+  uint64_t* pfull = empty + kStages;
+  uint64_t* pempty = pfull + kPkStages;
+  uint64_t* done = pempty + kPkStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kTileM, t0 = blockIdx.y * BN;
-  // split-K: blockIdx.z owns k-tiles [kb0, kb0 + nk) (combined in the epilogue)
+  // split-K: blockIdx.z (= cluster rank) owns k-tiles [kb0, kb0 + nk)
   const int nk_all = K / C::kTileK;
   const int nk_per = (nk_all + ksplit - 1) / ksplit;
   const int kb0 = blockIdx.z * nk_per;
@@ -152,10 +186,14 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       mbar_init(&full[s], C::kIsW4 ? 1 + 4 : 1);  // TMA arrive (+ 4 dequant warps)
       mbar_init(&empty[s], 1);
     }
+    for (int s = 0; s < kPkStages; ++s) {
+      mbar_init(&pfull[s], 1);
+      mbar_init(&pempty[s], 4);
+    }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
-    if (!C::kIsW4) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -169,12 +207,12 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // ---- TMA producer
+    // ---- TMA producer: activation tiles (+ weight tiles for FP16 / INT8)
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % kStages;
       const uint32_t ph = (kb / kStages) & 1;
       mbar_wait(&empty[s], ph ^ 1);
-      mbar_expect_tx(&full[s], C::kIsW4 ? C::kBBytes : C::kStageBytes);
+      mbar_expect_tx(&full[s], C::kIsW4 ? C::kBBytes : C::kABytes + C::kBBytes);
       if (!C::kIsW4) tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * C::kTileK, n0);
       tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kb) * C::kTileK, t0);
     }
@@ -196,19 +234,34 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       umma_commit(&empty[s]);
     }
     umma_commit(done);  // with nk == 0 this still arrives (no MMA issued: D stays unwritten)
+  } else if (C::kIsW4 && warp == 3 && lane == 0) {
+    // ---- W4 packed-weight producer: 128 rows x 64 k (8 words per row, 4 KB)
+    // per k-tile, kPkStages deep, ahead of the dequantisers
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % kPkStages;
+      const uint32_t ph = (kb / kPkStages) & 1;
+      mbar_wait(&pempty[s], ph ^ 1);
+      mbar_expect_tx(&pfull[s], C::kPkBytes);
+      tma_load_2d(sP + s * C::kPkBytes, &tmA, &pfull[s], (kb0 + kb) * 8, n0);
+    }
   } else if (C::kIsW4 && warp >= 4) {
-    // ---- W4 dequantisers: thread r (0..127) owns weight row n0 + r of every k-tile
+    // ---- W4 dequantisers: thread r (0..127) owns weight row n0 + r of every
+    // k-tile: packed words from the smem ring -> fp16 (q-8)*s in the SW128
+    // K-major layout the UMMA descriptor reads (no int4 UMMA on sm_100a)
     const int r = threadIdx.x - 128;
-    const uint32_t* wrow = w4 + size_t(n0 + r) * (K / 8);
     const half* srow = static_cast<const half*>(wscale) + size_t(n0 + r) * (K / kW4Group);
     const half2 k1032 = __float2half2_rn(1032.0f);
     for (int kb = 0; kb < nk; ++kb) {
+      const int ps = kb % kPkStages;
+      const uint32_t pph = (kb / kPkStages) & 1;
       const int s = kb % kStages;
       const uint32_t ph = (kb / kStages) & 1;
-      // 64 k per tile = 8 packed words; one group scale covers it (128 | 64)
-      const uint4 p0 = ld_stream(wrow + (kb0 + kb) * 8);
-      const uint4 p1 = ld_stream(wrow + (kb0 + kb) * 8 + 4);
       const half2 s2 = __half2half2(srow[((kb0 + kb) * 64) / kW4Group]);
+      mbar_wait(&pfull[ps], pph);
+      const uint4* prow = reinterpret_cast<const uint4*>(sP + ps * C::kPkBytes + r * 32);
+      const uint4 p0 = prow[0], p1 = prow[1];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pempty[ps]);
       mbar_wait(&empty[s], ph ^ 1);
       uint8_t* rowp = sA + s * C::kABytes + r * 128;
       const uint32_t words[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
@@ -232,86 +285,85 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
 
   // ---- epilogue (warps 0-3): TMEM lane = weight row, column = token
   __syncwarp();  // reconverge the producer / MMA lanes before .sync.aligned TMEM loads
+  const int row = (warp & 3) * 32 + lane;
+  const int n = n0 + row;
+  float ws = 1.0f;
+  if (FMT == kINT8 && warp < 4) ws = static_cast<const float*>(wscale)[n];
+  // column j of this tile (token t0 + j), raw accumulator bits u
+  auto emit = [&](int j, uint32_t u) {
+    const int t = t0 + j;
+    if (EPI == kEpiRaw) {  // INT8 test entry: the int32 accumulator itself
+      if (t < T) reinterpret_cast<uint32_t*>(y)[size_t(t) * N + n] = u;
+      return;
+    }
+    const float v = FMT == kINT8 ? (float(int(u)) * (t < T ? xscale[t] : 0.0f)) * ws
+                                 : __uint_as_float(u);
+    if (EPI == kEpiSwiglu) {  // rows (2i, 2i+1) = (gate_i, up_i) sit in adjacent lanes
+      const float up = __shfl_xor_sync(0xffffffffu, v, 1);
+      if (t < T && (lane & 1) == 0) y[size_t(t) * (N / 2) + (n >> 1)] = silu(v) * up;
+    } else if (t < T) {
+      if (EPI == kEpiStore) y[size_t(t) * N + n] = v;
+      else y[size_t(t) * N + n] += v;
+    }
+  };
   if (warp < 4) {
     mbar_wait(done, 0);
     tc_fence_after();
-    const int row = warp * 32 + lane;
-    const int n = n0 + row;
-    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
-    float ws = 1.0f;
-    if (FMT == kINT8) ws = static_cast<const float*>(wscale)[n];
-    // Split-K is deterministic: every split stores its raw partial tile
-    // (INT8: the int32 accumulators themselves) to ws_part[z][tile][BN][128];
-    // the CTA that completes a tile's count sums the ksplit partials in z
-    // order and runs the epilogue once, so the INT8 result is the exact int32
-    // sum scaled once, and fp32 results do not depend on CTA arrival order.
-    const int tile_id = blockIdx.y * gridDim.x + blockIdx.x;
-    const size_t tile_stride = size_t(BN) * kTileM;
-    const size_t z_stride = size_t(gridDim.x) * gridDim.y * tile_stride;
-    bool last = true;
-    if (ksplit > 1) {
-      uint32_t* mine = ws_part + blockIdx.z * z_stride + tile_id * tile_stride + row;
+  }
+  const uint32_t trow = tmem + (uint32_t((warp & 3) * 32) << 16);
+  if (ksplit == 1) {
+    if (warp < 4) {
 #pragma unroll 1
       for (int j0 = 0; j0 < BN; j0 += 16) {
         uint32_t r[16];
         tmem_ld16(trow + j0, r);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) mine[size_t(j0 + j) * kTileM] = nk > 0 ? r[j] : 0u;
+        for (int j = 0; j < 16; ++j) emit(j0 + j, r[j]);
       }
-      __threadfence();
-      named_sync(1, 128);
-      __shared__ int s_last;
-      if (threadIdx.x == 0) {
-        const int old = atomicAdd(&tile_cnt[tile_id], 1);
-        s_last = old == ksplit - 1;
-        if (s_last) tile_cnt[tile_id] = 0;  // self-resetting for the next launch
-      }
-      named_sync(1, 128);
-      last = s_last != 0;
-      __threadfence();
     }
-    if (last) {
-      const uint32_t* parts = ws_part + tile_id * tile_stride + row;
+  } else {
+    // Deterministic split-K through distributed shared memory: every CTA of
+    // the cluster stages its raw partial tile [BN][128] in its own (now idle)
+    // A ring; after a cluster barrier CTA `rank` sums column slice
+    // [rank*BN/ks, (rank+1)*BN/ks) over the ks partials in rank order and runs
+    // the epilogue for it. INT8 partials are int32, so the result is the exact
+    // int32 sum, scaled once. No global workspace, no atomics, no tail CTA.
+    uint32_t* red = reinterpret_cast<uint32_t*>(sA);
+    if (warp < 4) {
 #pragma unroll 1
       for (int j0 = 0; j0 < BN; j0 += 16) {
         uint32_t r[16];
-        if (ksplit > 1) {
+        tmem_ld16(trow + j0, r);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            Acc32 a = 0;
-            for (int z = 0; z < ksplit; ++z) {
-              const uint32_t u = __ldcg(parts + z * z_stride + size_t(j0 + j) * kTileM);
-              if (FMT == kINT8) a += Acc32(int(u));
-              else a += Acc32(__uint_as_float(u));
-            }
-            r[j] = FMT == kINT8 ? uint32_t(int(a)) : __float_as_uint(float(a));
-          }
-        } else {
-          tmem_ld16(trow + j0, r);
-        }
+        for (int j = 0; j < 16; ++j) red[(j0 + j) * kTileM + row] = nk > 0 ? r[j] : 0u;
+      }
+    }
+    cluster_sync_all();
+    if (warp < 4) {
+      const int rank = int(cluster_ctarank());
+      const int cols = BN / ksplit;  // >= 2
+      // 8 columns x every split's partial in flight per batch (DSMEM latency)
+#pragma unroll 1
+      for (int c0 = 0; c0 < cols; c0 += 8) {
+        uint32_t u[8][kMaxSplit];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int t = t0 + j0 + j;
-          if (EPI == kEpiRaw) {  // INT8 test entry: the int32 accumulator itself
-            if (t < T) reinterpret_cast<uint32_t*>(y)[size_t(t) * N + n] = r[j];
-            continue;
-          }
-          float v;
-          if (FMT == kINT8) {
-            v = (float(int(r[j])) * (t < T ? xscale[t] : 0.0f)) * ws;
-          } else {
-            v = __uint_as_float(r[j]);
-          }
-          if (EPI == kEpiSwiglu) {  // never split (nonlinear)
-            const float up = __shfl_xor_sync(0xffffffffu, v, 1);
-            if (t < T && (lane & 1) == 0) y[size_t(t) * (N / 2) + (n >> 1)] = silu(v) * up;
-          } else if (t < T) {
-            if (EPI == kEpiStore) y[size_t(t) * N + n] = v;
-            else y[size_t(t) * N + n] += v;
-          }
+        for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+          for (int z = 0; z < kMaxSplit; ++z)
+            if (c0 + jj < cols && z < ksplit)
+              u[jj][z] = ld_dsmem(&red[(rank * cols + c0 + jj) * kTileM + row], uint32_t(z));
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          if (c0 + jj >= cols) break;  // warp-uniform
+          Acc32 a = 0;
+#pragma unroll
+          for (int z = 0; z < kMaxSplit; ++z)
+            if (z < ksplit) a += FMT == kINT8 ? Acc32(int(u[jj][z])) : Acc32(__uint_as_float(u[jj][z]));
+          emit(rank * cols + c0 + jj, FMT == kINT8 ? uint32_t(int(a)) : __float_as_uint(float(a)));
         }
       }
     }
+    cluster_sync_all();  // peers have read this CTA's partials before it exits
   }
   tc_fence_before();
   __syncthreads();
@@ -342,73 +394,103 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// 2-D K-major tile map: rows x k elements, box = box_rows x 128 bytes, SWIZZLE_128B.
-CUtensorMap make_map(const void* base, int elt_bytes, uint64_t rows, uint64_t k, int box_rows) {
+// 2-D K-major tile map: rows x k elements, box = box_rows x box_bytes.
+CUtensorMap make_map(const void* base, CUtensorMapDataType dt, int elt_bytes, uint64_t rows,
+                     uint64_t k, int box_rows, int box_bytes, CUtensorMapSwizzle swz) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {k, rows};
   const cuuint64_t strides[1] = {k * elt_bytes};
-  const cuuint32_t box[2] = {cuuint32_t(kTileKBytes / elt_bytes), cuuint32_t(box_rows)};
+  const cuuint32_t box[2] = {cuuint32_t(box_bytes / elt_bytes), cuuint32_t(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_fn()(&m, elt_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                                 2, const_cast<void*>(base), dims, strides, box, estr,
-                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  const CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
   return m;
 }
+CUtensorMap make_sw128_map(const void* base, int elt_bytes, uint64_t rows, uint64_t k, int box_rows) {
+  return make_map(base, elt_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                  elt_bytes, rows, k, box_rows, kTileKBytes, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// Split-K factor: the number of CTAs per output tile (a cluster along z) that
+// best fills the resident CTA slots. Tiles x ks CTAs over `slots` resident
+// CTAs: efficiency = work / (slots * waves). A split must keep >= 4 k-tiles.
+int choose_split(int tiles, int nk, int slots) {
+  auto eff = [&](int ks) {
+    const long long ctas = (long long)tiles * ks;
+    const long long waves = (ctas + slots - 1) / slots;
+    return double(ctas) / double(waves * slots);
+  };
+  int best = 1;
+  double best_e = eff(1);
+  for (int ks = 2; ks <= kMaxSplit; ks *= 2) {
+    if (nk / ks < 4) break;
+    const double e = eff(ks);
+    if (e > best_e + 0.05) {
+      best = ks;
+      best_e = e;
+    }
+  }
+  return best;
+}
 
 template <int FMT, int BN, int EPI>
 void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, float* y,
-               const GemmWs& gw, cudaStream_t st) {
+               cudaStream_t st) {
   using C = TcCfg<FMT, BN>;
-  static bool attr = false;
-  if (!attr) {
+  static int per_sm = 0;
+  if (!per_sm) {
     MSW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<FMT, BN, EPI>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    attr = true;
+    MSW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_tc_kernel<FMT, BN, EPI>,
+                                                           C::kThreads, C::kSmem));
+    per_sm = std::max(per_sm, 1);
   }
   const int elt = C::kElt;
-  CUtensorMap ta{};
-  if (FMT != kW4) ta = make_map(W.w, elt, W.n, W.k, kTileM);
-  const CUtensorMap tb = make_map(xact, elt, T, W.k, BN);
-  // small grids (continuous-batching steps: T <= 64, n = 4096) leave most SMs
-  // idle; split K across CTAs (deterministic combine in the epilogue)
+  // FP16 / INT8: weight tiles 128 rows x 128 B, SWIZZLE_128B; W4: packed
+  // words 128 rows x 8 words (32 B), unswizzled (the dequantisers swizzle)
+  const CUtensorMap ta =
+      FMT == kW4 ? make_map(W.w, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, W.n, W.k / 8, kTileM, 32,
+                            CU_TENSOR_MAP_SWIZZLE_NONE)
+                 : make_sw128_map(W.w, elt, W.n, W.k, kTileM);
+  const CUtensorMap tb = make_sw128_map(xact, elt, T, W.k, BN);
   const int tiles = (W.n / kTileM) * ((T + BN - 1) / BN);
-  const int nk = W.k / C::kTileK;
-  int ksplit = 1;
-  if (EPI != kEpiSwiglu)
-    while (tiles * ksplit * 2 <= kNumSMs && nk / (ksplit * 2) >= 8) ksplit *= 2;
-  if (ksplit > 1) {
-    const int per = (nk + ksplit - 1) / ksplit;
-    ksplit = (nk + per - 1) / per;  // every split owns >= 1 k-tile
-  }
-  if (ksplit > 1 && (size_t(ksplit) * tiles * BN * kTileM > gw.part_elems || tiles > gw.cnt_n))
-    ksplit = 1;  // workspace too small for this shape: unsplit (still exact)
-  const dim3 grid(W.n / kTileM, (T + BN - 1) / BN, ksplit);
-  gemm_tc_kernel<FMT, BN, EPI><<<grid, C::kThreads, C::kSmem, st>>>(
-      ta, tb, W.n, W.k, T, W.s, xscale, static_cast<const uint32_t*>(W.w), y, ksplit, gw.part,
-      gw.cnt);
-  MSW_LAUNCH_CHECK();
+  const int ksplit = choose_split(tiles, W.k / C::kTileK, kNumSMs * per_sm);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(W.n / kTileM, (T + BN - 1) / BN, ksplit);
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = ksplit;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MSW_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<FMT, BN, EPI>, ta, tb, W.n, W.k, T, W.s, xscale,
+                              y, ksplit));
 }
 
 template <int FMT, int EPI>
 void launch_fmt_epi(const LinearW& W, const void* x, const float* xs, int T, float* y,
-                    const GemmWs& gw, cudaStream_t st) {
-  if (T <= 16) return launch_bn<FMT, 16, EPI>(W, x, xs, T, y, gw, st);
-  if (T <= 32) return launch_bn<FMT, 32, EPI>(W, x, xs, T, y, gw, st);
-  if (T <= 64) return launch_bn<FMT, 64, EPI>(W, x, xs, T, y, gw, st);
-  return launch_bn<FMT, 128, EPI>(W, x, xs, T, y, gw, st);
+                    cudaStream_t st) {
+  if (T <= 16) return launch_bn<FMT, 16, EPI>(W, x, xs, T, y, st);
+  if (T <= 32) return launch_bn<FMT, 32, EPI>(W, x, xs, T, y, st);
+  if (T <= 64) return launch_bn<FMT, 64, EPI>(W, x, xs, T, y, st);
+  return launch_bn<FMT, 128, EPI>(W, x, xs, T, y, st);
 }
 
 template <int FMT>
 void launch_fmt(const LinearW& W, int epi, const void* x, const float* xs, int T, float* y,
-                const GemmWs& gw, cudaStream_t st) {
-  if (epi == kEpiStore) return launch_fmt_epi<FMT, kEpiStore>(W, x, xs, T, y, gw, st);
-  if (epi == kEpiResid) return launch_fmt_epi<FMT, kEpiResid>(W, x, xs, T, y, gw, st);
-  if (epi == kEpiSwiglu) return launch_fmt_epi<FMT, kEpiSwiglu>(W, x, xs, T, y, gw, st);
+                cudaStream_t st) {
+  if (epi == kEpiStore) return launch_fmt_epi<FMT, kEpiStore>(W, x, xs, T, y, st);
+  if (epi == kEpiResid) return launch_fmt_epi<FMT, kEpiResid>(W, x, xs, T, y, st);
+  if (epi == kEpiSwiglu) return launch_fmt_epi<FMT, kEpiSwiglu>(W, x, xs, T, y, st);
   if constexpr (FMT == kINT8) {
-    if (epi == kEpiRaw) return launch_fmt_epi<FMT, kEpiRaw>(W, x, xs, T, y, gw, st);
+    if (epi == kEpiRaw) return launch_fmt_epi<FMT, kEpiRaw>(W, x, xs, T, y, st);
   }
   throw ConfigErr("gemm_tc: bad epilogue for this format");
 }
@@ -420,12 +502,12 @@ bool gemm_tc_supported(const LinearW& W) {
 }
 
 void launch_gemm_tc(const LinearW& W, int epi, const half* xh, const int8_t* xq,
-                    const float* xscale, int T, float* y, const GemmWs& gw, cudaStream_t st) {
+                    const float* xscale, int T, float* y, cudaStream_t st) {
   if (!gemm_tc_supported(W)) throw ConfigErr("gemm_tc: n must be a multiple of 128, k of 128");
   switch (W.fmt) {
-    case kFP16: return launch_fmt<kFP16>(W, epi, xh, xscale, T, y, gw, st);
-    case kINT8: return launch_fmt<kINT8>(W, epi, xq, xscale, T, y, gw, st);
-    case kW4: return launch_fmt<kW4>(W, epi, xh, xscale, T, y, gw, st);
+    case kFP16: return launch_fmt<kFP16>(W, epi, xh, xscale, T, y, st);
+    case kINT8: return launch_fmt<kINT8>(W, epi, xq, xscale, T, y, st);
+    case kW4: return launch_fmt<kW4>(W, epi, xh, xscale, T, y, st);
     default: throw ConfigErr("gemm_tc: bad format");
   }
 }

@@ -63,24 +63,13 @@ void launch_repack_tf(int fmt, const void* src, int n, int k, void* dst, cudaStr
 // quantisation (xq + per-token scale).
 void launch_prep_act(int fmt, const float* x, int T, int K, const half* gamma, float eps,
                      half* xh, int8_t* xq, float* xscale, cudaStream_t st);
-// Split-K workspace of the tcgen05 GEMM (owned by the caller, one per stream):
-// part holds per-split raw partial tiles, cnt per-tile arrival counters
-// (zeroed once at allocation, self-resetting).
-struct GemmWs {
-  uint32_t* part = nullptr;
-  size_t part_elems = 0;
-  int* cnt = nullptr;
-  int cnt_n = 0;
-};
-constexpr size_t kGemmWsPartElems = size_t(kNumSMs) * 128 * 128;  // >= ksplit*tiles*BN*128
-constexpr int kGemmWsTiles = kNumSMs;
 void launch_gemm(const LinearW& W, int epi, const half* xh, const int8_t* xq, const float* xscale,
-                 int T, float* y, const GemmWs& gw, cudaStream_t st);
+                 int T, float* y, cudaStream_t st);
 
 // ---- gemm_tc.cu: tcgen05/TMEM/TMA tensor-core path (n % 128 == 0, k % 128 == 0)
 bool gemm_tc_supported(const LinearW& W);
 void launch_gemm_tc(const LinearW& W, int epi, const half* xh, const int8_t* xq,
-                    const float* xscale, int T, float* y, const GemmWs& gw, cudaStream_t st);
+                    const float* xscale, int T, float* y, cudaStream_t st);
 
 // ---- attention.cu -----------------------------------------------------------
 struct AttnShape {
@@ -126,6 +115,11 @@ void launch_gather_rows(const float* src, const int* rows, int n, int width, flo
 // step += 1, pos += 1, slot from block-table row 0
 void launch_advance(const int* next, int* tok, int* pos, int* slot, int* step, int* history,
                     const int* block_table, cudaStream_t st);
+// continuous batching: hist[hbase[t] + pos[t]] = tok[t] = next[t]; pos[t] += 1;
+// slot[t] from block-table row seq_of[t]
+void launch_cb_advance(const int* next, int T, int* tok, int* pos, int* slot, const int* seq_of,
+                       const int* hbase, int* hist, const int* block_table, int bt_stride,
+                       cudaStream_t st);
 
 // ---- speculative decoding state (device) and round kernels (misc.cu) ----------
 constexpr int kSpecMaxK = 8;

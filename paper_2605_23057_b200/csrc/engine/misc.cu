@@ -103,6 +103,26 @@ __global__ void advance_kernel(const int* next, int* tok, int* pos, int* slot, i
 }
 
 
+// Continuous-batching step bookkeeping (T live sequences, one token each):
+// the step's argmax becomes each sequence's next input, is appended to that
+// sequence's device history (index hbase[t] + pos[t]), and position / slot
+// advance through the sequence's own block-table row (seq_of[t]).
+__global__ void cb_advance_kernel(const int* __restrict__ next, int T, int* tok, int* pos,
+                                  int* slot, const int* __restrict__ seq_of,
+                                  const int* __restrict__ hbase, int* hist,
+                                  const int* __restrict__ block_table, int bt_stride) {
+  pdl_wait();
+  pdl_trigger();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int out = next[t];
+  const int p = pos[t];
+  hist[hbase[t] + p] = out;
+  tok[t] = out;
+  pos[t] = p + 1;
+  slot[t] = block_table[size_t(seq_of[t]) * bt_stride + ((p + 1) >> 4)] * kKvBlock + ((p + 1) & 15);
+}
+
 // ---- speculative decoding, device side (one round = draft T=2 step, k-1
 // draft T=1 steps, target verify of k+1 tokens, accept) --------------------
 // Draft step 0 re-runs position n-2 with the token already there (same
@@ -247,6 +267,13 @@ void launch_advance(const int* next, int* tok, int* pos, int* slot, int* step, i
                     const int* block_table, cudaStream_t st) {
   launch_pdl(advance_kernel, dim3(1), dim3(32), 0, st, next, tok, pos, slot, step, history,
              block_table);
+}
+
+void launch_cb_advance(const int* next, int T, int* tok, int* pos, int* slot, const int* seq_of,
+                       const int* hbase, int* hist, const int* block_table, int bt_stride,
+                       cudaStream_t st) {
+  launch_pdl(cb_advance_kernel, dim3(ceil_div(T, 64)), dim3(64), 0, st, next, T, tok, pos, slot,
+             seq_of, hbase, hist, block_table, bt_stride);
 }
 
 void launch_spec_init(SpecState* ss, const int* next, int plen, int n_new, int prompt_last,
