@@ -35,7 +35,7 @@
 namespace msw {
 namespace {
 
-constexpr int kStages = 4;
+constexpr int kMaxStages = 8;  // operand ring depth cap (barrier arrays)
 constexpr int kTileM = 128;     // weight rows per CTA (UMMA M)
 constexpr int kTileKBytes = 128;  // one SW128 row per k-tile
 
@@ -130,11 +130,20 @@ struct TcCfg {
   static constexpr int kPkBytes = kIsW4 ? kTileM * 32 : 0;    // 128 rows x 8 packed words
   static constexpr int kThreads = kIsW4 ? 256 : 128;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  // operand ring as deep as ~220 KB of shared memory allows (one CTA per SM):
+  // a short prefill / CB step streams weights at HBM rate only with enough
+  // bytes in flight per SM (latency x bandwidth / 148)
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStagesFit = (220 * 1024 - kPkStages * kPkBytes) / kStageBytes;
+  static constexpr int kStages = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
   static constexpr int kRingBytes = kStages * (kABytes + kBBytes) + kPkStages * kPkBytes;
-  static constexpr int kSmem = kRingBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmem = kRingBytes + 1024 /*align*/ + 512 /*barriers*/;
   // split-K partial tile [BN][128] (fp32 / int32), staged in the A ring once
-  // every MMA has completed
+  // every MMA has completed; up to ks-1 incoming column slices ((ks-1)/ks of
+  // a tile) land in the B ring
+  static_assert(kStages >= 4, "ring too shallow");
   static_assert(BN * kTileM * 4 <= kStages * kABytes, "partial tile must fit the A ring");
+  static_assert(BN * kTileM * 4 <= kStages * kBBytes, "incoming slices must fit the B ring");
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -146,12 +155,18 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
-// 32-bit load from the same smem offset in cluster CTA `rank` (DSMEM)
-__device__ __forceinline__ uint32_t ld_dsmem(const void* local, uint32_t rank) {
-  uint32_t remote, v;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote) : "memory");
-  return v;
+// Bulk copy of `bytes` from this CTA's smem to the same-named buffers of
+// cluster CTA `rank`: dst / bar are local addresses mapped into the peer.
+__device__ __forceinline__ void bulk_s2s_peer(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint32_t rank) {
+  uint32_t rdst, rbar;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rdst) : "r"(smem_u32(dst)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          rdst),
+      "r"(smem_u32(src)), "r"(bytes), "r"(rbar)
+      : "memory");
 }
 
 template <int FMT, int BN, int EPI>
@@ -164,14 +179,15 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * C::kABytes;
-  uint8_t* sP = sB + kStages * C::kBBytes;  // W4 packed ring
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint8_t* sP = sB + C::kStages * C::kBBytes;  // W4 packed ring
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kRingBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* pfull = empty + kStages;
+  uint64_t* empty = full + C::kStages;
+  uint64_t* pfull = empty + C::kStages;
   uint64_t* pempty = pfull + kPkStages;
   uint64_t* done = pempty + kPkStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* rbar = done + 1;  // split-K: incoming partial slices
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kTileM, t0 = blockIdx.y * BN;
@@ -182,7 +198,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   const int nk = max(0, min(nk_all - kb0, nk_per));
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], C::kIsW4 ? 1 + 4 : 1);  // TMA arrive (+ 4 dequant warps)
       mbar_init(&empty[s], 1);
     }
@@ -191,6 +207,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       mbar_init(&pempty[s], 4);
     }
     mbar_init(done, 1);
+    mbar_init(rbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -209,8 +226,8 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   if (warp == 0 && lane == 0) {
     // ---- TMA producer: activation tiles (+ weight tiles for FP16 / INT8)
     for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
+      const int s = kb % C::kStages;
+      const uint32_t ph = (kb / C::kStages) & 1;
       mbar_wait(&empty[s], ph ^ 1);
       mbar_expect_tx(&full[s], C::kIsW4 ? C::kBBytes : C::kABytes + C::kBBytes);
       if (!C::kIsW4) tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * C::kTileK, n0);
@@ -220,8 +237,8 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     // ---- MMA issuer
     constexpr uint32_t idesc = instr_desc<FMT, BN>();
     for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
+      const int s = kb % C::kStages;
+      const uint32_t ph = (kb / C::kStages) & 1;
       mbar_wait(&full[s], ph);
       tc_fence_after();
       const uint32_t a0 = smem_u32(sA + s * C::kABytes);
@@ -254,8 +271,8 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     for (int kb = 0; kb < nk; ++kb) {
       const int ps = kb % kPkStages;
       const uint32_t pph = (kb / kPkStages) & 1;
-      const int s = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
+      const int s = kb % C::kStages;
+      const uint32_t ph = (kb / C::kStages) & 1;
       const half2 s2 = __half2half2(srow[((kb0 + kb) * 64) / kW4Group]);
       mbar_wait(&pfull[ps], pph);
       const uint4* prow = reinterpret_cast<const uint4*>(sP + ps * C::kPkBytes + r * 32);
@@ -324,11 +341,18 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   } else {
     // Deterministic split-K through distributed shared memory: every CTA of
     // the cluster stages its raw partial tile [BN][128] in its own (now idle)
-    // A ring; after a cluster barrier CTA `rank` sums column slice
-    // [rank*BN/ks, (rank+1)*BN/ks) over the ks partials in rank order and runs
-    // the epilogue for it. INT8 partials are int32, so the result is the exact
-    // int32 sum, scaled once. No global workspace, no atomics, no tail CTA.
+    // A ring; after a cluster barrier each CTA pushes column slice r of its
+    // partial to CTA r with one bulk copy (cp.async.bulk smem -> peer smem,
+    // completion on the receiver's mbarrier), and CTA r sums its slice over
+    // the ks partials in rank order and runs the epilogue for it. INT8
+    // partials are int32, so the result is the exact int32 sum, scaled once.
+    // No global workspace, no atomics, no tail CTA.
     uint32_t* red = reinterpret_cast<uint32_t*>(sA);
+    uint32_t* recv = reinterpret_cast<uint32_t*>(sB);  // idle B ring: (ks-1) incoming slices
+    const int cpr = BN / ksplit;  // columns owned per rank (>= 2)
+    const uint32_t slice_bytes = uint32_t(cpr) * kTileM * 4;
+    const int rank = int(cluster_ctarank());
+    if (threadIdx.x == 0) mbar_expect_tx(rbar, uint32_t(ksplit - 1) * slice_bytes);
     if (warp < 4) {
 #pragma unroll 1
       for (int j0 = 0; j0 < BN; j0 += 16) {
@@ -338,29 +362,28 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
         for (int j = 0; j < 16; ++j) red[(j0 + j) * kTileM + row] = nk > 0 ? r[j] : 0u;
       }
     }
-    cluster_sync_all();
+    fence_async_smem();  // generic stores -> visible to the bulk-copy (async) proxy
+    cluster_sync_all();  // partials staged, every CTA's mainloop done, receivers armed
+    if (threadIdx.x == 0) {
+      for (int r = 0; r < ksplit; ++r) {
+        if (r == rank) continue;
+        const int idx = rank < r ? rank : rank - 1;  // this CTA's slot among r's senders
+        bulk_s2s_peer(recv + size_t(idx) * cpr * kTileM, red + size_t(r) * cpr * kTileM,
+                      slice_bytes, rbar, uint32_t(r));
+      }
+    }
     if (warp < 4) {
-      const int rank = int(cluster_ctarank());
-      const int cols = BN / ksplit;  // >= 2
-      // 8 columns x every split's partial in flight per batch (DSMEM latency)
+      mbar_wait(rbar, 0);
 #pragma unroll 1
-      for (int c0 = 0; c0 < cols; c0 += 8) {
-        uint32_t u[8][kMaxSplit];
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj)
-#pragma unroll
-          for (int z = 0; z < kMaxSplit; ++z)
-            if (c0 + jj < cols && z < ksplit)
-              u[jj][z] = ld_dsmem(&red[(rank * cols + c0 + jj) * kTileM + row], uint32_t(z));
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          if (c0 + jj >= cols) break;  // warp-uniform
-          Acc32 a = 0;
-#pragma unroll
-          for (int z = 0; z < kMaxSplit; ++z)
-            if (z < ksplit) a += FMT == kINT8 ? Acc32(int(u[jj][z])) : Acc32(__uint_as_float(u[jj][z]));
-          emit(rank * cols + c0 + jj, FMT == kINT8 ? uint32_t(int(a)) : __float_as_uint(float(a)));
+      for (int c = 0; c < cpr; ++c) {
+        Acc32 a = 0;
+        for (int z = 0; z < ksplit; ++z) {
+          const uint32_t u = z == rank ? red[(rank * cpr + c) * kTileM + row]
+                                       : recv[((z < rank ? z : z - 1) * cpr + c) * kTileM + row];
+          if (FMT == kINT8) a += Acc32(int(u));
+          else a += Acc32(__uint_as_float(u));
         }
+        emit(rank * cpr + c, FMT == kINT8 ? uint32_t(int(a)) : __float_as_uint(float(a)));
       }
     }
     cluster_sync_all();  // peers have read this CTA's partials before it exits
@@ -414,26 +437,16 @@ CUtensorMap make_sw128_map(const void* base, int elt_bytes, uint64_t rows, uint6
                   elt_bytes, rows, k, box_rows, kTileKBytes, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// Split-K factor: the number of CTAs per output tile (a cluster along z) that
-// best fills the resident CTA slots. Tiles x ks CTAs over `slots` resident
-// CTAs: efficiency = work / (slots * waves). A split must keep >= 4 k-tiles.
+// Split-K factor: only when the output tiles fill less than half of the
+// resident CTA slots (a continuous-batching step, a short prefill of a
+// 4096-row projection), split K over the largest power of two (<= 8, each
+// split keeping >= 8 k-tiles) that keeps the CTAs within one wave. Fuller
+// grids run unsplit: short-lived split CTAs cost more in pipeline fill and
+// reduction than the wave tail they save.
 int choose_split(int tiles, int nk, int slots) {
-  auto eff = [&](int ks) {
-    const long long ctas = (long long)tiles * ks;
-    const long long waves = (ctas + slots - 1) / slots;
-    return double(ctas) / double(waves * slots);
-  };
-  int best = 1;
-  double best_e = eff(1);
-  for (int ks = 2; ks <= kMaxSplit; ks *= 2) {
-    if (nk / ks < 4) break;
-    const double e = eff(ks);
-    if (e > best_e + 0.05) {
-      best = ks;
-      best_e = e;
-    }
-  }
-  return best;
+  int ks = 1;
+  while (ks < kMaxSplit && tiles * ks * 2 <= slots && nk / (ks * 2) >= 8) ks *= 2;
+  return ks;
 }
 
 template <int FMT, int BN, int EPI>
