@@ -361,8 +361,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tile = tile_begin + i;
       // 128 (row, col) values; lane handles rows 2*(lane>>3)+{0,1} (a pair), col lane & 7,
       // for row pairs lane>>3 in {0..3} and +4 in a second pass
+      if (NT == 1) {
+        // one token: compact [warp][16] column-0 partials; lane (row pair rp,
+        // quarter q) sums a quarter of the active warps, then a fixed 4-lane
+        // shuffle tree (integer sums stay exact)
+        const uint32_t* p1 = &part[b][0][0][0];
+        const int rp = lane >> 2, q = lane & 3;
+        const int row = 2 * rp;
+        Acc a0 = 0, a1 = 0;
+        for (int w2 = q; w2 < ACTIVE; w2 += 4) {
+          if (FMT == kINT8) {
+            a0 += Acc(int(p1[w2 * 16 + row]));
+            a1 += Acc(int(p1[w2 * 16 + row + 1]));
+          } else {
+            a0 += Acc(__uint_as_float(p1[w2 * 16 + row]));
+            a1 += Acc(__uint_as_float(p1[w2 * 16 + row + 1]));
+          }
+        }
+        a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+        a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+        if (q == 0) {
+          if (FMT == kINT8 && EPI == kEpiRaw) {
+            reinterpret_cast<int*>(y)[tile * 16 + row] = int(a0);
+            reinterpret_cast<int*>(y)[tile * 16 + row + 1] = int(a1);
+          } else {
+            float v0 = float(a0), v1 = float(a1);
+            if (FMT == kINT8) {
+              const int lrr = i * 16 + row;
+              v0 = (v0 * xscale[0]) * sc_f[lrr];
+              v1 = (v1 * xscale[0]) * sc_f[lrr + 1];
+            }
+            store_pair<EPI>(y, n, 0, tile * 16 + row, v0, v1);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tile_free[b]);
+        continue;
+      }
 #pragma unroll
-      for (int pass = 0; pass < 2; ++pass) {
+      for (int pass = 0; pass < (NT == 1 ? 0 : 2); ++pass) {
         const int rp = (lane >> 3) + pass * 4;  // row pair 0..7
         const int col = lane & 7;
         const int row = 2 * rp;
@@ -501,17 +540,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp < ACTIVE) {
         const int b = ti & 1;
         if (ti >= 2) mbar_wait(&tile_free[b], ((ti >> 1) - 1) & 1);  // epilogue drained it
-        uint32_t* pw = &part[b][warp][0][0];
         uint32_t r4[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const Acc tot = acc[i] + acc2[i];
           r4[i] = FMT == kINT8 ? uint32_t(int(tot)) : __float_as_uint(float(tot));
         }
-        pw[g * 8 + 2 * tq] = r4[0];
-        pw[g * 8 + 2 * tq + 1] = r4[1];
-        pw[(g + 8) * 8 + 2 * tq] = r4[2];
-        pw[(g + 8) * 8 + 2 * tq + 1] = r4[3];
+        if (NT == 1) {  // column 0 only: lanes tq == 0 hold rows g and g + 8
+          uint32_t* p1 = &part[b][0][0][0] + warp * 16;
+          if (tq == 0) {
+            p1[g] = r4[0];
+            p1[g + 8] = r4[2];
+          }
+        } else {
+          uint32_t* pw = &part[b][warp][0][0];
+          pw[g * 8 + 2 * tq] = r4[0];
+          pw[g * 8 + 2 * tq + 1] = r4[1];
+          pw[(g + 8) * 8 + 2 * tq] = r4[2];
+          pw[(g + 8) * 8 + 2 * tq + 1] = r4[3];
+        }
         // each lane's arrive releases its OWN partial stores: a lane-0 arrive after
         // __syncwarp() let the epilogue read other lanes' stale partials
         // (~5-30% of 6-token K=14336 runs, scripts/repro_gemv_t6.py)
@@ -622,17 +669,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b = i & 1;
       mbar_wait(&tile_full[b], (i >> 1) & 1);
       const int tile = tile_begin + i;
-#pragma unroll
-      for (int pass = 0; pass < 2; ++pass) {
-        const int row = 2 * ((lane >> 3) + pass * 4);
-        const int col = lane & 7;
+      if (NT == 1) {
+        // one token: only column 0 exists (compact [warp][16] partials). Lane
+        // (row pair rp, quarter q) sums warps 4q..4q+3 of rows 2rp, 2rp+1, and
+        // a 4-lane shuffle tree finishes the 16-warp sum (fixed order)
+        const float* p1 = &part[b][0][0][0];
+        const int rp = lane >> 2, q = lane & 3;
         float v0 = 0.f, v1 = 0.f;
 #pragma unroll
-        for (int w2 = 0; w2 < kConsumers; ++w2) {
-          v0 += part[b][w2][row][col];
-          v1 += part[b][w2][row + 1][col];
+        for (int i2 = 0; i2 < kConsumers / 4; ++i2) {
+          v0 += p1[(q * (kConsumers / 4) + i2) * 16 + 2 * rp];
+          v1 += p1[(q * (kConsumers / 4) + i2) * 16 + 2 * rp + 1];
         }
-        if (col < T) store_pair<EPI>(y, n, col, tile * 16 + row, v0, v1);
+        v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+        v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+        if (q == 0) store_pair<EPI>(y, n, 0, tile * 16 + 2 * rp, v0, v1);
+      } else {
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          const int row = 2 * ((lane >> 3) + pass * 4);
+          const int col = lane & 7;
+          float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+          for (int w2 = 0; w2 < kConsumers; ++w2) {
+            v0 += part[b][w2][row][col];
+            v1 += part[b][w2][row + 1][col];
+          }
+          if (col < T) store_pair<EPI>(y, n, col, tile * 16 + row, v0, v1);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_free[b]);
@@ -689,9 +755,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto flush = [&](int ti) {
     const int b = ti & 1;
     if (ti >= 2) mbar_wait(&tile_free[b], ((ti >> 1) - 1) & 1);
-    float* pw = &part[b][warp][0][0];
-    *reinterpret_cast<float2*>(pw + g * 8 + 2 * tq) = make_float2(acc[0], acc[1]);
-    *reinterpret_cast<float2*>(pw + (g + 8) * 8 + 2 * tq) = make_float2(acc[2], acc[3]);
+    if (NT == 1) {  // column 0 only: lanes tq == 0 hold rows g and g + 8
+      float* p1 = &part[b][0][0][0] + warp * 16;
+      if (tq == 0) {
+        p1[g] = acc[0];
+        p1[g + 8] = acc[2];
+      }
+    } else {
+      float* pw = &part[b][warp][0][0];
+      *reinterpret_cast<float2*>(pw + g * 8 + 2 * tq) = make_float2(acc[0], acc[1]);
+      *reinterpret_cast<float2*>(pw + (g + 8) * 8 + 2 * tq) = make_float2(acc[2], acc[3]);
+    }
     mbar_arrive(&tile_full[b]);  // per-lane release of its own stores (see gemv_tf_kernel)
     acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
   };
