@@ -36,6 +36,7 @@ def lib() -> C.CDLL:
         L.orc_quant_w4_rows.argtypes = [vp, i32, i32, vp, vp]
         L.orc_gemv_i8_acc.argtypes = [vp, vp, i32, i32, vp]
         L.orc_linear.argtypes = [C.c_int, vp, vp, i32, i32, vp, i32, vp]
+        L.orc_model_tensor.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp]
         _lib = L
     return _lib
 
@@ -73,6 +74,34 @@ class OracleModel:
 
     def successor(self, t: int) -> int:
         return lib().orc_successor(self.h, int(t))
+
+    # tensor ids of orc_model_tensor (oracle_model.h)
+    EMBED, LM_HEAD, FINAL_NORM, ATTN_NORM, FFN_NORM, QKV, O, GATE, UP, DOWN = range(10)
+
+    def tensor(self, which: int, layer: int = 0, fmt: int = 0):
+        """One weight tensor: fp16 array (fmt 0 / norms / embed / lm_head), or
+        (q int8 [n,k], s fp32 [n]) for fmt 1, (q nibble-per-byte [n,k], s fp16
+        [n,k/128]) for fmt 2."""
+        c = self.cfg
+        H, V, F, D = c.hidden, c.vocab, c.ffn, c.head_dim
+        if which in (self.EMBED, self.LM_HEAD):
+            shape = (V, H)
+        elif which in (self.FINAL_NORM, self.ATTN_NORM, self.FFN_NORM):
+            shape = (H,)
+        else:
+            shape = {self.QKV: ((c.n_heads + 2 * c.n_kv_heads) * D, H), self.O: (H, c.n_heads * D),
+                     self.GATE: (F, H), self.UP: (F, H), self.DOWN: (H, F)}[which]
+        if which < self.QKV or fmt == 0:
+            w = np.zeros(shape, np.float16)
+            s = None
+        elif fmt == 1:
+            w, s = np.zeros(shape, np.int8), np.zeros(shape[0], np.float32)
+        else:
+            w, s = np.zeros(shape, np.uint8), np.zeros((shape[0], shape[1] // 128), np.float16)
+        rc = lib().orc_model_tensor(self.h, which, layer, fmt, _p(w), _p(s) if s is not None else None)
+        if rc != 0:
+            raise RuntimeError(f"orc_model_tensor({which}, {layer}, {fmt}) not resident")
+        return w if s is None else (w, s)
 
 
 def spec_generate(target: OracleModel, draft: OracleModel, k: int, prompt, n_new: int,

@@ -454,6 +454,29 @@ void orc_model_destroy(orc_model* m) {
 }
 
 int32_t orc_successor(orc_model* m, int32_t t) { return m->succ[t]; }
+
+int orc_model_tensor(orc_model* m, int which, int layer, int fmt, void* w, void* s) {
+  const int64_t H = m->c.hidden, V = m->c.vocab;
+  if (which <= 2) {
+    const h16* src = which == 0 ? m->embed : (which == 1 ? m->lm_head : m->final_norm);
+    memcpy(w, src, sizeof(h16) * (size_t)(which == 2 ? H : V * H));
+    return 0;
+  }
+  if (layer < 0 || layer >= m->c.n_layers) return -1;
+  const orc_layer* ly = &m->layers[layer];
+  if (which == 3 || which == 4) {
+    memcpy(w, which == 3 ? ly->attn_norm : ly->ffn_norm, sizeof(h16) * (size_t)H);
+    return 0;
+  }
+  const orc_lin* L = which == 5 ? &ly->qkv : which == 6 ? &ly->o : which == 7 ? &ly->gate
+                   : which == 8 ? &ly->up : which == 9 ? &ly->down : NULL;
+  if (!L || fmt < 0 || fmt > 2 || !L->w[fmt]) return -1;
+  const size_t nk = (size_t)L->n * L->k;
+  memcpy(w, L->w[fmt], fmt == 0 ? sizeof(h16) * nk : nk);
+  if (fmt == 1) memcpy(s, L->s[1], sizeof(float) * (size_t)L->n);
+  if (fmt == 2) memcpy(s, L->s[2], sizeof(h16) * (size_t)L->n * (L->k / MSW_W4_GROUP));
+  return 0;
+}
 int orc_threads(void) { return omp_get_max_threads(); }
 
 /* y = x * rsqrt(mean(x^2) + eps) * g, fp32 (sum in double) */
