@@ -164,3 +164,24 @@ def test_int8_split_k_linear_deterministic(cuda_ok):
     for o in outs[1:]:
         assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
     assert np.array_equal(outs[0], O.linear(_capi.W_INT8, q8, s8, x))
+
+
+@pytest.mark.parametrize("n,k", [(4096, 4096), (6144, 4096), (4096, 14336), (2400, 4096)])
+def test_w4_decode_balanced_ranges(cuda_ok, n, k):
+    """Batch-1 W4 decode GEMV at 8B shapes (o, qkv, down, and an n where tiles
+    do not divide evenly): with >= 148 tiles each CTA streams a chunk-balanced
+    range and tiles straddling two CTAs are finished by the second one to
+    arrive. Within the W4 bar of the oracle and bitwise identical across
+    repeated launches (the two-part fp32 sum is order-independent)."""
+    torch = _torch()
+    w = O.fill_fp16(n, k, 3, 777 + n + k, (int(np.ceil(np.log2(k))) + 1) // 2)
+    q4, s4 = O.quant_w4_rows(w)
+    packed = _pack_w4_host(q4)
+    dw = torch.from_numpy(packed.view(np.int32)).cuda()
+    ds = torch.from_numpy(s4.view(np.int16)).cuda()
+    x = np.random.default_rng(n + k).standard_normal((1, k)).astype(np.float32)
+    outs = [_run_linear(_capi.W_W4, dw, ds, n, k, x) for _ in range(6)]
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+    ref = O.linear(_capi.W_W4, q4, s4, x)
+    assert np.abs(outs[0] - ref).max() / np.abs(ref).max() < 2e-3
