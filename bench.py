@@ -411,14 +411,15 @@ def run_mix(args):
     from paper_2605_23057_b200.dispatch import aggregate_rows, shard_trace
     text = deploy_mix_trace(args.mix_per_class)
     lines = text.splitlines()
-    my_idx = shard_trace(text, ws)[rank]  # cohorts whole, prefix group sticky, least-loaded
+    # cohorts whole, prefix groups sticky, longest-predicted-first onto the least-loaded GPU
+    my_idx = shard_trace(text, ws, prefix_groups=args.prefix_groups)[rank]
     mine = "".join(lines[i] + "\n" for i in my_idx)
     execute_trace(eng, "\n".join(lines[:2]) + "\n", max_output_tokens=4)  # warm-up (graphs, attrs)
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rows, summ = execute_trace(eng, mine, prefix_len=768)
+    rows, summ = execute_trace(eng, mine, prefix_len=768, prefix_groups=args.prefix_groups)
     wall = time.perf_counter() - t0
     vals = torch.tensor([summ["generated_tokens"], summ["mode_time_ms"], wall], dtype=torch.float64,
                         device="cuda")
@@ -459,32 +460,121 @@ def run_mix(args):
             "aggregate_latency_speedup": agg["aggregate_latency_speedup"],
             "collapsed_mean_speedup": agg["collapsed_mean_speedup"],
             "per_family_mean_speedup": agg["per_family_mean_speedup"], "per_mode_rank0": per_mode,
-            "placement": "CB cohorts whole per GPU, prefix group sticky, least outstanding tokens",
+            "placement": f"CB cohorts whole per GPU, {args.prefix_groups} sticky prefix groups, LPT on the "
+                         "B200-measured cost model (dispatch.py)",
             "scaling": "weak", "data": "synthetic", "wall_s": vals[2].item()}), flush=True)
     eng.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
 
 
+# ---- per-config rooflines -----------------------------------
+def linear_params(cfg) -> int:
+    """Weights of every linear of one forward (QKV, O, gate/up, down x layers + lm_head)."""
+    h, f, d = cfg.hidden, cfg.ffn, cfg.head_dim
+    qkv = h * (cfg.n_heads + 2 * cfg.n_kv_heads) * d
+    return cfg.n_layers * (qkv + cfg.n_heads * d * h + 2 * h * f + f * h) + cfg.vocab * h
+
+
+def kv_bytes_per_pos(cfg) -> int:
+    return 2 * cfg.n_layers * cfg.n_kv_heads * cfg.head_dim * 2
+
+
+def prefill_flops(cfg, t: int, ctx0: int = 0) -> float:
+    """2 * linear params * t + causal attention (QK and PV) over positions
+    ctx0 .. ctx0 + t - 1."""
+    att = 0.0
+    if t > 0:  # sum over query positions p of (p + 1) keys, QK + PV = 4 * Hq * D per key
+        att = 4.0 * cfg.n_layers * cfg.n_heads * cfg.head_dim * (t * ctx0 + t * (t + 1) / 2)
+    return 2.0 * linear_params(cfg) * t + att
+
+
+def tensor_peak(kind: str) -> tuple[float, str]:
+    """Dense TFLOP/s for the prefill floor: MEASURED_PEAKS bf16 sustained (a
+    long step); int8 = 2x that (the B200's nominal int8:bf16 dense ratio)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        bf = float(p.get("bf16_tflops_sustained") or p["bf16_tflops"])
+        src = "measured bf16 sustained"
+    except Exception:
+        bf, src = 1400.0, "fallback"
+    return (2.0 * bf, src + " x2 (int8)") if kind == "int8" else (bf, src)
+
+
+def cpu_mode_sample(mode: int, cfg_name: str = "llama8b", prompt_len: int = 4, new_tokens: int = 3,
+                    draft: str | None = None, k: int = 4):
+    """The CPU oracle (C port, OpenMP over all host cores) running one mode's
+    arithmetic on a bounded sample of the config (8B shape): tokens/s of full
+    forwards, and the host-DRAM bytes/s the oracle's storage implies (fp16 2 B,
+    int8 1 B, W4 one nibble per byte: 1 B per weight)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # checker / baseline only
+    from paper_2605_23057_b200.configs import model_cfg
+    cfg = model_cfg(cfg_name)
+    fmt = {0: 0, 1: 1, 2: 2, 4: 0, 10: 2, 11: 1}[mode]
+    omode = {0: 0, 1: 1, 2: 2, 4: 0, 10: 2, 11: 1}[mode]
+    t0 = time.perf_counter()
+    m = O.OracleModel(cfg, seed=0, modes_mask=1 << omode, max_ctx=prompt_len + new_tokens + 16)
+    d = None
+    if draft:
+        d = O.OracleModel(model_cfg(draft), seed=0, is_draft=True, modes_mask=1, max_ctx=prompt_len + new_tokens + 16)
+    t_init = time.perf_counter() - t0
+    p = synth_prompt(5, prompt_len, cfg.vocab)
+    t0 = time.perf_counter()
+    if d is not None:
+        _, _, st = O.spec_generate(m, d, k, p, new_tokens)
+    else:
+        m.generate(omode, p, new_tokens)
+    dt = time.perf_counter() - t0
+    m.close()
+    if d is not None:
+        d.close()
+    bpw = {0: 2.0, 1: 1.0, 2: 1.0}[fmt]
+    if draft:  # per emitted token: the rounds' draft + target forwards
+        from paper_2605_23057_b200.configs import model_cfg as mc
+        fw = prompt_len + st["rounds"] * (k + 1)  # target verify tokens (approx. forwards)
+        sample = (f"{cfg_name} FP16 target + {draft} draft, k={k}: {prompt_len}-token prompt, "
+                  f"{new_tokens} tokens, {st['rounds']} rounds in {dt:.1f} s")
+        return {"value": new_tokens / dt, "unit": "tokens/s", "cores": O.lib().orc_threads(),
+                "kind": "port", "sample": sample, "init_s": round(t_init, 1)}
+    forwards = prompt_len + new_tokens - 1
+    host_gbs = forwards * linear_params(cfg) * bpw / dt / 1e9
+    return {"value": forwards / dt, "unit": "tokens/s (full forwards)", "cores": O.lib().orc_threads(),
+            "kind": "port", "host_dram_gbs": round(host_gbs, 1),
+            "sample": f"{cfg_name} mode {mode} arithmetic: {prompt_len}-token prompt + {new_tokens} new "
+                      f"tokens ({forwards} forwards, {dt:.1f} s; weight init {t_init:.1f} s excluded)"}
+
+
 def run_configs(args):
     """BASELINE configs 3a (GPTQ + prefix caching), 3b (INT8 + continuous
     batching, ragged batch 64) and 4 (speculative decoding, 1B draft + 8B
-    target, k=4) on one GPU, through the C ABI. One JSON line per config."""
+    target, k=4) on one GPU, through the C ABI. One JSON line per config, each
+    with its roofline (the algorithmic floor: HBM bytes / measured HBM peak +
+    prefill FLOPs / tensor peak, against the measured time) and the CPU
+    oracle's rate on a bounded sample of the same arithmetic."""
     import numpy as np
     import torch
-    from paper_2605_23057_b200 import MODE_GPTQ_PC, MODE_INT8_CB, MODE_SPEC, engine_cfg
+    from paper_2605_23057_b200 import MODE_FP16, MODE_GPTQ_PC, MODE_INT8_CB, MODE_SPEC, engine_cfg
+    from paper_2605_23057_b200.configs import model_cfg
     from paper_2605_23057_b200.engine import Engine
     torch.cuda.set_device(0)
     eng = Engine(engine_cfg(target="llama8b", draft="llama1b", seed=0, kv_blocks=6144, max_batch=64,
                             max_seq_len=2400, use_graphs=True))
+    c8, c1 = model_cfg("llama8b"), model_cfg("llama1b")
+    hbm, _ = peaks()
+    kvp = kv_bytes_per_pos(c8)
     rng = np.random.default_rng(7)
+    cpu = not args.no_cpu_baseline
     base = {"metric": "decode tokens/s per mode and routed mix (1/2/4/8 B200); mean latency vs FP16 mode",
             "unit": "tokens/s", "n_gpus": 1, "data": "synthetic"}
     # 3a: shared-prefix chat, 1024+-10% prompts with a shared 768-token prefix, 128+-10% outputs
     shared = synth_prompt(99, 768, 128256)
     n_req = args.cfg_requests
     eng.reset_prefix_cache()
-    tot_tok, tot_ms, hits = 0, 0.0, 0
+    wb4 = eng.weight_bytes(2)
+    tot_tok, tot_ms, dec_ms, pre_ms, hits, floor_dec, floor_pre = 0, 0.0, 0.0, 0.0, 0, 0.0, 0.0
+    tp16, _ = tensor_peak("f16")
     for i in range(n_req):
         plen = int(round(1024 * (0.9 + 0.2 * rng.random())))
         p = np.concatenate([shared, synth_prompt(1000 + i, plen - 768, 128256)])
@@ -492,10 +582,22 @@ def run_configs(args):
         r = eng.run(MODE_GPTQ_PC, p, out)
         tot_tok += out
         tot_ms += r.total_ms
+        dec_ms += r.decode_ms
+        pre_ms += r.prefill_ms
         hits += r.prefix_hit_tokens
-    print(json.dumps(dict(base, config="3a_gptq_prefix_caching", value=tot_tok / (tot_ms / 1e3),
-                          requests=n_req, prefix_hit_tokens=hits,
-                          mean_request_ms=tot_ms / n_req)), flush=True)
+        sfx = plen - r.prefix_hit_tokens
+        floor_pre += prefill_flops(c8, sfx, r.prefix_hit_tokens) / (tp16 * 1e12) * 1e3
+        floor_dec += sum(wb4 + (plen + j) * kvp for j in range(out - 1)) / (hbm * 1e9) * 1e3
+    line = dict(base, config="3a_gptq_prefix_caching", value=tot_tok / (tot_ms / 1e3),
+                requests=n_req, prefix_hit_tokens=hits, mean_request_ms=tot_ms / n_req,
+                decode_tok_s=(tot_tok - n_req) / (dec_ms / 1e3),
+                roofline={"bound": "hbm (decode) + tensor (suffix prefill)",
+                          "decode_frac": floor_dec / dec_ms, "prefill_frac": floor_pre / pre_ms,
+                          "request_frac": (floor_dec + floor_pre) / tot_ms,
+                          "peaks": {"hbm_gbs": hbm, "tensor_tflops": tp16}})
+    if cpu:
+        line["cpu_baseline"] = cpu_mode_sample(2)
+    print(json.dumps(line), flush=True)
     # 3b: 64 co-scheduled requests, prompts 1024+-10%, outputs 128+-10%, INT8 + continuous batching
     prompts, outs = [], []
     for i in range(64):
@@ -503,24 +605,62 @@ def run_configs(args):
         prompts.append(synth_prompt(2000 + i, plen, 128256))
         outs.append(int(round(128 * (0.9 + 0.2 * rng.random()))))
     eng.run_batch(MODE_INT8_CB, prompts[:4], [4] * 4)  # warm-up
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = eng.run_batch(MODE_INT8_CB, prompts, outs)
     wall = time.perf_counter() - t0
-    print(json.dumps(dict(base, config="3b_int8_continuous_batching_b64", value=sum(outs) / wall,
-                          requests=64, generated_tokens=sum(outs), wall_s=wall,
-                          mean_request_ms=statistics.mean(r.total_ms for r in res))), flush=True)
-    # 4: speculative decoding on long generations (SyntheticSL-shape prompt, 1024 new tokens)
-    tot_tok, tot_dec, prop, acc = 0, 0.0, 0, 0
+    wb8 = eng.weight_bytes(1)
+    tpi8, i8src = tensor_peak("int8")
+    pre_wall = max(r.prefill_ms for r in res)  # one packed admission prefill of all 64
+    steps = max(outs) - 1
+    dec_bytes = 0.0
+    for s_ in range(1, steps + 1):  # step s: every sequence with more than s tokens to emit
+        live = [len(pr) + s_ for pr, o in zip(prompts, outs) if o > s_]
+        dec_bytes += wb8 + sum(live) * kvp
+    floor_pre = sum(prefill_flops(c8, len(pr)) for pr in prompts) / (tpi8 * 1e12) * 1e3
+    floor_dec = dec_bytes / (hbm * 1e9) * 1e3
+    line = dict(base, config="3b_int8_continuous_batching_b64", value=sum(outs) / wall,
+                requests=64, generated_tokens=sum(outs), wall_s=wall, prefill_ms=pre_wall,
+                decode_ms=wall * 1e3 - pre_wall,
+                mean_request_ms=statistics.mean(r.total_ms for r in res),
+                roofline={"bound": "tensor (packed 64 x ~1024 prefill) + hbm (decode steps: INT8 "
+                                   "weights + every live sequence's KV)",
+                          "prefill_floor_ms": floor_pre, "decode_floor_ms": floor_dec,
+                          "prefill_frac": floor_pre / pre_wall,
+                          "decode_frac": floor_dec / max(1e-9, wall * 1e3 - pre_wall),
+                          "frac": (floor_pre + floor_dec) / (wall * 1e3),
+                          "peaks": {"hbm_gbs": hbm, "int8_tops": tpi8, "int8_source": i8src}})
+    if cpu:
+        line["cpu_baseline"] = cpu_mode_sample(1)
+    print(json.dumps(line), flush=True)
+    # 4: speculative decoding on long generations (SyntheticSL-shape prompt, 1024 new tokens),
+    # against FP16 batch-1 on the same requests
+    wb16, wbd = eng.weight_bytes(0), 2 * linear_params(c1)
+    tot_tok, tot_dec, tot16, prop, acc, rounds = 0, 0.0, 0.0, 0, 0, 0
     for i in range(args.cfg_requests // 4 or 1):
         p = synth_prompt(3000 + i, 128, 128256)
         r = eng.run(MODE_SPEC, p, 1024)
+        r16 = eng.run(MODE_FP16, p, 1024)
+        assert np.array_equal(r.tokens, r16.tokens), "speculative tokens != FP16 greedy tokens"
         tot_tok += 1023
         tot_dec += r.decode_ms
+        tot16 += r16.decode_ms
         prop += r.spec_proposed
         acc += r.spec_accepted
-    print(json.dumps(dict(base, config="4_speculative_k4", value=tot_tok / (tot_dec / 1e3),
-                          acceptance=acc / max(1, prop), draft="llama1b-shape", target="llama8b-shape")),
-          flush=True)
+        rounds += r.spec_rounds
+    k = 4
+    # per round: the draft's k forwards (T=2 catch-up + k-1 steps) and one target verify of k+1 tokens
+    floor = rounds * (k * wbd + wb16) / (hbm * 1e9) * 1e3
+    line = dict(base, config="4_speculative_k4", value=tot_tok / (tot_dec / 1e3),
+                acceptance=acc / max(1, prop), rounds=rounds,
+                tokens_per_round=tot_tok / max(1, rounds), fp16_tok_s=tot_tok / (tot16 / 1e3),
+                speedup_vs_fp16=tot16 / tot_dec, draft="llama1b-shape", target="llama8b-shape",
+                roofline={"bound": "hbm", "bytes_per_round": k * wbd + wb16,
+                          "frac": floor / tot_dec, "peak_gbs": hbm,
+                          "token_ceiling_tok_s": tot_tok / (floor / 1e3)})
+    if cpu:
+        line["cpu_baseline"] = cpu_mode_sample(4, prompt_len=4, new_tokens=6, draft="llama1b")
+    print(json.dumps(line), flush=True)
     eng.close()
 
 
@@ -560,6 +700,7 @@ def main():
     ap.add_argument("--profile-out-cap", type=int, default=0, help="cap generated tokens per request")
     ap.add_argument("--cfg-requests", type=int, default=8)
     ap.add_argument("--mix-per-class", type=int, default=4)
+    ap.add_argument("--prefix-groups", type=int, default=8, help="mix: shared-prefix groups")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)

@@ -38,6 +38,17 @@ struct RoutingDecision {
   double overhead_ms = 0.0;  // wall-clock cost of the decision itself
 };
 
+// Feasibility envelope (reference routing.hpp:38-47): quality is a one-sided
+// floor, energy and memory one-sided caps. The executor checks every executed
+// request's measured ratios against it (SimRequestResult::constraint_violated).
+struct ConstraintSet {
+  double quality_floor_pp = -1.5;
+  double energy_ratio_max = 1.0;
+  double memory_ratio_max = 1.10;
+};
+
+void validate(const ConstraintSet& constraints);
+
 // Seven ordered rules (reference routing.cpp:63-100). Never returns FP16.
 RoutingDecision route_rule(const RequestDescriptor& request, WorkloadClass cls,
                            const ClassifierConfig& config);

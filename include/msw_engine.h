@@ -121,6 +121,12 @@ const char* msw_last_error(void);
 /* Resident HBM bytes per mode's weights (all linears + lm_head), the
  * algorithmic bytes one batch-1 decode token streams. */
 int msw_engine_weight_bytes(msw_engine* e, int32_t mode, int64_t* bytes);
+/* HBM footprint of serving one request of `tokens` positions in `mode`: the
+ * mode's resident weights (speculative decoding: target FP16 + draft) plus
+ * the request's K/V cache (target, and draft for speculative decoding). The
+ * executor's memory_ratio (reference SimRequestResult::memory_ratio,
+ * sim.hpp:49) is this over the FP16 figure for the same request. */
+int msw_engine_memory_bytes(msw_engine* e, int32_t mode, int32_t tokens, int64_t* bytes);
 /* Drops every cached prefix block (prefix caching) and resets counters. */
 int msw_engine_reset_prefix_cache(msw_engine* e);
 

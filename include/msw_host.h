@@ -100,6 +100,15 @@ typedef struct msw_exec_opts {
   int32_t max_output_tokens; /* > 0 caps generation */
   int32_t max_prompt_tokens; /* > 0 caps prompts */
   int32_t cohort_max;        /* continuous-batching cohort size (64) */
+  /* reference ConstraintSet (routing.hpp:41-45): violation accounting */
+  double quality_floor_pp;   /* -1.5 */
+  double energy_ratio_max;   /* 1.0 */
+  double memory_ratio_max;   /* 1.10 */
+  int32_t power_device;      /* >= 0: measure energy per request on this CUDA device */
+  const double* quality_delta_pp; /* [12] per InferenceMode value, or NULL (all 0) */
+  const char* results_csv;    /* optional: per-request SimRequestResult fields */
+  const char* comparison_csv; /* optional: the reference's comparison.csv (report.cpp:83-111) */
+  int32_t prefix_groups;      /* shared-prefix groups (<= 1: one group) */
 } msw_exec_opts;
 
 typedef struct msw_exec_row {
@@ -119,6 +128,12 @@ typedef struct msw_exec_row {
   double overhead_ms;
   double prefill_ms;
   double decode_ms;
+  /* reference SimRequestResult (sim.hpp:48-53), measured */
+  double energy_j;       /* -1 when energy is not measured */
+  double energy_ratio;
+  double memory_ratio;
+  double quality_delta_pp;
+  int32_t constraint_violated;
 } msw_exec_row;
 
 typedef struct msw_exec_summary {
@@ -130,6 +145,13 @@ typedef struct msw_exec_summary {
   double mean_overhead_ms;
   double mode_time_ms;
   int64_t generated_tokens;
+  double mean_energy_ratio;
+  double mean_memory_ratio;
+  double mean_quality_delta_pp;
+  double collapsed_mean_energy_ratio;
+  double constraint_violation_rate;
+  int32_t quality_gate_passed;          /* evaluate_quality_gate (sim.cpp:265-296), 1.5 pp */
+  double collapsed_benchmark_delta_pp;
 } msw_exec_summary;
 
 /* Routes (RulePolicy, cfg NULL = defaults) and executes every request of an

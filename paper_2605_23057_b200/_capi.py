@@ -83,6 +83,10 @@ class ExecOpts(C.Structure):
         ("extra_overhead_ms", C.c_double), ("measure_fp16_baseline", C.c_int32),
         ("token_seed", C.c_uint64), ("prefix_len", C.c_int32), ("max_output_tokens", C.c_int32),
         ("max_prompt_tokens", C.c_int32), ("cohort_max", C.c_int32),
+        ("quality_floor_pp", C.c_double), ("energy_ratio_max", C.c_double),
+        ("memory_ratio_max", C.c_double), ("power_device", C.c_int32),
+        ("quality_delta_pp", C.POINTER(C.c_double)), ("results_csv", C.c_char_p),
+        ("comparison_csv", C.c_char_p), ("prefix_groups", C.c_int32),
     ]
 
 
@@ -94,6 +98,8 @@ class ExecRow(C.Structure):
         ("prefix_hit_tokens", C.c_int32), ("fp16_latency_ms", C.c_double),
         ("mode_latency_ms", C.c_double), ("speedup", C.c_double), ("overhead_ms", C.c_double),
         ("prefill_ms", C.c_double), ("decode_ms", C.c_double),
+        ("energy_j", C.c_double), ("energy_ratio", C.c_double), ("memory_ratio", C.c_double),
+        ("quality_delta_pp", C.c_double), ("constraint_violated", C.c_int32),
     ]
 
 
@@ -102,7 +108,10 @@ class ExecSummary(C.Structure):
         ("request_count", C.c_int32), ("fallback_count", C.c_int32), ("mean_speedup", C.c_double),
         ("aggregate_latency_speedup", C.c_double), ("collapsed_mean_speedup", C.c_double),
         ("mean_overhead_ms", C.c_double), ("mode_time_ms", C.c_double),
-        ("generated_tokens", C.c_int64),
+        ("generated_tokens", C.c_int64), ("mean_energy_ratio", C.c_double),
+        ("mean_memory_ratio", C.c_double), ("mean_quality_delta_pp", C.c_double),
+        ("collapsed_mean_energy_ratio", C.c_double), ("constraint_violation_rate", C.c_double),
+        ("quality_gate_passed", C.c_int32), ("collapsed_benchmark_delta_pp", C.c_double),
     ]
 
 
@@ -132,6 +141,7 @@ def engine_lib() -> C.CDLL:
         lib.msw_engine_destroy.restype = None
         lib.msw_last_error.restype = C.c_char_p
         lib.msw_engine_weight_bytes.argtypes = [vp, i32, C.POINTER(i64)]
+        lib.msw_engine_memory_bytes.argtypes = [vp, i32, i32, C.POINTER(i64)]
         lib.msw_engine_reset_prefix_cache.argtypes = [vp]
         lib.msw_linear.argtypes = [i32, vp, vp, i32, i32, vp, i32, vp, vp]
         lib.msw_gemv_i8_acc.argtypes = [vp, vp, i32, i32, vp, vp]

@@ -1307,6 +1307,24 @@ int msw_engine_weight_bytes(msw_engine* e, int32_t mode, int64_t* bytes) {
   });
 }
 
+int msw_engine_memory_bytes(msw_engine* e, int32_t mode, int32_t tokens, int64_t* bytes) {
+  return guarded([&] {
+    if (!e || !bytes) throw ConfigErr("NULL argument");
+    if (tokens < 0) throw DataErr("tokens must be >= 0");
+    const int fmt = fmt_of_mode(mode);
+    if (!e->target.fmt_on[fmt]) throw ConfigErr("mode not resident");
+    auto kv_pos = [](const Model& m) {
+      return int64_t(2) * m.c.n_layers * m.c.n_kv_heads * m.c.head_dim * 2;  // K + V fp16
+    };
+    int64_t b = int64_t(e->target.weight_bytes(fmt)) + int64_t(tokens) * kv_pos(e->target);
+    if (mode == MSW_MODE_SPECULATIVE) {
+      if (!e->cfg.has_draft) throw ConfigErr("speculative decoding needs a draft model");
+      b += int64_t(e->draft.weight_bytes(kFP16)) + int64_t(tokens) * kv_pos(e->draft);
+    }
+    *bytes = b;
+  });
+}
+
 int msw_engine_reset_prefix_cache(msw_engine* e) {
   return guarded([&] {
     if (!e) throw ConfigErr("NULL argument");

@@ -274,6 +274,11 @@ RoutingDecision route_rule(const RequestDescriptor& r, WorkloadClass cls,
   return d;
 }
 
+void validate(const ConstraintSet& c) {
+  if (!(c.energy_ratio_max > 0.0) || !(c.memory_ratio_max > 0.0))
+    throw ConfigError("constraint caps must be positive");
+}
+
 RoutingDecision route_static(InferenceMode mode) {
   RoutingDecision d;
   d.mode = mode;

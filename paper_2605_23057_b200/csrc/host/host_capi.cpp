@@ -220,6 +220,15 @@ int msw_execute_trace(struct msw_engine* engine, int32_t vocab, const char* ndjs
     o.max_prompt_tokens = opts->max_prompt_tokens;
     o.cohort_max = opts->cohort_max > 0 ? opts->cohort_max : 64;
     o.vocab = vocab;
+    o.constraints.quality_floor_pp = opts->quality_floor_pp;
+    o.constraints.energy_ratio_max = opts->energy_ratio_max;
+    o.constraints.memory_ratio_max = opts->memory_ratio_max;
+    ms::validate(o.constraints);
+    o.power_device = opts->power_device;
+    o.prefix_groups = opts->prefix_groups > 1 ? opts->prefix_groups : 1;
+    if (opts->quality_delta_pp)
+      for (int m = 0; m < ms::kModeCount; ++m)
+        o.quality_delta_pp[static_cast<ms::InferenceMode>(m)] = opts->quality_delta_pp[m];
     const ms::RulePolicy policy(o.classifier);
     const ms::ExecRunResult run = ms::run_policy(trace, policy, engine, o);
     for (size_t i = 0; i < run.results.size(); ++i) {
@@ -241,7 +250,14 @@ int msw_execute_trace(struct msw_engine* engine, int32_t vocab, const char* ndjs
       w.overhead_ms = r.overhead_ms;
       w.prefill_ms = r.prefill_ms;
       w.decode_ms = r.decode_ms;
+      w.energy_j = r.energy_j;
+      w.energy_ratio = r.energy_ratio;
+      w.memory_ratio = r.memory_ratio;
+      w.quality_delta_pp = r.quality_delta_pp;
+      w.constraint_violated = r.constraint_violated;
     }
+    if (opts->results_csv) ms::write_results_csv(run.results, opts->results_csv);
+    if (opts->comparison_csv) ms::write_comparison_csv({run}, opts->comparison_csv);
     if (summary) {
       const auto& p = run.report;
       summary->request_count = p.request_count;
@@ -252,6 +268,14 @@ int msw_execute_trace(struct msw_engine* engine, int32_t vocab, const char* ndjs
       summary->mean_overhead_ms = p.mean_overhead_ms;
       summary->mode_time_ms = p.mode_time_ms;
       summary->generated_tokens = p.generated_tokens;
+      summary->mean_energy_ratio = p.mean_energy_ratio;
+      summary->mean_memory_ratio = p.mean_memory_ratio;
+      summary->mean_quality_delta_pp = p.mean_quality_delta_pp;
+      summary->collapsed_mean_energy_ratio = p.collapsed_mean_energy_ratio;
+      summary->constraint_violation_rate = p.constraint_violation_rate;
+      const ms::ExecQualityGate gate = ms::evaluate_quality_gate(run.results);
+      summary->quality_gate_passed = gate.passed;
+      summary->collapsed_benchmark_delta_pp = gate.collapsed_benchmark_delta_pp;
     }
   });
 }

@@ -118,6 +118,12 @@ class Engine:
         check_engine(engine_lib().msw_engine_weight_bytes(self.h, mode, C.byref(b)))
         return b.value
 
+    def memory_bytes(self, mode: int, tokens: int) -> int:
+        """HBM footprint of one `tokens`-position request in `mode` (weights + KV)."""
+        b = C.c_int64()
+        check_engine(engine_lib().msw_engine_memory_bytes(self.h, mode, tokens, C.byref(b)))
+        return b.value
+
     def reset_prefix_cache(self):
         check_engine(engine_lib().msw_engine_reset_prefix_cache(self.h))
 
@@ -127,16 +133,31 @@ __all__ = ["Engine", "RunResult", "_capi"]
 
 def execute_trace(engine: Engine, ndjson: str, *, token_seed: int = 0, prefix_len: int = 768,
                   max_output_tokens: int = 0, max_prompt_tokens: int = 0, fallback: bool = True,
-                  measure_fp16: bool = True, zero_overhead: bool = False, cohort_max: int = 64):
+                  measure_fp16: bool = True, zero_overhead: bool = False, cohort_max: int = 64,
+                  constraints: tuple[float, float, float] = (-1.5, 1.0, 1.10),
+                  power_device: int = -1, quality_delta_pp: dict[int, float] | None = None,
+                  results_csv: str | None = None, comparison_csv: str | None = None,
+                  prefix_groups: int = 1):
     """Route (RulePolicy) and execute a trace through the C++ executor
-    (libmodeswitch msw_execute_trace). Returns (rows as dicts, summary dict)."""
+    (libmodeswitch msw_execute_trace). constraints = the reference
+    ConstraintSet (quality_floor_pp, energy_ratio_max, memory_ratio_max);
+    power_device >= 0 measures energy per request; quality_delta_pp maps
+    InferenceMode values to the quality delta charged to that mode (the
+    reference profile's cells; random-init weights have no measurable
+    quality). Returns (rows as dicts, summary dict)."""
     from ._capi import ExecOpts, ExecRow, ExecSummary, check_host, host_lib
     n_max = ndjson.count("\n") + 1
     rows = (ExecRow * n_max)()
     n = C.c_int32()
     summ = ExecSummary()
+    qd = None
+    if quality_delta_pp:
+        qd = (C.c_double * 12)(*[float(quality_delta_pp.get(m, 0.0)) for m in range(12)])
     opts = ExecOpts(int(fallback), int(zero_overhead), 0.0, int(measure_fp16), token_seed, prefix_len,
-                    max_output_tokens, max_prompt_tokens, cohort_max)
+                    max_output_tokens, max_prompt_tokens, cohort_max, constraints[0], constraints[1],
+                    constraints[2], power_device, qd,
+                    results_csv.encode() if results_csv else None,
+                    comparison_csv.encode() if comparison_csv else None, prefix_groups)
     check_host(host_lib().msw_execute_trace(engine.h, engine.vocab, ndjson.encode(), None,
                                             C.byref(opts), n_max, rows, C.byref(n), C.byref(summ)))
     out = [{f: getattr(rows[i], f) for f, _ in ExecRow._fields_} for i in range(n.value)]

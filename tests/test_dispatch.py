@@ -12,7 +12,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2605_23057_b200 import controller as ctl
-from paper_2605_23057_b200.dispatch import CB_MODE, PC_MODE, aggregate_rows, rank_trace, shard_trace
+from paper_2605_23057_b200.dispatch import (CB_MODE, PC_MODE, CostModel, aggregate_rows, predicted_load,
+                                            prefix_group, rank_trace, shard_trace)
 
 COUNTS = {"SyntheticSS": 6, "SyntheticSL": 4, "GSM8K": 4, "SharedPrefixChat": 5,
           "MemoryPressureLongContext": 3, "TruthfulQA": 4}
@@ -60,6 +61,57 @@ def test_shard_placement_invariants(world):
     # the shared-prefix group is sticky
     pc = [i for i in range(len(lines)) if routes[i]["mode"] == PC_MODE]
     assert pc and len({owner[i] for i in pc}) == 1
+
+
+def _deploy_mix(per_class):
+    """BASELINE config 5 (bench.py deploy_mix_trace): short interactive, long
+    generation, shared-prefix chat and 8K long-context requests, tagged."""
+    counts = {"SyntheticSS": per_class, "SyntheticSL": per_class, "GSM8K": per_class,
+              "SharedPrefixChat": per_class, "MemoryPressureLongContext": per_class}
+    out = []
+    for line in ctl.generate_trace(counts, jitter=0.10, seed=7).splitlines():
+        d = ctl.parse_trace_line(line)
+        if d["workload_tag"] == "MemoryPressureLongContext":
+            d["prompt_tokens"] *= 4
+        out.append(ctl.format_trace_line(d))
+    return "\n".join(out) + "\n"
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_config5_predicted_time_balanced(world):
+    """On the config-5 deployment mix (64 per class), the B200-measured cost
+    model places work so that every GPU's predicted time is within 10% of the
+    mean (8 prefix groups, so shared-prefix traffic is not one indivisible unit)."""
+    text = _deploy_mix(64)
+    cm = CostModel.load()
+    shards = shard_trace(text, world, cm, prefix_groups=8)
+    load = predicted_load(text, shards, cm, prefix_groups=8)
+    mean = sum(load) / world
+    assert max(load) <= 1.10 * mean, (load, mean)
+
+
+def test_prefix_groups_are_sticky_and_spread():
+    text = _deploy_mix(16)
+    lines = [l for l in text.splitlines() if l.strip()]
+    routes = ctl.route_ndjson(text)
+    shards = shard_trace(text, 4, prefix_groups=4)
+    owner = {i: r for r, s in enumerate(shards) for i in s}
+    groups = {}
+    for i, l in enumerate(lines):
+        if routes[i]["mode"] == PC_MODE:
+            groups.setdefault(prefix_group(ctl.parse_trace_line(l)["request_id"], 4), set()).add(owner[i])
+    assert len(groups) == 4 and all(len(v) == 1 for v in groups.values())
+    assert len({next(iter(v)) for v in groups.values()}) > 1  # groups land on different GPUs
+    assert prefix_group("SharedPrefixChat-0", 1) == 0
+
+
+def test_cost_model_is_the_reference_formula():
+    cm = CostModel.load()
+    d = {"prompt_tokens": 1000, "expected_output_tokens": 100}
+    assert cm.fp16_ms(d) == pytest.approx(cm.fixed + cm.prefill * 1000 + cm.decode * 100)
+    sp = cm.speedup[("gptq4", "SyntheticSS")]
+    assert cm.mode_ms(d, "gptq4", "SyntheticSS") == pytest.approx(cm.fp16_ms(d) / sp)
+    assert cm.decode > 10 * cm.prefill  # a decode token costs far more than a prefill token on B200
 
 
 def _free_port():
