@@ -330,13 +330,18 @@ def run_ours(args):
     value = ws * dec_tokens / (dec_ms_max / 1000.0)
     e2e = ws * NEW * args.steps / (tot_ms_max / 1000.0)
     per_mode = {}
+    # algorithmic bytes per decode token = every linear's weights +
+    # lm_head + the KV the token's attention reads (context PROMPT + j at step j)
+    from paper_2605_23057_b200.configs import model_cfg
+    kv_tok = kv_bytes_per_pos(model_cfg("llama8b")) * sum(PROMPT + j for j in range(1, NEW)) / (NEW - 1)
     for _, name in MODES:
         a = agg[name]
         tps = (NEW - 1) * args.steps / (a["dec_ms"] / 1000.0)
         per_mode[name] = {"decode_tok_s": tps, "ms_per_token": a["dec_ms"] / ((NEW - 1) * args.steps),
                           "prefill_ms": a["pre_ms"] / args.steps, "request_ms": a["tot_ms"] / args.steps,
                           "weight_bytes_per_token": wbytes[name],
-                          "hbm_frac_of_measured": wbytes[name] * tps / 1e9 / peaks()[0],
+                          "kv_bytes_per_token": kv_tok,
+                          "hbm_frac_of_measured": (wbytes[name] + kv_tok) * tps / 1e9 / peaks()[0],
                           "latency_speedup_vs_fp16": statistics.mean(speedups[name])}
         if energy[name]:
             per_mode[name]["joules_per_token"] = statistics.mean(energy[name])

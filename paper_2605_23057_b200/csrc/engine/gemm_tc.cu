@@ -141,9 +141,11 @@ struct TcCfg {
   // split-K partial tile [BN][128] (fp32 / int32), staged in the A ring once
   // every MMA has completed; up to ks-1 incoming column slices ((ks-1)/ks of
   // a tile) land in the B ring
-  static_assert(kStages >= 4, "ring too shallow");
-  static_assert(BN * kTileM * 4 <= kStages * kABytes, "partial tile must fit the A ring");
-  static_assert(BN * kTileM * 4 <= kStages * kBBytes, "incoming slices must fit the B ring");
+  static_assert(kStages >= (BN > 128 ? 3 : 4), "ring too shallow");
+  // split-K (BN <= 128 only; long prefills fill the machine without it)
+  static constexpr bool kCanSplit = BN <= 128;
+  static_assert(!kCanSplit || BN * kTileM * 4 <= kStages * kABytes, "partial tile must fit the A ring");
+  static_assert(!kCanSplit || BN * kTileM * 4 <= kStages * kBBytes, "incoming slices must fit the B ring");
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -190,7 +192,12 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * kTileM, t0 = blockIdx.y * BN;
+  // grid x = token tiles, y = weight-row tiles: the CTAs that share one
+  // 128-row weight slab are adjacent in launch order, so a long prefill
+  // (T = 1024: 8 token tiles) reads each weight byte from HBM once and from
+  // L2 for the other tiles (weight-tile-major order read it 8 times: 1.89 GB
+  // of DRAM for a 235 MB FP16 gate_up)
+  const int t0 = blockIdx.x * BN, n0 = blockIdx.y * kTileM;
   // split-K: blockIdx.z (= cluster rank) owns k-tiles [kb0, kb0 + nk)
   const int nk_all = K / C::kTileK;
   const int nk_per = (nk_all + ksplit - 1) / ksplit;
@@ -338,7 +345,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
         for (int j = 0; j < 16; ++j) emit(j0 + j, r[j]);
       }
     }
-  } else {
+  } else if constexpr (C::kCanSplit) {
     // Deterministic split-K through distributed shared memory: every CTA of
     // the cluster stages its raw partial tile [BN][128] in its own (now idle)
     // A ring; after a cluster barrier each CTA pushes column slice r of its
@@ -470,9 +477,9 @@ void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, f
                  : make_sw128_map(W.w, elt, W.n, W.k, kTileM);
   const CUtensorMap tb = make_sw128_map(xact, elt, T, W.k, BN);
   const int tiles = (W.n / kTileM) * ((T + BN - 1) / BN);
-  const int ksplit = choose_split(tiles, W.k / C::kTileK, kNumSMs * per_sm);
+  const int ksplit = C::kCanSplit ? choose_split(tiles, W.k / C::kTileK, kNumSMs * per_sm) : 1;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(W.n / kTileM, (T + BN - 1) / BN, ksplit);
+  cfg.gridDim = dim3((T + BN - 1) / BN, W.n / kTileM, ksplit);
   cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
@@ -493,7 +500,10 @@ void launch_fmt_epi(const LinearW& W, const void* x, const float* xs, int T, flo
   if (T <= 16) return launch_bn<FMT, 16, EPI>(W, x, xs, T, y, st);
   if (T <= 32) return launch_bn<FMT, 32, EPI>(W, x, xs, T, y, st);
   if (T <= 64) return launch_bn<FMT, 64, EPI>(W, x, xs, T, y, st);
-  return launch_bn<FMT, 128, EPI>(W, x, xs, T, y, st);
+  if (T <= 128) return launch_bn<FMT, 128, EPI>(W, x, xs, T, y, st);
+  // long prefills: 128 x 256 tiles (UMMA N = 256, 256 TMEM columns) halve the
+  // weight-operand traffic (and, for W4, the dequantisation) per FLOP
+  return launch_bn<FMT, 256, EPI>(W, x, xs, T, y, st);
 }
 
 template <int FMT>

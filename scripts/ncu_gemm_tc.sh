@@ -13,5 +13,6 @@ for fmt in 0 1 2; do
         -o gpurun_out/$tag python scripts/gemm_tc_probe.py $fmt $1 $2 $3 1 > /dev/null 2>&1
     ncu -i gpurun_out/$tag.ncu-rep --page raw --csv > gpurun_out/$tag.csv 2>/dev/null
     python scripts/ncu_metrics.py gpurun_out/$tag.csv "$tag" >> $out
+    rm -f gpurun_out/$tag.ncu-rep gpurun_out/$tag.csv  # keep gpurun_out small (64 MiB merge cap)
   done
 done
