@@ -323,6 +323,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 // the 4-warp / 64-position version spent 6.5 of its 17.8 us per layer in the
 // fence + atomic + last-CTA split merge; scripts/attn_timeline.py.)
 constexpr int kDecWarps = 8;
+constexpr int kRunMax = 6;  // = kGemvMaxTokens: longest run of one sequence in one launch
 #ifndef MSW_ATTN_MMA
 #define MSW_ATTN_MMA 1  // decode attention tile on mma.sync (0: scalar FMA loops)
 #endif
@@ -352,12 +353,16 @@ __global__ void __launch_bounds__(kDecWarps * 32)
                        const int* __restrict__ seq_of, const int* __restrict__ block_table,
                        int max_blocks, half* __restrict__ kc, half* __restrict__ vc, int Hq, int Hk,
                        int nsplit, float* __restrict__ part_o, float* __restrict__ part_ml,
-                       int* __restrict__ counters, float* __restrict__ o) {
+                       int* __restrict__ counters, float* __restrict__ o, int run) {
   constexpr int DPL = D / 32;
   constexpr int RS = D + kKvPad;  // staged row stride (halves)
   extern __shared__ __align__(16) half kv_smem[];  // [warp][K|V][32][RS]
   __shared__ __align__(16) float qs[G][D];
-  __shared__ __align__(16) half knew[D], vnew[D];
+  // new keys / values of this launch: row 0 only for independent tokens; rows
+  // 0..t for a run (tokens 0..T-1 = consecutive positions of one sequence)
+  __shared__ __align__(16) half knew_all[kRunMax][D], vnew_all[kRunMax][D];
+  half* const knew = knew_all[0];
+  half* const vnew = vnew_all[0];
   __shared__ float wm[kDecWarps][G], wl[kDecWarps][G];
   __shared__ float wacc[kDecWarps][G][D];
   __shared__ int is_last;
@@ -366,6 +371,10 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   ATT_TP(0);
   const int p_self = pos[t];
   const int ctx = p_self + 1;
+  // positions [p_new, p_self] come from this launch's qkv rows, not the cache:
+  // the own position for independent tokens; every earlier token of the run
+  // too (their cache rows are appended by other CTAs of this launch)
+  const int p_new = run ? p_self - t : p_self;
   const int chunk = split_chunk_dec(ctx, nsplit);
   const int begin = sp * chunk;
   if (begin >= ctx) {
@@ -391,7 +400,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     for (int i = 0; i < 32 / RPI; ++i) {
       const int r = i * RPI + lane / CPR;
       const int p = base + r;
-      if (p < end && p != p_self) {
+      if (p < end && p < p_new) {
         const int sl = bt[p >> 4] * kKvBlock + (p & 15);
         cp_async16(sK + r * RS + c * 8, kc + kv_off(sl, hk, Hk, D) + c * 8);
         cp_async16(sV + r * RS + c * 8, vc + kv_off(sl, hk, Hk, D) + c * 8);
@@ -437,6 +446,21 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     for (int d = threadIdx.x; d < D; d += blockDim.x)
       vnew[d] = __float2half_rn(row[size_t(Hq + Hk + hk) * D + d]);
   }
+  if (run && t > 0) {  // keys / values of the run's earlier tokens (rows 0..t-1)
+    for (int i = threadIdx.x; i < t * (D / 2); i += blockDim.x) {
+      const int q = 1 + i / (D / 2), j = i % (D / 2);  // row q: token t - q at p_self - q
+      const float* rw = qkv + size_t(t - q) * (Hq + 2 * Hk) * D;
+      const float2 rt = rope[size_t(p_self - q) * (D / 2) + j];
+      const float* src = rw + size_t(Hq + hk) * D;
+      const float x0 = src[j], x1 = src[j + D / 2];
+      knew_all[q][j] = __float2half_rn(__fsub_rn(__fmul_rn(x0, rt.x), __fmul_rn(x1, rt.y)));
+      knew_all[q][j + D / 2] = __float2half_rn(__fadd_rn(__fmul_rn(x1, rt.x), __fmul_rn(x0, rt.y)));
+    }
+    for (int i = threadIdx.x; i < t * D; i += blockDim.x) {
+      const int q = 1 + i / D, d = i % D;
+      vnew_all[q][d] = __float2half_rn(qkv[size_t(t - q) * (Hq + 2 * Hk) * D + size_t(Hq + Hk + hk) * D + d]);
+    }
+  }
   __syncthreads();
   ATT_TP(2);
   if (sp == 0) {
@@ -473,11 +497,13 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     cp_async_wait_all();
     if (base == first) ATT_TP(6);  // warp 0: first tile staged
     const int p = base + lane;
-    if (p == p_self) {  // the new token's row comes from smem, not the cache
+    if (p >= p_new && p <= p_self) {  // this launch's new rows come from smem, not the cache
+      const half* kn = knew_all[p_self - p];
+      const half* vn = vnew_all[p_self - p];
 #pragma unroll 1
       for (int c = 0; c < D / 8; ++c) {
-        *reinterpret_cast<uint4*>(sK + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(knew + c * 8);
-        *reinterpret_cast<uint4*>(sV + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(vnew + c * 8);
+        *reinterpret_cast<uint4*>(sK + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(kn + c * 8);
+        *reinterpret_cast<uint4*>(sV + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(vn + c * 8);
       }
     } else if (p >= end) {  // P = 0 there, but 0 x stale-NaN V would poison the MMA
 #pragma unroll 1
@@ -574,11 +600,13 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     }
     cp_async_wait_all();
     const int p = base + lane;
-    if (p == p_self) {  // the new token's row comes from smem, not the cache
+    if (p >= p_new && p <= p_self) {  // this launch's new rows come from smem, not the cache
+      const half* kn = knew_all[p_self - p];
+      const half* vn = vnew_all[p_self - p];
 #pragma unroll 1
       for (int c = 0; c < D / 8; ++c) {
-        *reinterpret_cast<uint4*>(sK + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(knew + c * 8);
-        *reinterpret_cast<uint4*>(sV + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(vnew + c * 8);
+        *reinterpret_cast<uint4*>(sK + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(kn + c * 8);
+        *reinterpret_cast<uint4*>(sV + lane * RS + c * 8) = *reinterpret_cast<const uint4*>(vn + c * 8);
       }
     }
     __syncwarp();
@@ -805,8 +833,9 @@ void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
 void launch_attention_decode(const float* qkv, const float2* rope, int T, const int* pos,
                              const int* slot, const int* seq_of, const int* block_table, half* kc,
                              half* vc, const AttnShape& a, int nsplit, float* part_o,
-                             float* part_ml, int* counters, float* o, cudaStream_t st) {
+                             float* part_ml, int* counters, float* o, cudaStream_t st, bool run) {
   const int G = a.n_heads / a.n_kv_heads;
+  if (run && T > kRunMax) throw ConfigErr("attention: a one-sequence run is at most 6 tokens");
   const dim3 grid(T, a.n_kv_heads, nsplit), thr(kDecWarps * 32);
 #define MSW_DEC(DD, GG)                                                                       \
   if (a.head_dim == DD && G == GG) {                                                          \
@@ -819,7 +848,7 @@ void launch_attention_decode(const float* qkv, const float2* rope, int T, const 
     }                                                                                         \
     return launch_pdl(attn_decode_kernel<DD, GG>, grid, thr, smem, st, qkv, rope, pos,        \
                       slot, seq_of, block_table, a.max_blocks_per_seq, kc, vc, a.n_heads,     \
-                      a.n_kv_heads, nsplit, part_o, part_ml, counters, o);                    \
+                      a.n_kv_heads, nsplit, part_o, part_ml, counters, o, run ? 1 : 0);       \
   }
   MSW_DEC(128, 1)
   MSW_DEC(128, 2)

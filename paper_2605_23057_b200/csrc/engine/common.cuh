@@ -145,6 +145,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Orders this thread's prior generic-proxy shared-memory accesses (and those
+// it acquired) before its subsequent async-proxy operations (bulk copies).
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 // 1-D bulk async copy global -> shared, completion counted on an mbarrier.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -168,9 +173,16 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// Named barrier over the first `threads` threads (id 1..15; 0 is __syncthreads).
+// Named barrier over `threads` threads (id 1..15; 0 is __syncthreads).
+// The NON-aligned form: every thread arrives individually, so a warp that
+// reaches it diverged (the compiler does not know an inline-asm barrier needs
+// reconvergence) is still counted correctly. `bar.sync` is
+// barrier.sync.aligned, which is undefined for a diverged warp: compute-
+// sanitizer synccheck flagged it at the GEMV prologue barriers, and it let
+// consumer warps start on partially written activations (the sporadic stale
+// tiles of the FP16 6-token K=14336 GEMV, scripts/repro_gemv_t6.py).
 __device__ __forceinline__ void named_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // Bulk L2 prefetch of a contiguous byte range (TMA unit, no registers used).

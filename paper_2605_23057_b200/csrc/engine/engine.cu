@@ -496,7 +496,7 @@ constexpr bool diag_skip(const char*) { return false; }
 #endif
 
 void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_identity,
-             bool tokens_independent) {
+             bool tokens_independent, bool one_seq = false) {
   Scratch& s = e->sc;
   cudaStream_t st = e->st;
   const msw_model_cfg& c = m.c;
@@ -530,9 +530,10 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
       launch_gemm(ly.qkv[fmt], kEpiStore, s.xh, s.xq, s.xscale, T, s.qkv, st);
       n += 2;
     }
-    if (tokens_independent) {  // decode / CB: RoPE + KV append fused into attention
+    const bool run = !tokens_independent && one_seq && T <= kGemvMaxTokens;
+    if (tokens_independent || run) {  // decode / CB / short runs: RoPE + KV append fused
       if (!diag_skip("attn")) launch_attention_decode(s.qkv, m.rope, T, s.pos, s.slot, s.seq_of, m.block_table, kc,
-                              vc, m.ash, nsplit, s.part_o, s.part_ml, s.split_cnt, s.o, st);
+                              vc, m.ash, nsplit, s.part_o, s.part_ml, s.split_cnt, s.o, st, run);
       n += 1;
     } else {
       launch_rope_append(s.qkv, T, s.pos, s.slot, m.rope, m.ash, s.q16, kc, vc, st);
@@ -672,7 +673,8 @@ void prefill(msw_engine* e, Model& m, int fmt, int row, const int32_t* prompt, i
       st_rows[0] = T - 1;
       MSW_CUDA(cudaMemcpyAsync(s.logit_rows, st_rows, sizeof(int), cudaMemcpyHostToDevice, e->st));
     }
-    forward(e, m, fmt, T, 1, /*rows_identity=*/T == 1, /*tokens_independent=*/T == 1);
+    forward(e, m, fmt, T, 1, /*rows_identity=*/T == 1, /*tokens_independent=*/T == 1,
+            /*one_seq=*/true);
     MSW_CUDA(cudaStreamSynchronize(e->st));  // staging is reused by the next chunk
   }
 }
@@ -874,13 +876,14 @@ void spec_round(msw_engine* e, cudaGraphConditionalHandle cond, bool use_cond) {
   const int k = e->cfg.spec_k;
   cudaStream_t st = e->st;
   launch_spec_draft_setup(s.spec, s.tok, s.pos, s.slot, s.seq_of, s.logit_rows, dr.block_table, st);
-  forward(e, dr, kFP16, 2, 1, /*rows_identity=*/false, /*tokens_independent=*/false);
+  forward(e, dr, kFP16, 2, 1, /*rows_identity=*/false, /*tokens_independent=*/false,
+          /*one_seq=*/true);
   for (int i = 1; i < k; ++i) {
     launch_spec_draft_next(s.spec, i, s.next, s.tok, s.pos, s.slot, s.seq_of, dr.block_table, st);
     forward(e, dr, kFP16, 1, 1, true, true);
   }
   launch_spec_verify_setup(s.spec, k, s.next, s.tok, s.pos, s.slot, s.seq_of, tg.block_table, st);
-  forward(e, tg, kFP16, k + 1, k + 1, true, false);
+  forward(e, tg, kFP16, k + 1, k + 1, true, false, /*one_seq=*/true);
   launch_spec_accept(s.spec, k, s.next, s.logits, tg.c.vocab, cond, use_cond, st);
   e->launches += 4 + k;
 }

@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       const int s = kb % kPkStages;
       const uint32_t ph = (kb / kPkStages) & 1;
       mbar_wait(&pempty[s], ph ^ 1);
+      fence_proxy_async();  // dequantisers' generic reads of this slot before the TMA overwrite
       mbar_expect_tx(&pfull[s], C::kPkBytes);
       tma_load_2d(sP + s * C::kPkBytes, &tmA, &pfull[s], (kb0 + kb) * 8, n0);
     }

@@ -335,6 +335,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int st = 0; st < total_stages; ++st) {
         mbar_wait(&empty[s], phase ^ 1);
+        // the consumers read this slot with generic-proxy loads; order those
+        // reads (acquired through the empty barrier) before the async-proxy
+        // bulk copy that overwrites it
+        fence_proxy_async();
         mbar_expect_tx(&full[s], STAGE_BYTES);
         bulk_g2s(ring + size_t(s) * STAGE_BYTES, src + size_t(st) * STAGE_BYTES, STAGE_BYTES, &full[s]);
         if (++s == n_stages) {
@@ -559,9 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pw[(g + 8) * 8 + 2 * tq] = r4[2];
           pw[(g + 8) * 8 + 2 * tq + 1] = r4[3];
         }
-        // each lane's arrive releases its OWN partial stores: a lane-0 arrive after
-        // __syncwarp() let the epilogue read other lanes' stale partials
-        // (~5-30% of 6-token K=14336 runs, scripts/repro_gemv_t6.py)
+        // each lane's arrive releases its OWN partial stores
         mbar_arrive(&tile_full[b]);
       }
 #pragma unroll
@@ -645,6 +647,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int st = 0; st < total_stages; ++st) {
         mbar_wait(&empty[s], phase ^ 1);
+        // the consumers read this slot with generic-proxy loads; order those
+        // reads (acquired through the empty barrier) before the async-proxy
+        // bulk copy that overwrites it
+        fence_proxy_async();
         mbar_expect_tx(&full[s], STAGE_BYTES);
         bulk_g2s(ring + size_t(s) * STAGE_BYTES, src + size_t(st) * STAGE_BYTES, STAGE_BYTES,
                  &full[s]);
@@ -1083,20 +1089,7 @@ void launch_gemv_(const LinearW& W, int pro, int epi, const float* x, int T, con
   if (T < 1 || T > kGemvMaxTokens) throw ConfigErr("gemv: 1..6 tokens");
   if (!W.w_tf) throw ConfigErr("gemv: decode (tile-fragment) weight layout missing");
   switch (W.fmt) {
-    case kFP16:
-      if (T == 6 && size_t(kGemvMaxTokens) * 2 * W.k > 120 * 1024 &&
-          !diag_env("MSW_GEMV_NO_SPLIT")) {
-        // FP16, 6 real tokens, large K: the 6-column activation stage leaves a
-        // 2-stage ring, and this case returned stale rows in ~5-45% of runs
-        // (scripts/repro_gemv_t6.py). No engine path issues it
-        // (speculative verify is T = k + 1 = 5, which runs in one launch);
-        // run it as 4 + 2 tokens.
-        const size_t yrow = epi == kEpiSwiglu ? size_t(W.n / 2) : size_t(W.n);
-        dispatch_fmt<kFP16>(W, pro, epi, x, 4, gamma, eps, y, st);
-        return dispatch_fmt<kFP16>(W, pro, epi, x + size_t(4) * W.k, T - 4, gamma, eps,
-                                   y + 4 * yrow, st);
-      }
-      return dispatch_fmt<kFP16>(W, pro, epi, x, T, gamma, eps, y, st);
+    case kFP16: return dispatch_fmt<kFP16>(W, pro, epi, x, T, gamma, eps, y, st);
     case kINT8: return dispatch_fmt<kINT8>(W, pro, epi, x, T, gamma, eps, y, st);
     case kW4:
       if (T > 1 && size_t(kGemvMaxTokens) * 4 * W.k > 120 * 1024) {

@@ -98,10 +98,15 @@ void launch_attention_prefill(const half* q, int T, const int* pos, const int* s
 
 // Decode / continuous batching (each token is the newest of its own sequence):
 // RoPE + KV append fused into the attention kernel; reads fp32 qkv directly.
+// run = true: the T <= 6 tokens are consecutive positions of ONE sequence
+// (speculative verify, the draft's catch-up step, short prefills); token t's
+// CTAs take the keys / values of tokens 0..t from the qkv rows instead of the
+// cache, so no separate RoPE/append launch is needed.
 void launch_attention_decode(const float* qkv, const float2* rope, int T, const int* pos,
                              const int* slot, const int* seq_of, const int* block_table, half* kc,
                              half* vc, const AttnShape& a, int nsplit, float* part_o,
-                             float* part_ml, int* counters, float* o, cudaStream_t st);
+                             float* part_ml, int* counters, float* o, cudaStream_t st,
+                             bool run = false);
 
 // ---- misc.cu ------------------------------------------------------------------
 void launch_embed(const half* emb, const int* tok, int T, int H, float* h, cudaStream_t st);

@@ -185,3 +185,43 @@ def test_w4_decode_balanced_ranges(cuda_ok, n, k):
         assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
     ref = O.linear(_capi.W_W4, q4, s4, x)
     assert np.abs(outs[0] - ref).max() / np.abs(ref).max() < 2e-3
+
+
+@pytest.mark.parametrize("fmt,t,n,k", [(_capi.W_FP16, 6, 256, 14336), (_capi.W_FP16, 5, 256, 14336),
+                                       (_capi.W_FP16, 6, 512, 4096), (_capi.W_INT8, 6, 256, 14336),
+                                       (_capi.W_INT8, 4, 512, 4096), (_capi.W_W4, 1, 4096, 14336)])
+def test_decode_gemv_stress_repeatable(cuda_ok, fmt, t, n, k):
+    """Repeated launches of the decode GEMV (one CTA per SM, cp.async.bulk ring
+    read with generic loads) are bitwise identical and within the oracle bar.
+    The FP16 6-token K=14336 shape leaves a 2-stage ring; it returned stale
+    tiles in ~1.5% of runs until the producer fenced the consumers' generic
+    reads against the async-proxy overwrite (fence.proxy.async, gemv.cu)."""
+    torch = _torch()
+    w = O.fill_fp16(n, k, 13, 999 + n + k, (int(np.ceil(np.log2(k))) + 1) // 2)
+    lib = engine_lib()
+    if fmt == _capi.W_FP16:
+        src, s, ref_w, ref_s = torch.from_numpy(w.view(np.int16)).cuda(), None, w, None
+    elif fmt == _capi.W_INT8:
+        q8, s8 = O.quant_int8_rows(w)
+        src, s, ref_w, ref_s = torch.from_numpy(q8).cuda(), torch.from_numpy(s8).cuda(), q8, s8
+    else:
+        q4, s4 = O.quant_w4_rows(w)
+        src = torch.from_numpy(_pack_w4_host(q4).view(np.int32)).cuda()
+        s, ref_w, ref_s = torch.from_numpy(s4.view(np.int16)).cuda(), q4, s4
+    tf = torch.empty_like(src)
+    check_engine(lib.msw_repack_decode(fmt, src.data_ptr(), n, k, tf.data_ptr(), None))
+    x = np.random.default_rng(k + t).standard_normal((t, k)).astype(np.float32)
+    dx = torch.from_numpy(x).cuda()
+    outs = []
+    for _ in range(60):
+        dy = torch.full((t, n), float("nan"), device="cuda")
+        check_engine(lib.msw_linear_decode(fmt, tf.data_ptr(), s.data_ptr() if s is not None else None,
+                                           n, k, dx.data_ptr(), t, dy.data_ptr(), None))
+        outs.append(dy)
+    torch.cuda.synchronize()
+    first = outs[0].cpu().numpy()
+    for o in outs[1:]:
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), first.view(np.uint32))
+    ref = O.linear(fmt, ref_w, ref_s, x)
+    tol = {_capi.W_FP16: 2e-5, _capi.W_INT8: 0.0, _capi.W_W4: 2e-3}[fmt]
+    assert np.abs(first - ref).max() <= tol * np.abs(ref).max()
