@@ -92,7 +92,7 @@ __device__ __forceinline__ void prologue(const float* __restrict__ x, const half
                                          float eps, int k, int T, uint8_t* xs, float* red,
                                          float* xscale) {
   const int tid = threadIdx.x;
-  for (int t = 0; t < NT; ++t) {
+  for (int t = 0; t < (FMT == kW4 ? NT : T); ++t) {  // FP16 / INT8 stage the T real rows only
     const int bytes = FMT == kINT8 ? k : 2 * k;
     if (t >= T) {  // padding token columns: never stored, but keep them finite
       for (int i = tid; i < bytes / 16; i += kConsThreads)
@@ -181,6 +181,109 @@ __device__ __forceinline__ void prologue(const float* __restrict__ x, const half
     }
     named_sync(1, kConsThreads);
   }
+}
+
+// Multi-token FP16 / INT8 prologue (verify, small continuous-batching
+// steps): every token's statistics in ONE pass and one block reduction
+// (instead of one pass and two barriers per token in sequence), then one
+// conversion pass over all tokens. red2: [2][NT][kConsumers] floats.
+template <int FMT, int PRO, int NT>
+__device__ __forceinline__ void prologue_multi(const float* __restrict__ x,
+                                               const half* __restrict__ gamma, float eps, int k,
+                                               int T, uint8_t* xs, float* red2, float* xscale) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k4 = k / 4;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float* redm = red2;                       // [NT][kConsumers]
+  float* redx = red2 + NT * kConsumers;     // [NT][kConsumers]
+  float r[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) r[t] = 1.0f;
+  if (PRO == kProNorm) {
+    float ss[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) ss[t] = 0.0f;
+    for (int i = tid; i < k4; i += kConsThreads) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        if (t < T) {
+          const float4 v = x4[size_t(t) * k4 + i];
+          ss[t] = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss[t]))));
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const float w = warp_sum(ss[t]);
+      if (lane == 0) redm[t * kConsumers + warp] = w;
+    }
+    named_sync(1, kConsThreads);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const float v = warp_sum(lane < kConsumers ? redm[t * kConsumers + lane] : 0.0f);
+      r[t] = 1.0f / sqrtf(v / float(k) + eps);
+    }
+  }
+  auto act4 = [&](int t, int i) -> float4 {
+    float4 v = x4[size_t(t) * k4 + i];
+    if (PRO == kProNorm) {
+      const half2* gm = reinterpret_cast<const half2*>(gamma) + 2 * i;
+      const float2 g0 = __half22float2(gm[0]), g1 = __half22float2(gm[1]);
+      v.x = (v.x * r[t]) * g0.x;
+      v.y = (v.y * r[t]) * g0.y;
+      v.z = (v.z * r[t]) * g1.x;
+      v.w = (v.w * r[t]) * g1.y;
+    }
+    return v;
+  };
+  if (FMT == kINT8) {
+    float am[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) am[t] = 0.0f;
+    for (int i = tid; i < k4; i += kConsThreads) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        if (t < T) {
+          const float4 v = act4(t, i);
+          am[t] = fmaxf(am[t], fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const float w = warp_max(am[t]);
+      if (lane == 0) redx[t * kConsumers + warp] = w;
+    }
+    named_sync(1, kConsThreads);
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+      am[t] = warp_max(lane < kConsumers ? redx[t * kConsumers + lane] : 0.0f);
+    for (int i = tid; i < k4; i += kConsThreads) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        if (t < T) {
+          const float4 v = act4(t, i);
+          const float sc = am[t] / 127.0f;
+          auto q = [&](float u) -> int8_t {
+            const float w = am[t] > 0.0f ? rintf(u / sc) : 0.0f;
+            return static_cast<int8_t>(fminf(fmaxf(w, -127.0f), 127.0f));
+          };
+          *reinterpret_cast<char4*>(xs + size_t(t) * k + perm_i8(4 * i)) =
+              make_char4(q(v.x), q(v.y), q(v.z), q(v.w));
+        }
+    }
+    if (tid < NT) xscale[tid] = tid < T ? am[tid] / 127.0f : 0.0f;
+  } else {
+    for (int i = tid; i < k4; i += kConsThreads) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        if (t < T) {
+          const float4 v = act4(t, i);
+          half* xh = reinterpret_cast<half*>(xs + size_t(t) * 2 * k);
+          *reinterpret_cast<half2*>(xh + perm_f16(4 * i)) = __floats2half2_rn(v.x, v.y);
+          *reinterpret_cast<half2*>(xh + perm_f16(4 * i + 2)) = __floats2half2_rn(v.z, v.w);
+        }
+    }
+  }
+  named_sync(1, kConsThreads);
 }
 
 // Batch-1 W4 prologue (k <= 16384): x stays in registers between the RMSNorm
@@ -284,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages], sbar;
   __shared__ uint64_t tile_full[2], tile_free[2];
   __shared__ float red[32];
+  __shared__ float red2[2 * NT * kConsumers];  // multi-token prologue reductions
   __shared__ float xscale[NT];
   __shared__ __align__(16) uint32_t part[2][kConsumers][16][8];  // per-warp tile partials
   __shared__ __align__(16) uint8_t zero_b[64];
@@ -299,8 +403,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total_stages = ntile_cta * stages_tile;
   const int groups_k = k / kW4Group;
   const int rows = ntile_cta * 16;
-  const int xbytes = FMT == kINT8 ? NT * k
-                                  : (FMT == kW4 ? NT * 4 * k + NT * (k / kW4Group) * 4 : NT * 2 * k);
+  // FP16 / INT8 stage only the T real token rows (a 5-token FP16 verify at
+  // K = 14336 keeps a 3-stage ring instead of 2); W4 keeps NT rows
+  const int xbytes = FMT == kINT8 ? T * k
+                                  : (FMT == kW4 ? NT * 4 * k + NT * (k / kW4Group) * 4 : T * 2 * k);
   const int sbytes = FMT == kW4 ? rows * groups_k * 2 : (FMT == kINT8 ? rows * 4 : 0);
   uint8_t* xs = smem;
   uint8_t* sc_smem = smem + ((xbytes + 127) & ~127);
@@ -453,7 +559,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // consumers
   pdl_wait();
   pdl_trigger();
-  prologue<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red, xscale);
+  if constexpr (NT > 1 && FMT != kW4)
+    prologue_multi<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red2, xscale);
+  else
+    prologue<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red, xscale);
   named_sync(3, kConsThreads + 32);  // release the epilogue warp (xscale ready)
   const int g = lane >> 2, tq = lane & 3;
   const bool has_tok = g < T;  // this lane's MMA column is a real token
@@ -946,9 +1055,9 @@ void launch_tf_s(const LinearW& W, const float* x, int T, const half* gamma, flo
   const int ntiles = W.n / 16;
   const int grid = std::max(1, std::min(ntiles, kNumSMs));
   const int stage_bytes = S * kChunkBytes;
-  const size_t xraw = FMT == kINT8 ? size_t(NT) * W.k
+  const size_t xraw = FMT == kINT8 ? size_t(T) * W.k
                                    : (FMT == kW4 ? size_t(NT) * 4 * W.k + size_t(NT) * (W.k / kW4Group) * 4
-                                                 : size_t(NT) * 2 * W.k);
+                                                 : size_t(T) * 2 * W.k);
   const size_t xbytes = (xraw + 127) & ~size_t(127);
   const int per_cta = (ntiles + grid - 1) / grid;
   const size_t sbytes = FMT == kW4 ? size_t(per_cta) * 16 * (W.k / kW4Group) * 2
