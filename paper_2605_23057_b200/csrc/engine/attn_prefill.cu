@@ -296,6 +296,9 @@ void launch_pf(int T, const half* q, const int* pos, const int* seq_of, const in
 void launch_attention_prefill(const half* q, int T, const int* pos, const int* seq_of,
                               const int* block_table, const half* kc, const half* vc,
                               const AttnShape& a, float* o, cudaStream_t st) {
+  if (a.n_blocks > 0 && attention_prefill_tc05_supported(a))
+    return launch_attention_prefill_tc05(q, T, pos, seq_of, block_table, kc, vc,
+                                         uint64_t(a.n_blocks) * a.n_kv_heads * kKvBlock, a, o, st);
   const int G = a.n_heads / a.n_kv_heads;
 #define MSW_PF(DD, GG)                                                                       \
   if (a.head_dim == DD && G == GG)                                                           \

@@ -395,12 +395,16 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
   m.kv_layer_elems = size_t(m.nblk) * Hk * kKvBlock * D;
   m.kc = model_alloc<half>(m, m.kv_layer_elems * L);
   m.vc = model_alloc<half>(m, m.kv_layer_elems * L);
+  // finite contents everywhere: tensor-core attention reads whole 16-row
+  // blocks, and 0 x NaN from never-written rows would poison P x V
+  MSW_CUDA(cudaMemsetAsync(m.kc, 0, sizeof(half) * m.kv_layer_elems * L, st));
+  MSW_CUDA(cudaMemsetAsync(m.vc, 0, sizeof(half) * m.kv_layer_elems * L, st));
   m.max_blocks = (cfg.max_seq_len + kKvBlock - 1) / kKvBlock + 2;
   m.bt_rows = is_draft ? 1 : std::max(1, cfg.max_batch);
   m.block_table = model_alloc<int>(m, size_t(m.bt_rows) * m.max_blocks);
   MSW_CUDA(cudaMemset(m.block_table, 0, sizeof(int) * size_t(m.bt_rows) * m.max_blocks));
   m.pool.init(m.nblk);
-  m.ash = AttnShape{Hq, Hk, D, m.max_blocks};
+  m.ash = AttnShape{Hq, Hk, D, m.max_blocks, m.nblk};
   // decode attention splits hold >= 256 positions (attention.cu kDecMinChunk):
   // no more splits than max_seq_len needs, so short-context engines do not
   // launch idle CTAs

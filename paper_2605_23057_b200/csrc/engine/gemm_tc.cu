@@ -128,7 +128,10 @@ struct TcCfg {
   static constexpr int kABytes = kTileM * kTileKBytes;        // 16 KB
   static constexpr int kBBytes = BN * kTileKBytes;
   static constexpr int kPkBytes = kIsW4 ? kTileM * 32 : 0;    // 128 rows x 8 packed words
-  static constexpr int kThreads = kIsW4 ? 256 : 128;
+  // W4: 8 dequantiser warps (two per weight row, 4 packed words each) keep the
+  // fp16 operand production ahead of the MMA (4 warps bounded W4 prefill below FP16)
+  static constexpr int kDqWarps = 8;
+  static constexpr int kThreads = kIsW4 ? 128 + kDqWarps * 32 : 128;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
   // operand ring as deep as ~220 KB of shared memory allows (one CTA per SM):
   // a short prefill / CB step streams weights at HBM rate only with enough
@@ -206,12 +209,12 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], C::kIsW4 ? 1 + 4 : 1);  // TMA arrive (+ 4 dequant warps)
+      mbar_init(&full[s], C::kIsW4 ? 1 + C::kDqWarps : 1);  // TMA arrive (+ dequant warps)
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kPkStages; ++s) {
       mbar_init(&pfull[s], 1);
-      mbar_init(&pempty[s], 4);
+      mbar_init(&pempty[s], C::kDqWarps);
     }
     mbar_init(done, 1);
     mbar_init(rbar, 1);
@@ -270,10 +273,11 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       tma_load_2d(sP + s * C::kPkBytes, &tmA, &pfull[s], (kb0 + kb) * 8, n0);
     }
   } else if (C::kIsW4 && warp >= 4) {
-    // ---- W4 dequantisers: thread r (0..127) owns weight row n0 + r of every
-    // k-tile: packed words from the smem ring -> fp16 (q-8)*s in the SW128
-    // K-major layout the UMMA descriptor reads (no int4 UMMA on sm_100a)
-    const int r = threadIdx.x - 128;
+    // ---- W4 dequantisers: thread (r, hf) owns packed words 4hf..4hf+3 (k
+    // 32hf..32hf+31) of weight row n0 + r of every k-tile: packed words from
+    // the smem ring -> fp16 (q-8)*s in the SW128 K-major layout the UMMA
+    // descriptor reads (no int4 UMMA on sm_100a)
+    const int r = (threadIdx.x - 128) & 127, hf = (threadIdx.x - 128) >> 7;
     const half* srow = static_cast<const half*>(wscale) + size_t(n0 + r) * (K / kW4Group);
     const half2 k1032 = __float2half2_rn(1032.0f);
     for (int kb = 0; kb < nk; ++kb) {
@@ -283,19 +287,19 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       const uint32_t ph = (kb / C::kStages) & 1;
       const half2 s2 = __half2half2(srow[((kb0 + kb) * 64) / kW4Group]);
       mbar_wait(&pfull[ps], pph);
-      const uint4* prow = reinterpret_cast<const uint4*>(sP + ps * C::kPkBytes + r * 32);
-      const uint4 p0 = prow[0], p1 = prow[1];
+      const uint4 p0 = reinterpret_cast<const uint4*>(sP + ps * C::kPkBytes + r * 32)[hf];
       __syncwarp();
       if (lane == 0) mbar_arrive(&pempty[ps]);
       mbar_wait(&empty[s], ph ^ 1);
       uint8_t* rowp = sA + s * C::kABytes + r * 128;
-      const uint32_t words[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+      const uint32_t words[4] = {p0.x, p0.y, p0.z, p0.w};
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {  // chunk c = k 8c..8c+7 = packed word c
+      for (int cc = 0; cc < 4; ++cc) {  // chunk c = k 8c..8c+7 = packed word c
+        const int c = 4 * hf + cc;
         uint32_t out[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          uint32_t u = lop3_and_or(words[c] >> (4 * i), 0x000F000Fu, 0x64006400u);
+          uint32_t u = lop3_and_or(words[cc] >> (4 * i), 0x000F000Fu, 0x64006400u);
           const half2 q = __hsub2(*reinterpret_cast<const half2*>(&u), k1032);
           const half2 wv = __hmul2(q, s2);
           out[i] = *reinterpret_cast<const uint32_t*>(&wv);

@@ -75,6 +75,7 @@ void launch_gemm_tc(const LinearW& W, int epi, const half* xh, const int8_t* xq,
 struct AttnShape {
   int n_heads, n_kv_heads, head_dim;
   int max_blocks_per_seq;  // block-table row stride
+  int n_blocks = 0;        // KV pool blocks per layer (tensor maps over the pool)
 };
 // qkv fp32 [T, (Hq+2Hk)*D] -> RoPE on q,k -> q fp16 [T,Hq,D]; k,v fp16 into the
 // paged cache at slot[t] (= block*16 + offset) of this layer.
@@ -92,6 +93,12 @@ void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
 
 // Same semantics on the tensor pipe (attn_prefill.cu): many query tokens,
 // packed from any number of sequences; no split-KV (o written directly).
+// head_dim 128 runs on tcgen05 (attn_prefill_tc05.cu, TMA + TMEM); needs
+// a.n_blocks (the KV pool is addressed through TMA tensor maps).
+bool attention_prefill_tc05_supported(const AttnShape& a);
+void launch_attention_prefill_tc05(const half* q, int T, const int* pos, const int* seq_of,
+                                   const int* block_table, const half* kc, const half* vc,
+                                   uint64_t kv_rows, const AttnShape& a, float* o, cudaStream_t st);
 void launch_attention_prefill(const half* q, int T, const int* pos, const int* seq_of,
                               const int* block_table, const half* kc, const half* vc,
                               const AttnShape& a, float* o, cudaStream_t st);
