@@ -177,7 +177,7 @@ def profiled_traffic():
         return None
 
 
-def cpu_baseline_8b(new_tokens: int = 3, prompt_len: int = 4):
+def cpu_baseline_8b(new_tokens: int = 27, prompt_len: int = 4):
     """CPU oracle (C port, OpenMP over all host cores), 8B shape, W4 mode."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O  # checker / baseline only
@@ -601,7 +601,7 @@ def run_configs(args):
                           "request_frac": (floor_dec + floor_pre) / tot_ms,
                           "peaks": {"hbm_gbs": hbm, "tensor_tflops": tp16}})
     if cpu:
-        line["cpu_baseline"] = cpu_mode_sample(2)
+        line["cpu_baseline"] = cpu_mode_sample(2, new_tokens=27)
     print(json.dumps(line), flush=True)
     # 3b: 64 co-scheduled requests, prompts 1024+-10%, outputs 128+-10%, INT8 + continuous batching
     prompts, outs = [], []
@@ -636,7 +636,7 @@ def run_configs(args):
                           "frac": (floor_pre + floor_dec) / (wall * 1e3),
                           "peaks": {"hbm_gbs": hbm, "int8_tops": tpi8, "int8_source": i8src}})
     if cpu:
-        line["cpu_baseline"] = cpu_mode_sample(1)
+        line["cpu_baseline"] = cpu_mode_sample(1, new_tokens=57)
     print(json.dumps(line), flush=True)
     # 4: speculative decoding on long generations (SyntheticSL-shape prompt, 1024 new tokens),
     # against FP16 batch-1 on the same requests
@@ -664,7 +664,7 @@ def run_configs(args):
                           "frac": floor / tot_dec, "peak_gbs": hbm,
                           "token_ceiling_tok_s": tot_tok / (floor / 1e3)})
     if cpu:
-        line["cpu_baseline"] = cpu_mode_sample(4, prompt_len=4, new_tokens=6, draft="llama1b")
+        line["cpu_baseline"] = cpu_mode_sample(4, prompt_len=4, new_tokens=16, draft="llama1b")
     print(json.dumps(line), flush=True)
     eng.close()
 

@@ -312,6 +312,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (it > 0) {
           mbar_wait(&o_done, (it - 1) & 1);
           tc_after();
+          // rescale O only when some row of the warp saw a new maximum (the
+          // row maxima settle after the first tiles)
+          if (__any_sync(0xffffffffu, corr != 1.0f))
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
             uint32_t u[32];
