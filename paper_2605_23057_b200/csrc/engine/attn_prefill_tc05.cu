@@ -8,18 +8,20 @@
 //
 // Per CTA: 128 query rows = 128/G consecutive tokens x the G query heads of
 // one kv head (TMEM lane = row), KV tiles of 128 positions.
-//   warp 4 (one lane) : TMA producer. A KV tile is 8 paged blocks; each block
+//   warp 8 (one lane) : TMA producer. A KV tile is 8 paged blocks; each block
 //                       is 16 rows x 256 B per kv head, loaded as two
 //                       SWIZZLE_128B boxes (d 0..63, 64..127) for K and for V
 //                       into a double-buffered ring.
-//   warp 5 (one lane) : MMA issuer. S_j = Q K_j^T (kind::f16, M = N = 128,
+//   warp 9 (one lane) : MMA issuer. S_j = Q K_j^T (kind::f16, M = N = 128,
 //                       K = D; Q and K K-major) into one of two TMEM S
 //                       buffers, issued one tile ahead of the softmax; then
 //                       O += P_j V_j with P (fp16) read from TMEM as the A
 //                       operand and V_j as an MN-major B operand (the cache
 //                       rows are d-contiguous), accumulating in TMEM.
-//   warps 0-3         : softmax, one thread per query row: tcgen05.ld of the
-//                       row's 128 scores (row max / sum are thread-local),
+//   warps 0-7         : softmax, two threads per query row (warps w and w+4
+//                       share TMEM lane quarter w & 3 and take the two
+//                       64-column halves): tcgen05.ld of the half-row's
+//                       scores, one shared-memory exchange of the row max,
 //                       causal mask, online softmax in the exp2 domain, the
 //                       O rescale (tcgen05.ld/st) and P (tcgen05.st); at the
 //                       end O / l -> fp32 o.
@@ -44,7 +46,9 @@ constexpr int kHalfBytes = kKT * 128;         // one 64-d half of a K or V tile 
 constexpr int kTileBytes = 2 * kHalfBytes;    // K or V tile (32 KB)
 constexpr int kQBytes = 2 * kRows * 128;      // Q tile, two 64-d halves (32 KB)
 constexpr int kSmem = kQBytes + 2 * 2 * kTileBytes + 1024;  // Q + 2 stages x (K, V) + align
-constexpr int kThreads = 6 * 32;
+constexpr int kSmWarps = 8;                    // softmax warps: 2 per TMEM lane quarter
+constexpr int kThreads = (kSmWarps + 2) * 32;  // + TMA producer + MMA issuer
+constexpr int kWProd = kSmWarps, kWMma = kSmWarps + 1;
 constexpr uint32_t kColS0 = 0, kColS1 = 128, kColP = 256, kColO = 320;
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
@@ -128,6 +132,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t kv_full[2], kv_empty[2], s_full[2], p_ready, o_done, q_ready;
   __shared__ uint32_t tmem_slot;
   __shared__ int s_pos[TOK], s_seq[TOK];
+  __shared__ float xmax[2][2][kRows];  // [tile parity][column half][row]: partial row maxima
+  __shared__ float xl[2][kRows];       // per column half: partial row sums (epilogue)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * TOK, hk = blockIdx.y;
@@ -139,14 +145,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&kv_empty[s], 1);
       mbar_init(&s_full[s], 1);
     }
-    mbar_init(&p_ready, 4);  // one arrive per softmax warp
+    mbar_init(&p_ready, kSmWarps);  // one arrive per softmax warp
     mbar_init(&o_done, 1);
-    mbar_init(&q_ready, 4);
+    mbar_init(&q_ready, kSmWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
   }
-  if (warp == 5) {
+  if (warp == kWMma) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_u32(&tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return nxt;
   };
 
-  if (warp == 4) {
+  if (warp == kWProd) {
     // ---- TMA producer: K and V tiles of every pass, double buffered
     if (lane == 0) {
       int it = 0, seq = INT_MIN, kv_end, lim;
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kWMma) {
     // ---- MMA issuer
     if (lane == 0) {
       mbar_wait(&q_ready, 0);
@@ -250,25 +256,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       (void)pv_done;
     }
   } else {
-    // ---- softmax / epilogue warps 0-3: thread = query row r = tl * G + g
-    const int r = threadIdx.x;
+    // ---- softmax / epilogue warps 0-7: thread = (query row r = tl * G + g,
+    // column half ch); warps w and w + 4 share TMEM lane quarter w & 3
+    const int r = (warp & 3) * 32 + lane, ch = warp >> 2;
     const int tl = r / G, g = r % G;
     const int t = t0 + tl;
     const int hq = hk * G + g;
-    {  // Q row -> SW128 K-major smem (two 64-d halves), 16-byte chunks XOR (r & 7)
-      const uint4* src = reinterpret_cast<const uint4*>(q + (size_t(t < T ? t : 0) * Hq + hq) * kD);
+    {  // Q row half -> SW128 K-major smem (64-d half ch), 16-byte chunks XOR (r & 7)
+      const uint4* src = reinterpret_cast<const uint4*>(q + (size_t(t < T ? t : 0) * Hq + hq) * kD) + ch * 8;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
+      for (int c = 0; c < 8; ++c) {
         const uint4 v = t < T ? src[c] : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(sQ + (c >> 3) * (kRows * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+        *reinterpret_cast<uint4*>(sQ + ch * (kRows * 128) + r * 128 + ((c ^ (r & 7)) << 4)) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_ready);
     }
-    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+    const uint32_t trow = tmem + (uint32_t((warp & 3) * 32) << 16);
+    const uint32_t col_s = ch * 64, col_p = ch * 32, col_o = ch * 64;
     const int my_pos = s_pos[tl], my_seq = s_seq[tl];
-    float m = -INFINITY, l = 0.0f;
+    float m = -INFINITY, l = 0.0f;  // l: this half's partial sum (same scale as the other half)
     int it = 0, seq = INT_MIN, kv_end, lim_max;
     while ((seq = next_seq(seq, kv_end, lim_max)) != INT_MAX) {
       const int lim = my_seq == seq ? my_pos : -1;
@@ -277,31 +285,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = it & 1;
         mbar_wait(&s_full[s], (it >> 1) & 1);
         tc_after();
-        // scores of this row: 4 x 32 columns
-        float sc[kKT];
+        // this half's 64 scores of the row
+        float sc[64];
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
+        for (int c2 = 0; c2 < 2; ++c2) {
           uint32_t u[32];
-          tld32(trow + (s ? kColS1 : kColS0) + c4 * 32, u);
+          tld32(trow + (s ? kColS1 : kColS0) + col_s + c2 * 32, u);
           tld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sc[c4 * 32 + i] = __uint_as_float(u[i]);
+          for (int i = 0; i < 32; ++i) sc[c2 * 32 + i] = __uint_as_float(u[i]);
         }
         float mt = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < kKT; ++i) {
-          const int kp = j * kKT + i;
+        for (int i = 0; i < 64; ++i) {
+          const int kp = j * kKT + ch * 64 + i;
           sc[i] = kp <= lim ? sc[i] * sl2 : -INFINITY;
           mt = fmaxf(mt, sc[i]);
         }
+        // row maximum over both halves (double-buffered exchange: one barrier per tile)
+        xmax[s][ch][r] = mt;
+        named_sync(2, kSmWarps * 32);
+        mt = fmaxf(mt, xmax[s][ch ^ 1][r]);
         const float mn = fmaxf(m, mt);
         const float u0 = mn == -INFINITY ? 0.0f : mn;
         const float corr = exp2f(m - u0);
         m = mn;
         float ls = 0.0f;
-        uint32_t pk[kKT / 2];
+        uint32_t pk[32];
 #pragma unroll
-        for (int i = 0; i < kKT / 2; ++i) {
+        for (int i = 0; i < 32; ++i) {
           const float e0 = exp2f(sc[2 * i] - u0), e1 = exp2f(sc[2 * i + 1] - u0);
           ls += e0 + e1;
           const half2 h = __floats2half2_rn(e0, e1);
@@ -312,45 +324,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (it > 0) {
           mbar_wait(&o_done, (it - 1) & 1);
           tc_after();
-          // rescale O only when some row of the warp saw a new maximum (the
-          // row maxima settle after the first tiles)
+          // rescale this half of O only when some row of the warp saw a new
+          // maximum (the row maxima settle after the first tiles)
           if (__any_sync(0xffffffffu, corr != 1.0f))
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
+          for (int c2 = 0; c2 < 2; ++c2) {
             uint32_t u[32];
-            tld32(trow + kColO + c4 * 32, u);
+            tld32(trow + kColO + col_o + c2 * 32, u);
             tld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * corr);
-            tst32(trow + kColO + c4 * 32, u);
+            tst32(trow + kColO + col_o + c2 * 32, u);
           }
         }
-#pragma unroll
-        for (int c2 = 0; c2 < 2; ++c2) {
-          uint32_t u[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) u[i] = pk[c2 * 32 + i];
-          tst32(trow + kColP + c2 * 32, u);
-        }
+        tst32(trow + kColP + col_p, pk);
         tst_wait();
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_ready);
       }
     }
-    // epilogue: O / l
+    // epilogue: O / l, l = both halves' partial sums
+    xl[ch][r] = l;
     if (it > 0) {
       mbar_wait(&o_done, (it - 1) & 1);
       tc_after();
     }
-    const float inv = l > 0.0f ? 1.0f / l : 0.0f;
+    named_sync(2, kSmWarps * 32);
+    const float lt = l + xl[ch ^ 1][r];
+    const float inv = lt > 0.0f ? 1.0f / lt : 0.0f;
 #pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
+    for (int c2 = 0; c2 < 2; ++c2) {
       uint32_t u[32];
-      tld32(trow + kColO + c4 * 32, u);
+      tld32(trow + kColO + col_o + c2 * 32, u);
       tld_wait();
       if (t < T && it > 0) {
-        float4* dst = reinterpret_cast<float4*>(o + (size_t(t) * Hq + hq) * kD + c4 * 32);
+        float4* dst = reinterpret_cast<float4*>(o + (size_t(t) * Hq + hq) * kD + col_o + c2 * 32);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           dst[i] = make_float4(__uint_as_float(u[4 * i]) * inv, __uint_as_float(u[4 * i + 1]) * inv,
@@ -360,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_before();
   __syncthreads();
-  if (warp == 5)
+  if (warp == kWMma)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 

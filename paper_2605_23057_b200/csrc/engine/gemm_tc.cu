@@ -319,6 +319,10 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   float ws = 1.0f;
   if (FMT == kINT8 && warp < 4) ws = static_cast<const float*>(wscale)[n];
   // column j of this tile (token t0 + j), raw accumulator bits u
+  // residual epilogue: the 16 y values of a column batch are read together
+  // (independent loads in flight) instead of one read-modify-write round trip
+  // per column; emit() of a batch uses them
+  float prev[16];
   auto emit = [&](int j, uint32_t u) {
     const int t = t0 + j;
     if (EPI == kEpiRaw) {  // INT8 test entry: the int32 accumulator itself
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       if (t < T && (lane & 1) == 0) y[size_t(t) * (N / 2) + (n >> 1)] = silu(v) * up;
     } else if (t < T) {
       if (EPI == kEpiStore) y[size_t(t) * N + n] = v;
-      else y[size_t(t) * N + n] += v;
+      else y[size_t(t) * N + n] = prev[j & 15] + v;  // prev: this 16-column batch's y
     }
   };
   if (warp < 4) {
@@ -346,6 +350,10 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       for (int j0 = 0; j0 < BN; j0 += 16) {
         uint32_t r[16];
         tmem_ld16(trow + j0, r);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {  // residual: all 16 reads in flight before the adds
+          if (EPI == kEpiResid) prev[j] = t0 + j0 + j < T ? y[size_t(t0 + j0 + j) * N + n] : 0.0f;
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) emit(j0 + j, r[j]);
       }
@@ -394,6 +402,10 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
                                        : recv[((z < rank ? z : z - 1) * cpr + c) * kTileM + row];
           if (FMT == kINT8) a += Acc32(int(u));
           else a += Acc32(__uint_as_float(u));
+        }
+        if (EPI == kEpiResid) {
+          const int tt = t0 + rank * cpr + c;
+          prev[(rank * cpr + c) & 15] = tt < T ? y[size_t(tt) * N + n] : 0.0f;
         }
         emit(rank * cpr + c, FMT == kINT8 ? uint32_t(int(a)) : __float_as_uint(float(a)));
       }

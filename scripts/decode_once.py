@@ -20,7 +20,7 @@ ap.add_argument("--reps", type=int, default=1)
 a = ap.parse_args()
 modes = [a.mode] if a.mode != 4 else [0, 4]
 eng = Engine(engine_cfg(target=a.target, draft="llama1b" if a.mode == 4 else None, modes=modes,
-                        kv_blocks=128, max_seq_len=a.prompt + a.new + 32, use_graphs=bool(a.graphs)))
+                        kv_blocks=max(128, (a.prompt + a.new + 64) // 16 + 8), max_seq_len=a.prompt + a.new + 32, use_graphs=bool(a.graphs)))
 p = np.random.default_rng(0).integers(0, eng.vocab, size=a.prompt).astype(np.int32)
 for rep in range(a.reps):
     r = eng.run(a.mode, p, a.new)
