@@ -340,6 +340,14 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     }
   };
   if (warp < 4) {
+    // residual epilogue: pull this row's y values for the tile's tokens into L2
+    // while the mainloop runs, so the epilogue's reads are L2 hits
+    if (EPI == kEpiResid) {  // split-K: only the columns this cluster rank finishes
+      const int c0 = ksplit == 1 ? 0 : int(cluster_ctarank()) * (BN / ksplit);
+      const int c1 = min(ksplit == 1 ? BN : c0 + BN / ksplit, T - t0);
+      for (int j = c0; j < c1; ++j)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(y + size_t(t0 + j) * N + n));
+    }
     mbar_wait(done, 0);
     tc_fence_after();
   }
