@@ -346,8 +346,8 @@ __device__ __forceinline__ int split_chunk_dec(int ctx, int nsplit) {
 //    the last CTA to finish (atomic counter) combines them, so there is no
 //    separate combine launch.
 
-template <int D, int G>
-__global__ void __launch_bounds__(kDecWarps * 32)
+template <int D, int G, int W>
+__global__ void __launch_bounds__(W * 32)
     attn_decode_kernel(const float* __restrict__ qkv, const float2* __restrict__ rope,
                        const int* __restrict__ pos, const int* __restrict__ slot,
                        const int* __restrict__ seq_of, const int* __restrict__ block_table,
@@ -363,8 +363,8 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   __shared__ __align__(16) half knew_all[kRunMax][D], vnew_all[kRunMax][D];
   half* const knew = knew_all[0];
   half* const vnew = vnew_all[0];
-  __shared__ float wm[kDecWarps][G], wl[kDecWarps][G];
-  __shared__ float wacc[kDecWarps][G][D];
+  __shared__ float wm[W][G], wl[W][G];
+  __shared__ float wacc[W][G][D];
   __shared__ int is_last;
   const int t = blockIdx.x, hk = blockIdx.y, sp = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -411,12 +411,12 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   if (first < end) stage_tile(first);  // cache history only: safe before the wait
   // the RoPE row of this position is a cold table row: fetch it before the wait
   // too (pos was written by the previous step's advance, long complete)
-  constexpr int kRopeIt = ((G + 1) * (D / 2) + kDecWarps * 32 - 1) / (kDecWarps * 32);
+  constexpr int kRopeIt = ((G + 1) * (D / 2) + W * 32 - 1) / (W * 32);
   const float2* rp = rope + size_t(p_self) * (D / 2);
   float2 rr[kRopeIt];
 #pragma unroll
   for (int it = 0; it < kRopeIt; ++it) {
-    const int i = threadIdx.x + it * kDecWarps * 32;
+    const int i = threadIdx.x + it * W * 32;
     if (i < (G + 1) * (D / 2)) rr[it] = rp[i % (D / 2)];
   }
 
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     const float* row = qkv + size_t(t) * (Hq + 2 * Hk) * D;
 #pragma unroll
     for (int it = 0; it < kRopeIt; ++it) {
-      const int i = threadIdx.x + it * kDecWarps * 32;
+      const int i = threadIdx.x + it * W * 32;
       if (i >= (G + 1) * (D / 2)) break;
       const int h = i / (D / 2), j = i % (D / 2);
       const float* src = h < G ? row + size_t(hk * G + h) * D : row + size_t(Hq + hk) * D;
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
 #pragma unroll
   for (int dt = 0; dt < DT; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.0f;
 #pragma unroll 1
-  for (int base = first; base < end; base += kDecWarps * 32) {
+  for (int base = first; base < end; base += W * 32) {
     if (base != first) {
       __syncwarp();
       stage_tile(base);
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     for (int d = 0; d < DPL; ++d) acc[g][d] = 0.0f;
   }
 #pragma unroll 1
-  for (int base = first; base < end; base += kDecWarps * 32) {
+  for (int base = first; base < end; base += W * 32) {
     if (base != first) {
       __syncwarp();
       stage_tile(base);
@@ -678,10 +678,10 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
     const int g = i / D, d = i % D;
     float M = -INFINITY;
-    for (int w = 0; w < kDecWarps; ++w) M = fmaxf(M, wm[w][g]);
+    for (int w = 0; w < W; ++w) M = fmaxf(M, wm[w][g]);
     float L = 0.0f, A = 0.0f;
     if (M != -INFINITY)
-      for (int w = 0; w < kDecWarps; ++w) {
+      for (int w = 0; w < W; ++w) {
         const float f = __expf(wm[w][g] - M);
         L += wl[w][g] * f;
         A += wacc[w][g][d] * f;
@@ -836,19 +836,28 @@ void launch_attention_decode(const float* qkv, const float2* rope, int T, const 
                              float* part_ml, int* counters, float* o, cudaStream_t st, bool run) {
   const int G = a.n_heads / a.n_kv_heads;
   if (run && T > kRunMax) throw ConfigErr("attention: a one-sequence run is at most 6 tokens");
-  const dim3 grid(T, a.n_kv_heads, nsplit), thr(kDecWarps * 32);
-#define MSW_DEC(DD, GG)                                                                       \
-  if (a.head_dim == DD && G == GG) {                                                          \
-    const size_t smem = size_t(kDecWarps) * 2 * 32 * (DD + kKvPad) * sizeof(half);            \
+  const dim3 grid(T, a.n_kv_heads, nsplit);
+  // many (token, kv head, split) CTAs (continuous batching): 4-warp CTAs use
+  // 70 KB of staging instead of 139 KB, so three are resident per SM and more
+  // KV is in flight; a few CTAs (batch-1 decode): 8 warps for latency
+  const bool wide = size_t(T) * a.n_kv_heads * nsplit >= size_t(2) * kNumSMs;
+#define MSW_DEC_W(DD, GG, WW)                                                                 \
+  {                                                                                           \
+    const size_t smem = size_t(WW) * 2 * 32 * (DD + kKvPad) * sizeof(half);                   \
     static bool attr = false;                                                                 \
     if (!attr) {                                                                              \
-      MSW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<DD, GG>,                               \
+      MSW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<DD, GG, WW>,                           \
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
       attr = true;                                                                            \
     }                                                                                         \
-    return launch_pdl(attn_decode_kernel<DD, GG>, grid, thr, smem, st, qkv, rope, pos,        \
-                      slot, seq_of, block_table, a.max_blocks_per_seq, kc, vc, a.n_heads,     \
-                      a.n_kv_heads, nsplit, part_o, part_ml, counters, o, run ? 1 : 0);       \
+    return launch_pdl(attn_decode_kernel<DD, GG, WW>, grid, dim3(WW * 32), smem, st, qkv,     \
+                      rope, pos, slot, seq_of, block_table, a.max_blocks_per_seq, kc, vc,     \
+                      a.n_heads, a.n_kv_heads, nsplit, part_o, part_ml, counters, o,          \
+                      run ? 1 : 0);                                                           \
+  }
+#define MSW_DEC(DD, GG)                                  \
+  if (a.head_dim == DD && G == GG) {                     \
+    if (wide) MSW_DEC_W(DD, GG, 4) else MSW_DEC_W(DD, GG, 8) \
   }
   MSW_DEC(128, 1)
   MSW_DEC(128, 2)
@@ -859,6 +868,7 @@ void launch_attention_decode(const float* qkv, const float2* rope, int T, const 
   MSW_DEC(64, 4)
   MSW_DEC(64, 8)
 #undef MSW_DEC
+#undef MSW_DEC_W
   throw ConfigErr("attention: unsupported head_dim / GQA group");
 }
 
