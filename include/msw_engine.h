@@ -40,6 +40,7 @@ enum {
   MSW_MODE_FP16 = 0,
   MSW_MODE_INT8 = 1,
   MSW_MODE_GPTQ4 = 2,
+  MSW_MODE_AWQ4 = 3,            /* AWQ-format W4: asymmetric g128 (scale + zero point) (screening mode) */
   MSW_MODE_SPECULATIVE = 4,
   MSW_MODE_CHUNKED_PREFILL = 6, /* FP16, prefill in 512-token chunks (screening mode) */
   MSW_MODE_CUDA_GRAPHS = 8,     /* FP16, graph-replayed decode (screening mode) */
@@ -48,7 +49,7 @@ enum {
 };
 
 /* Weight formats of a linear layer. */
-enum { MSW_W_FP16 = 0, MSW_W_INT8 = 1, MSW_W_W4G128 = 2 };
+enum { MSW_W_FP16 = 0, MSW_W_INT8 = 1, MSW_W_W4G128 = 2, MSW_W_AWQ4 = 3 };
 
 #define MSW_KV_BLOCK 16 /* tokens per paged-KV block */
 #define MSW_W4_GROUP 128

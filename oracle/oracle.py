@@ -37,6 +37,8 @@ def lib() -> C.CDLL:
         L.orc_gemv_i8_acc.argtypes = [vp, vp, i32, i32, vp]
         L.orc_linear.argtypes = [C.c_int, vp, vp, i32, i32, vp, i32, vp]
         L.orc_model_tensor.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp]
+        L.orc_quant_awq4_rows.argtypes = [vp, i32, i32, vp, vp, vp]
+        L.orc_linear_awq4.argtypes = [vp, vp, vp, i32, i32, vp, i32, vp]
         _lib = L
     return _lib
 
@@ -81,7 +83,7 @@ class OracleModel:
     def tensor(self, which: int, layer: int = 0, fmt: int = 0):
         """One weight tensor: fp16 array (fmt 0 / norms / embed / lm_head), or
         (q int8 [n,k], s fp32 [n]) for fmt 1, (q nibble-per-byte [n,k], s fp16
-        [n,k/128]) for fmt 2."""
+        [n,k/128]) for fmt 2 (GPTQ4) and 3 (AWQ4); fmt 4: AWQ4 zeros [n,k/128]."""
         c = self.cfg
         H, V, F, D = c.hidden, c.vocab, c.ffn, c.head_dim
         if which in (self.EMBED, self.LM_HEAD):
@@ -96,6 +98,8 @@ class OracleModel:
             s = None
         elif fmt == 1:
             w, s = np.zeros(shape, np.int8), np.zeros(shape[0], np.float32)
+        elif fmt == 4:  # AWQ4 zero points
+            w, s = np.zeros((shape[0], shape[1] // 128), np.uint8), None
         else:
             w, s = np.zeros(shape, np.uint8), np.zeros((shape[0], shape[1] // 128), np.float16)
         rc = lib().orc_model_tensor(self.h, which, layer, fmt, _p(w), _p(s) if s is not None else None)
@@ -138,6 +142,25 @@ def quant_w4_rows(w: np.ndarray):
     s = np.zeros((n, k // 128), dtype=np.uint16)
     lib().orc_quant_w4_rows(_p(np.ascontiguousarray(w)), n, k, _p(q), _p(s))
     return q, s
+
+
+def quant_awq4_rows(w: np.ndarray):
+    """AWQ format: q nibble-per-byte [n,k], fp16-bit scales and uint8 zeros [n,k/128]."""
+    n, k = w.shape
+    q = np.zeros((n, k), dtype=np.uint8)
+    s = np.zeros((n, k // 128), dtype=np.uint16)
+    z = np.zeros((n, k // 128), dtype=np.uint8)
+    lib().orc_quant_awq4_rows(_p(np.ascontiguousarray(w)), n, k, _p(q), _p(s), _p(z))
+    return q, s, z
+
+
+def linear_awq4(q: np.ndarray, s: np.ndarray, z: np.ndarray, x: np.ndarray) -> np.ndarray:
+    n, k = q.shape
+    x = np.ascontiguousarray(x, dtype=np.float32).reshape(-1, k)
+    y = np.zeros((x.shape[0], n), dtype=np.float32)
+    lib().orc_linear_awq4(_p(np.ascontiguousarray(q)), _p(np.ascontiguousarray(s)),
+                          _p(np.ascontiguousarray(z)), n, k, _p(x), x.shape[0], _p(y))
+    return y
 
 
 def gemv_i8_acc(w: np.ndarray, x: np.ndarray) -> np.ndarray:

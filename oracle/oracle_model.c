@@ -119,6 +119,38 @@ void orc_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* q_out,
     }
 }
 
+/* AWQ format (AutoAWQ pseudo_quantize_tensor, zero_point=True, w_bit 4,
+ * group 128): per group s = (max - min) / 15 (clamped to >= 1e-5) rounded to
+ * fp16, z = clamp(-rint(min / s), 0, 15), q = clamp(rint(w / s) + z, 0, 15),
+ * w' = (q - z) * s. The activation-aware per-channel scale search is an
+ * offline calibration step (needs activation statistics) and is identity here. */
+void orc_quant_awq4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* q_out,
+                         uint16_t* scales, uint8_t* zeros) {
+  const int32_t groups = k / MSW_W4_GROUP;
+#pragma omp parallel for schedule(static)
+  for (int32_t r = 0; r < n; ++r)
+    for (int32_t g = 0; g < groups; ++g) {
+      const uint16_t* src = w + (int64_t)r * k + (int64_t)g * MSW_W4_GROUP;
+      float mx = -INFINITY, mn = INFINITY;
+      for (int i = 0; i < MSW_W4_GROUP; ++i) {
+        mx = fmaxf(mx, h2f(src[i]));
+        mn = fminf(mn, h2f(src[i]));
+      }
+      const h16 sh = f2h(fmaxf(mx - mn, 1e-5f) / 15.0f);
+      const float s = h2f(sh);
+      float zf = -rintf(mn / s);
+      zf = zf < 0.0f ? 0.0f : (zf > 15.0f ? 15.0f : zf);
+      const int z = (int)zf;
+      scales[(int64_t)r * groups + g] = sh;
+      zeros[(int64_t)r * groups + g] = (uint8_t)z;
+      for (int i = 0; i < MSW_W4_GROUP; ++i) {
+        int q = (int)rintf(h2f(src[i]) / s) + z;
+        q = q < 0 ? 0 : (q > 15 ? 15 : q);
+        q_out[(int64_t)r * k + (int64_t)g * MSW_W4_GROUP + i] = (uint8_t)q;
+      }
+    }
+}
+
 void orc_gemv_i8_acc(const int8_t* w, const int8_t* x, int32_t n, int32_t k,
                      int32_t* acc) {
 #pragma omp parallel for schedule(static)
@@ -160,8 +192,8 @@ static void linear_fp16(const h16* w, int32_t n, int32_t k, const float* x16,
   }
 }
 
-static void linear_w4(const uint8_t* q, const h16* s, int32_t n, int32_t k,
-                      const float* x16, float* y) {
+static void linear_w4(const uint8_t* q, const h16* s, const uint8_t* zeros, int32_t n,
+                      int32_t k, const float* x16, float* y) {
   const int32_t groups = k / MSW_W4_GROUP;
 #pragma omp parallel
   {
@@ -171,7 +203,8 @@ static void linear_w4(const uint8_t* q, const h16* s, int32_t n, int32_t k,
       for (int32_t g = 0; g < groups; ++g) {
         float lut[16];
         const float sc = h2f(s[(int64_t)r * groups + g]);
-        for (int v = 0; v < 16; ++v) lut[v] = rnd16((float)(v - 8) * sc);
+        const int z = zeros ? zeros[(int64_t)r * groups + g] : 8;  /* GPTQ uint4b8: zero 8 */
+        for (int v = 0; v < 16; ++v) lut[v] = rnd16((float)(v - z) * sc);
         const uint8_t* src = q + (int64_t)r * k + (int64_t)g * MSW_W4_GROUP;
         for (int i = 0; i < MSW_W4_GROUP; ++i) row[g * MSW_W4_GROUP + i] = lut[src[i]];
       }
@@ -206,6 +239,16 @@ static void linear_i8(const int8_t* w, const float* ws, int32_t n, int32_t k,
   free(qx);
 }
 
+void orc_linear_awq4(const uint8_t* q, const uint16_t* scales, const uint8_t* zeros, int32_t n,
+                     int32_t k, const float* x, int32_t t, float* y) {
+  float* x16 = (float*)malloc(sizeof(float) * (size_t)k);
+  for (int32_t i = 0; i < t; ++i) {
+    for (int32_t c = 0; c < k; ++c) x16[c] = rnd16(x[(int64_t)i * k + c]);
+    linear_w4(q, (const h16*)scales, zeros, n, k, x16, y + (int64_t)i * n);
+  }
+  free(x16);
+}
+
 void orc_linear(int wtype, const void* w, const void* scales, int32_t n,
                 int32_t k, const float* x, int32_t t, float* y) {
   float* x16 = (float*)malloc(sizeof(float) * (size_t)k);
@@ -220,15 +263,16 @@ void orc_linear(int wtype, const void* w, const void* scales, int32_t n,
     if (wtype == MSW_W_FP16)
       linear_fp16((const h16*)w, n, k, x16, yi);
     else
-      linear_w4((const uint8_t*)w, (const h16*)scales, n, k, x16, yi);
+      linear_w4((const uint8_t*)w, (const h16*)scales, NULL, n, k, x16, yi);
   }
   free(x16);
 }
 
 /* -------------------------------------------------------------- model --- */
 typedef struct {
-  void* w[3];        /* per format: fp16 h16*, int8 int8_t*, w4 uint8_t* (nibble/byte) */
-  void* s[3];        /* NULL, float* [n], h16* [n, k/128] */
+  void* w[4];        /* per format: fp16 h16*, int8 int8_t*, w4 / awq4 uint8_t* (nibble/byte) */
+  void* s[4];        /* NULL, float* [n], h16* [n, k/128], h16* [n, k/128] */
+  uint8_t* z;        /* awq4 zero points [n, k/128] */
   int32_t n, k;
 } orc_lin;
 
@@ -256,7 +300,9 @@ struct orc_model {
 };
 
 static int fmt_of_mode(int mode) {
-  return mode == MSW_MODE_INT8 ? MSW_W_INT8 : (mode == MSW_MODE_GPTQ4 ? MSW_W_W4G128 : MSW_W_FP16);
+  return mode == MSW_MODE_INT8 ? MSW_W_INT8
+       : mode == MSW_MODE_GPTQ4 ? MSW_W_W4G128
+       : mode == MSW_MODE_AWQ4 ? MSW_W_AWQ4 : MSW_W_FP16;
 }
 
 static void build_lin(orc_lin* L, const orc_model* m, int32_t n, int32_t k,
@@ -273,6 +319,7 @@ static void build_lin(orc_lin* L, const orc_model* m, int32_t n, int32_t k,
   }
   memset(L->w, 0, sizeof L->w);
   memset(L->s, 0, sizeof L->s);
+  L->z = NULL;
   if (m->modes & ((1u << MSW_MODE_FP16) | (1u << MSW_MODE_SPECULATIVE))) {
     L->w[MSW_W_FP16] = full;
   }
@@ -286,14 +333,21 @@ static void build_lin(orc_lin* L, const orc_model* m, int32_t n, int32_t k,
     L->s[MSW_W_W4G128] = malloc(sizeof(h16) * (size_t)n * (k / MSW_W4_GROUP));
     orc_quant_w4_rows(full, n, k, (uint8_t*)L->w[MSW_W_W4G128], (h16*)L->s[MSW_W_W4G128]);
   }
+  if (m->modes & (1u << MSW_MODE_AWQ4)) {
+    L->w[MSW_W_AWQ4] = malloc((size_t)n * k);
+    L->s[MSW_W_AWQ4] = malloc(sizeof(h16) * (size_t)n * (k / MSW_W4_GROUP));
+    L->z = (uint8_t*)malloc((size_t)n * (k / MSW_W4_GROUP));
+    orc_quant_awq4_rows(full, n, k, (uint8_t*)L->w[MSW_W_AWQ4], (h16*)L->s[MSW_W_AWQ4], L->z);
+  }
   if (L->w[MSW_W_FP16] != full) free(full);
 }
 
 static void free_lin(orc_lin* L) {
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     free(L->w[i]);
     free(L->s[i]);
   }
+  free(L->z);
 }
 
 typedef struct {
@@ -470,11 +524,15 @@ int orc_model_tensor(orc_model* m, int which, int layer, int fmt, void* w, void*
   }
   const orc_lin* L = which == 5 ? &ly->qkv : which == 6 ? &ly->o : which == 7 ? &ly->gate
                    : which == 8 ? &ly->up : which == 9 ? &ly->down : NULL;
-  if (!L || fmt < 0 || fmt > 2 || !L->w[fmt]) return -1;
+  if (!L || fmt < 0 || fmt > 4 || !L->w[fmt == 4 ? 3 : fmt]) return -1;
   const size_t nk = (size_t)L->n * L->k;
+  if (fmt == 4) {  /* awq4 zero points [n, k/128] */
+    memcpy(w, L->z, (size_t)L->n * (L->k / MSW_W4_GROUP));
+    return 0;
+  }
   memcpy(w, L->w[fmt], fmt == 0 ? sizeof(h16) * nk : nk);
   if (fmt == 1) memcpy(s, L->s[1], sizeof(float) * (size_t)L->n);
-  if (fmt == 2) memcpy(s, L->s[2], sizeof(h16) * (size_t)L->n * (L->k / MSW_W4_GROUP));
+  if (fmt >= 2) memcpy(s, L->s[fmt], sizeof(h16) * (size_t)L->n * (L->k / MSW_W4_GROUP));
   return 0;
 }
 int orc_threads(void) { return omp_get_max_threads(); }
@@ -488,7 +546,10 @@ static void rmsnorm(const float* x, const h16* g, int32_t n, float eps, float* y
 }
 
 static void lin(const orc_lin* L, int fmt, const float* x, float* y) {
-  orc_linear(fmt, L->w[fmt], L->s[fmt], L->n, L->k, x, 1, y);
+  if (fmt == MSW_W_AWQ4)
+    orc_linear_awq4((const uint8_t*)L->w[fmt], (const uint16_t*)L->s[fmt], L->z, L->n, L->k, x, 1, y);
+  else
+    orc_linear(fmt, L->w[fmt], L->s[fmt], L->n, L->k, x, 1, y);
 }
 
 /* One decoder step for token `tok` at position `pos`; writes logits [V]. */

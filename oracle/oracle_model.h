@@ -45,7 +45,7 @@ orc_model* orc_model_create(const msw_model_cfg* cfg, uint64_t seed,
                             uint32_t modes_mask, int32_t max_ctx);
 void orc_model_destroy(orc_model* m);
 
-/* Greedy generation in one mode (FP16=0, INT8=1, GPTQ4=2). logits optional
+/* Greedy generation in one mode (FP16=0, INT8=1, GPTQ4=2, AWQ4=3). logits optional
  * [n_new, vocab]. Returns 0 on success. */
 int orc_generate(orc_model* m, int mode, const int32_t* prompt, int plen,
                  int n_new, int32_t* out, float* logits);
@@ -69,6 +69,12 @@ void orc_quant_int8_rows(const uint16_t* w, int32_t n, int32_t k, int8_t* q,
 /* q_out: one nibble value (0..15) per byte, [n, k]; scales fp16 [n, k/128] */
 void orc_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* q_out,
                        uint16_t* scales);
+/* AWQ format, asymmetric group-128: q nibble-per-byte [n, k], fp16 scales and
+ * uint8 zero points [n, k/128]; w' = (q - z) * s. */
+void orc_quant_awq4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* q_out,
+                         uint16_t* scales, uint8_t* zeros);
+void orc_linear_awq4(const uint8_t* q, const uint16_t* scales, const uint8_t* zeros, int32_t n,
+                     int32_t k, const float* x, int32_t t, float* y);
 void orc_gemv_i8_acc(const int8_t* w, const int8_t* x, int32_t n, int32_t k,
                      int32_t* acc);
 /* y[t,n] = sum_k W[n,k] x[t,k] with the mode's activation handling. */
@@ -82,7 +88,8 @@ int orc_threads(void);
  *        3 attn_norm [h], 4 ffn_norm [h] (layer l),
  *        5 qkv, 6 o, 7 gate, 8 up, 9 down (layer l, format fmt):
  *          fmt 0: w fp16 [n,k];   fmt 1: w int8 [n,k], s fp32 [n];
- *          fmt 2: w nibble-per-byte [n,k], s fp16 [n,k/128].
+ *          fmt 2 (GPTQ4) / 3 (AWQ4): w nibble-per-byte [n,k], s fp16 [n,k/128];
+ *          fmt 4: the AWQ4 zero points uint8 [n,k/128] into w.
  * Returns 0, or -1 if the tensor/format is not resident. */
 int orc_model_tensor(orc_model* m, int which, int layer, int fmt, void* w, void* s);
 

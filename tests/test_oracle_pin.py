@@ -60,9 +60,10 @@ def _hf_model(orc, fmt):
         if fmt == 1:
             q, s = orc.tensor(which, layer, 1)
             return t(q), t(s)   # W8A8 modules take (q, s)
-        q, s = orc.tensor(which, layer, 2)
-        deq = (q.astype(np.float32) - 8.0) * np.repeat(s.astype(np.float32), 128, axis=1)
-        return t(deq.astype(np.float16))   # GPTQ4 dequant rounded to fp16
+        q, s = orc.tensor(which, layer, fmt)
+        zero = 8.0 if fmt == 2 else np.repeat(orc.tensor(which, layer, 4).astype(np.float32), 128, axis=1)
+        deq = (q.astype(np.float32) - zero) * np.repeat(s.astype(np.float32), 128, axis=1)
+        return t(deq.astype(np.float16))   # GPTQ4 / AWQ4 dequant rounded to fp16
 
     sd = {"model.embed_tokens.weight": t(orc.tensor(orc.EMBED)),
           "lm_head.weight": t(orc.tensor(orc.LM_HEAD)),
@@ -115,7 +116,7 @@ def _w8a8_forward(q, s):
 
 @pytest.fixture(scope="module")
 def orc():
-    m = O.OracleModel(model_cfg("tiny"), seed=SEED, max_ctx=512)
+    m = O.OracleModel(model_cfg("tiny"), seed=SEED, max_ctx=512, modes_mask=0xFFF)
     yield m
     m.close()
 
@@ -135,7 +136,7 @@ def _rel(a, b):
 # transformers stays fp32, so the two differ by fp16 activation rounding.
 # INT8: the same W8A8 arithmetic; only fp32 summation order and the fp16
 # rounding of q/k/v differ (which can flip an int8 activation rounding).
-@pytest.mark.parametrize("mode,fmt,tol", [(0, 0, 5e-3), (2, 2, 5e-3), (1, 1, 2e-2)])
+@pytest.mark.parametrize("mode,fmt,tol", [(0, 0, 5e-3), (2, 2, 5e-3), (1, 1, 2e-2), (3, 3, 5e-3)])
 def test_oracle_matches_transformers_llama(orc, mode, fmt, tol):
     toks, lg = orc.generate(mode, PROMPT, N_NEW, want_logits=True)
     hf = _hf_model(orc, fmt)
@@ -200,3 +201,22 @@ def test_oracle_w4_scale_rule_is_gptq_symmetric(orc):
     sf = sc.astype(np.float32)[..., None]
     qq = np.clip(np.rint(wf / np.where(sf > 0, sf, 1)) + 8, 0, 15)
     assert np.array_equal(qq.reshape(q.shape).astype(np.uint8), q)
+
+
+def test_oracle_awq4_matches_autoawq_pseudo_quantize(orc):
+    """orc_quant_awq4_rows restates AutoAWQ's pseudo_quantize_tensor
+    (zero_point=True, w_bit=4, q_group_size=128): scales = (max - min).clamp(
+    min=1e-5) / 15, zeros = (-round(min / scales)).clamp(0, 15), q = clamp(
+    round(w / scales) + zeros, 0, 15), with the scale stored as fp16 first."""
+    w = orc.tensor(orc.DOWN, 0, 0)
+    q, s = orc.tensor(orc.DOWN, 0, 3)
+    z = orc.tensor(orc.DOWN, 0, 4)
+    wf = torch.from_numpy(w.astype(np.float32)).reshape(w.shape[0], -1, 128)
+    mx, mn = wf.amax(dim=2, keepdim=True), wf.amin(dim=2, keepdim=True)
+    sc = ((mx - mn).clamp(min=1e-5) / 15).half().float()
+    zz = (-torch.round(mn / sc)).clamp(0, 15)
+    qq = torch.clamp(torch.round(wf / sc) + zz, 0, 15)
+    assert np.array_equal(sc.squeeze(2).half().numpy(), s)
+    assert np.array_equal(zz.squeeze(2).numpy().astype(np.uint8), z)
+    assert np.array_equal(qq.reshape(q.shape).numpy().astype(np.uint8), q)
+    assert len(np.unique(z)) > 1  # zero points vary per group (uniform init: 7 or 8)
