@@ -170,6 +170,15 @@ int msw_fill_fp16(uint16_t* dst, int64_t rows, int64_t cols, uint64_t seed,
 /* Quantisers used at engine init, exposed for parity tests. */
 int msw_quant_int8_rows(const uint16_t* w, int32_t n, int32_t k, int8_t* q,
                         float* scales, void* stream);
+/* AWQ4 (AWQ format: asymmetric group-128, y = sum_g s_g sum (q - z_g) x):
+ * w row-packed words [n][k/8] as W4, fp16 scales and uint8 zero points
+ * [n][k/128]; same dispatch as msw_linear (decode GEMV t <= 6, tcgen05 GEMM). */
+int msw_linear_awq4(const void* w, const void* scales, const uint8_t* zeros, int32_t n, int32_t k,
+                    const float* x, int32_t t, float* y, void* stream);
+/* AWQ4 quantiser (AutoAWQ pseudo_quantize_tensor, zero_point=True), bit-identical
+ * to oracle/orc_quant_awq4_rows (packing as msw_quant_w4_rows). */
+int msw_quant_awq4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* packed, uint16_t* scales,
+                        uint8_t* zeros, void* stream);
 int msw_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* packed,
                       uint16_t* scales, void* stream);
 

@@ -44,6 +44,8 @@ int fmt_of_mode(int mode) {
     case MSW_MODE_GPTQ4:
     case MSW_MODE_GPTQ_PREFIX_CACHING:
       return kW4;
+    case MSW_MODE_AWQ4:
+      return kSlotAWQ4;
     default:
       throw ConfigErr("unsupported mode id " + std::to_string(mode));
   }
@@ -148,13 +150,13 @@ class BlockPool {
 struct Layer {
   half* attn_norm = nullptr;
   half* ffn_norm = nullptr;
-  LinearW qkv[3], o[3], gu[3], down[3];
+  LinearW qkv[kSlots], o[kSlots], gu[kSlots], down[kSlots];  // per weight slot
 };
 
 struct Model {
   msw_model_cfg c{};
   bool is_draft = false;
-  bool fmt_on[3] = {false, false, false};
+  bool fmt_on[kSlots] = {false, false, false, false};
   half* embed = nullptr;
   half* lm_head = nullptr;
   half* lm_head_tf = nullptr;  // decode (tile-fragment) copy
@@ -173,8 +175,8 @@ struct Model {
   AttnShape ash{};
   BlockPool pool;
   std::vector<void*> allocations;
-  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
-  int graph_nodes[3] = {0, 0, 0};
+  cudaGraphExec_t graph[kSlots] = {nullptr, nullptr, nullptr, nullptr};
+  int graph_nodes[kSlots] = {0, 0, 0, 0};
 
   size_t weight_bytes(int fmt) const {
     size_t b = size_t(c.vocab) * c.hidden * 2;  // fp16 lm_head in every mode
@@ -258,8 +260,9 @@ T* model_alloc(Model& m, size_t count) {
   return p;
 }
 
-LinearW make_linear(Model& m, int fmt, const half* master, int n, int k, cudaStream_t st) {
+LinearW make_linear(Model& m, int slot, const half* master, int n, int k, cudaStream_t st) {
   LinearW L;
+  const int fmt = slot == kSlotAWQ4 ? kW4 : slot;  // AWQ4: W4 layout plus zero points
   L.fmt = fmt;
   L.n = n;
   L.k = k;
@@ -273,6 +276,14 @@ LinearW make_linear(Model& m, int fmt, const half* master, int n, int k, cudaStr
     launch_quant_int8(master, n, k, q, s, st);
     L.w = q;
     L.s = s;
+  } else if (slot == kSlotAWQ4) {
+    uint32_t* q = model_alloc<uint32_t>(m, size_t(n) * k / 8);
+    half* s = model_alloc<half>(m, size_t(n) * (k / kW4Group));
+    uint8_t* z = model_alloc<uint8_t>(m, size_t(n) * (k / kW4Group));
+    launch_quant_awq4(master, n, k, q, s, z, st);
+    L.w = q;
+    L.s = s;
+    L.z = z;
   } else {
     uint32_t* q = model_alloc<uint32_t>(m, size_t(n) * k / 8);
     half* s = model_alloc<half>(m, size_t(n) * (k / kW4Group));
@@ -325,6 +336,7 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
                             (1u << MSW_MODE_CHUNKED_PREFILL) | (1u << MSW_MODE_CUDA_GRAPHS));
     m.fmt_on[kINT8] = mm & ((1u << MSW_MODE_INT8) | (1u << MSW_MODE_INT8_CONT_BATCHING));
     m.fmt_on[kW4] = mm & ((1u << MSW_MODE_GPTQ4) | (1u << MSW_MODE_GPTQ_PREFIX_CACHING));
+    m.fmt_on[kSlotAWQ4] = mm & (1u << MSW_MODE_AWQ4);
   }
 
   const size_t max_elems = std::max({size_t(Hq + 2 * Hk) * D * H, size_t(2) * F * H,
@@ -340,8 +352,8 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
     ly.ffn_norm = model_alloc<half>(m, H);
     launch_fill_norm(ly.attn_norm, H, seed, base + tid_layer(l, kAttnNorm), st);
     launch_fill_norm(ly.ffn_norm, H, seed, base + tid_layer(l, kFfnNorm), st);
-    auto each_fmt = [&](LinearW (&dst)[3], int n, int k) {
-      for (int f = 0; f < 3; ++f)
+    auto each_fmt = [&](LinearW (&dst)[kSlots], int n, int k) {
+      for (int f = 0; f < kSlots; ++f)
         if (m.fmt_on[f]) dst[f] = make_linear(m, f, master, n, k, st);
     };
     // qkv: rows [q (Hq*D); k (Hk*D); v (Hk*D)]
@@ -507,6 +519,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
   const int H = c.hidden, D = c.head_dim, Hq = c.n_heads, Hk = c.n_kv_heads, F = c.ffn;
   const float eps = c.rms_eps;
   const bool small = T <= kGemvMaxTokens;
+  const int kfmt = fmt == kSlotAWQ4 ? kW4 : fmt;  // activation handling of the weight slot
   // attention splits: enough CTAs to fill the GPU, fewer as the token count grows
   int nsplit = 1;
   if (T <= kMaxLogitRows) nsplit = std::max(1, std::min(m.nsplit, (2 * kNumSMs) / (T * Hk)));
@@ -530,7 +543,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
         launch_gemv(ly.qkv[fmt], kProNorm, kEpiStore, s.h, T, ly.attn_norm, eps, s.qkv, st, &ly.o[fmt]);
       ++n;
     } else {
-      launch_prep_act(fmt, s.h, T, H, ly.attn_norm, eps, s.xh, s.xq, s.xscale, st);
+      launch_prep_act(kfmt, s.h, T, H, ly.attn_norm, eps, s.xh, s.xq, s.xscale, st);
       launch_gemm(ly.qkv[fmt], kEpiStore, s.xh, s.xq, s.xscale, T, s.qkv, st);
       n += 2;
     }
@@ -561,11 +574,11 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
         launch_gemv(ly.down[fmt], kProPlain, kEpiResid, s.act, T, nullptr, eps, s.h, st, after_down);
       n += 3;
     } else {
-      launch_prep_act(fmt, s.o, T, Hq * D, nullptr, eps, s.xh, s.xq, s.xscale, st);
+      launch_prep_act(kfmt, s.o, T, Hq * D, nullptr, eps, s.xh, s.xq, s.xscale, st);
       launch_gemm(ly.o[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, st);
-      launch_prep_act(fmt, s.h, T, H, ly.ffn_norm, eps, s.xh, s.xq, s.xscale, st);
+      launch_prep_act(kfmt, s.h, T, H, ly.ffn_norm, eps, s.xh, s.xq, s.xscale, st);
       launch_gemm(ly.gu[fmt], kEpiSwiglu, s.xh, s.xq, s.xscale, T, s.act, st);
-      launch_prep_act(fmt, s.act, T, F, nullptr, eps, s.xh, s.xq, s.xscale, st);
+      launch_prep_act(kfmt, s.act, T, F, nullptr, eps, s.xh, s.xq, s.xscale, st);
       launch_gemm(ly.down[fmt], kEpiResid, s.xh, s.xq, s.xscale, T, s.h, st);
       n += 6;
     }
@@ -1346,13 +1359,15 @@ namespace {
 // dispatch (decode GEMV on the tile-fragment layout for t <= 6, prep_act +
 // tcgen05 GEMM otherwise) on row-major weights, with temporary buffers.
 void run_linear_entry(int32_t wtype, const void* w, const void* scales, int32_t n, int32_t k,
-                      const float* x, int32_t t, float* y, int epi, cudaStream_t st) {
+                      const float* x, int32_t t, float* y, int epi, cudaStream_t st,
+                      const uint8_t* zeros = nullptr) {
   LinearW W;
   W.fmt = wtype;
   W.n = n;
   W.k = k;
   W.w = w;
   W.s = scales;
+  W.z = zeros;
   if (t <= kGemvMaxTokens) {
     // weights arrive row-major; build the decode layout first
     uint8_t* tf = dalloc<uint8_t>(tf_bytes(wtype, n, k));
@@ -1441,6 +1456,23 @@ int msw_quant_int8_rows(const uint16_t* w, int32_t n, int32_t k, int8_t* q, floa
   return guarded([&] {
     launch_quant_int8(reinterpret_cast<const half*>(w), n, k, q, scales,
                       static_cast<cudaStream_t>(stream));
+  });
+}
+
+int msw_linear_awq4(const void* w, const void* scales, const uint8_t* zeros, int32_t n, int32_t k,
+                    const float* x, int32_t t, float* y, void* stream) {
+  return guarded([&] {
+    if (!zeros) throw ConfigErr("msw_linear_awq4: zero points required");
+    run_linear_entry(kW4, w, scales, n, k, x, t, y, kEpiStore, static_cast<cudaStream_t>(stream),
+                     zeros);
+  });
+}
+
+int msw_quant_awq4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* packed, uint16_t* scales,
+                        uint8_t* zeros, void* stream) {
+  return guarded([&] {
+    launch_quant_awq4(reinterpret_cast<const half*>(w), n, k, reinterpret_cast<uint32_t*>(packed),
+                      reinterpret_cast<half*>(scales), zeros, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -49,14 +49,16 @@ constexpr int BN = 64;  // weight rows per tile
 constexpr int BK = 32;
 
 template <int FMT>
-__device__ __forceinline__ float dequant(const uint8_t* w, const void* ws, int n, int k, int K) {
+__device__ __forceinline__ float dequant(const uint8_t* w, const void* ws, const uint8_t* wz, int n,
+                                         int k, int K) {
   if (FMT == kFP16) {
     return __half2float(reinterpret_cast<const half*>(w)[size_t(n) * K + k]);
   } else {
     const uint32_t word = reinterpret_cast<const uint32_t*>(w)[size_t(n) * (K / 8) + k / 8];
     const int idx = k & 7;
     const int pos = (idx >> 1) + 4 * (idx & 1);
-    const int q = int((word >> (4 * pos)) & 0xF) - 8;
+    const int zero = wz ? int(wz[size_t(n) * (K / kW4Group) + k / kW4Group]) : 8;  // AWQ / GPTQ
+    const int q = int((word >> (4 * pos)) & 0xF) - zero;
     const half s = static_cast<const half*>(ws)[size_t(n) * (K / kW4Group) + k / kW4Group];
     return __half2float(__hmul(__int2half_rn(q), s));
   }
@@ -66,7 +68,8 @@ template <int FMT, int EPI>
 __global__ void __launch_bounds__(256)
     gemm_tiled_kernel(const uint8_t* __restrict__ w, const void* __restrict__ ws, int N, int K,
                       const half* __restrict__ xh, const int8_t* __restrict__ xq,
-                      const float* __restrict__ xscale, int T, float* __restrict__ y) {
+                      const float* __restrict__ xscale, int T, float* __restrict__ y,
+                      const uint8_t* __restrict__ wz) {
   using Acc = typename std::conditional<FMT == kINT8, int, float>::type;
   __shared__ Acc Xs[BK][BM + 4];
   __shared__ Acc Ws[BK][BN + 4];
@@ -95,7 +98,7 @@ __global__ void __launch_bounds__(256)
       Acc v = 0;
       if (n < N) {
         if (FMT == kINT8) v = Acc(reinterpret_cast<const int8_t*>(w)[size_t(n) * K + k]);
-        else v = Acc(dequant<FMT>(w, ws, n, k, K));
+        else v = Acc(dequant<FMT>(w, ws, wz, n, k, K));
       }
       Ws[kk][nn] = v;
     }
@@ -153,13 +156,13 @@ void gemm_fmt(const LinearW& W, int epi, const half* xh, const int8_t* xq, const
   const dim3 grid(ceil_div(W.n, BN), ceil_div(T, BM));
   const uint8_t* w = static_cast<const uint8_t*>(W.w);
   if (epi == kEpiStore)
-    gemm_tiled_kernel<FMT, kEpiStore><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
+    gemm_tiled_kernel<FMT, kEpiStore><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y, W.z);
   else if (epi == kEpiResid)
-    gemm_tiled_kernel<FMT, kEpiResid><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
+    gemm_tiled_kernel<FMT, kEpiResid><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y, W.z);
   else if (epi == kEpiSwiglu)
-    gemm_tiled_kernel<FMT, kEpiSwiglu><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
+    gemm_tiled_kernel<FMT, kEpiSwiglu><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y, W.z);
   else if (FMT == kINT8 && epi == kEpiRaw)
-    gemm_tiled_kernel<FMT, kEpiRaw><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y);
+    gemm_tiled_kernel<FMT, kEpiRaw><<<grid, 256, 0, st>>>(w, W.s, W.n, W.k, xh, xq, xscale, T, y, W.z);
   else
     throw ConfigErr("gemm: bad epilogue");
   MSW_LAUNCH_CHECK();

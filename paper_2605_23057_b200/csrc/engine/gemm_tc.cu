@@ -178,7 +178,8 @@ template <int FMT, int BN, int EPI>
 __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int N, int K, int T, const void* __restrict__ wscale,
-                   const float* __restrict__ xscale, float* __restrict__ y, int ksplit) {
+                   const float* __restrict__ xscale, float* __restrict__ y, int ksplit,
+                   const uint8_t* __restrict__ wzero) {
   using C = TcCfg<FMT, BN>;
   using Acc32 = typename std::conditional<FMT == kINT8, int, float>::type;
   extern __shared__ uint8_t smem_raw[];
@@ -279,13 +280,17 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     // descriptor reads (no int4 UMMA on sm_100a)
     const int r = (threadIdx.x - 128) & 127, hf = (threadIdx.x - 128) >> 7;
     const half* srow = static_cast<const half*>(wscale) + size_t(n0 + r) * (K / kW4Group);
+    // (1024 + q) - (1024 + zero): zero 8 (GPTQ uint4b8) or the AWQ zero point of the group
+    const uint8_t* zrow = wzero ? wzero + size_t(n0 + r) * (K / kW4Group) : nullptr;
     const half2 k1032 = __float2half2_rn(1032.0f);
     for (int kb = 0; kb < nk; ++kb) {
       const int ps = kb % kPkStages;
       const uint32_t pph = (kb / kPkStages) & 1;
       const int s = kb % C::kStages;
       const uint32_t ph = (kb / C::kStages) & 1;
-      const half2 s2 = __half2half2(srow[((kb0 + kb) * 64) / kW4Group]);
+      const int grp = ((kb0 + kb) * 64) / kW4Group;
+      const half2 s2 = __half2half2(srow[grp]);
+      const half2 kz = zrow ? __float2half2_rn(1024.0f + float(zrow[grp])) : k1032;
       mbar_wait(&pfull[ps], pph);
       const uint4 p0 = reinterpret_cast<const uint4*>(sP + ps * C::kPkBytes + r * 32)[hf];
       __syncwarp();
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           uint32_t u = lop3_and_or(words[cc] >> (4 * i), 0x000F000Fu, 0x64006400u);
-          const half2 q = __hsub2(*reinterpret_cast<const half2*>(&u), k1032);
+          const half2 q = __hsub2(*reinterpret_cast<const half2*>(&u), kz);
           const half2 wv = __hmul2(q, s2);
           out[i] = *reinterpret_cast<const uint32_t*>(&wv);
         }
@@ -516,7 +521,7 @@ void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, f
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   MSW_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<FMT, BN, EPI>, ta, tb, W.n, W.k, T, W.s, xscale,
-                              y, ksplit));
+                              y, ksplit, FMT == kW4 ? W.z : static_cast<const uint8_t*>(nullptr)));
 }
 
 template <int FMT, int EPI>

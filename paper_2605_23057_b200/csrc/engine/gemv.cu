@@ -87,10 +87,15 @@ __device__ __forceinline__ float cons_max(float v, float* red) {
 }
 
 // x fp32 [T, k] -> smem: fp16 [NT][k] (FP16 / W4) or int8 [NT][k] + scale.
+// W4 per-group activation offsets (corr region after the two fp16 copies):
+// GPTQ (zero point 8): C[t][g] = 1032 * Se + 72 * So, one float per group;
+// AWQ (zp: zero point per row and group): B[t][g] = 1024 * Se + 64 * So and
+// S[t][g] = Se + So, the row's offset being B + z * S (Se / So: sums of the
+// fp16-rounded x over the even / odd k16 steps of the group).
 template <int FMT, int PRO, int NT>
 __device__ __forceinline__ void prologue(const float* __restrict__ x, const half* __restrict__ gamma,
                                          float eps, int k, int T, uint8_t* xs, float* red,
-                                         float* xscale) {
+                                         float* xscale, bool zp = false) {
   const int tid = threadIdx.x;
   for (int t = 0; t < (FMT == kW4 ? NT : T); ++t) {  // FP16 / INT8 stage the T real rows only
     const int bytes = FMT == kINT8 ? k : 2 * k;
@@ -175,7 +180,14 @@ __device__ __forceinline__ void prologue(const float* __restrict__ x, const half
             se += __shfl_xor_sync(0xffffffffu, se, o);
             so += __shfl_xor_sync(0xffffffffu, so, o);
           }
-          if (lane == 0) corr[grp] = float(1032.0 * se + 72.0 * so);
+          if (lane == 0) {
+            if (zp) {
+              corr[grp] = float(1024.0 * se + 64.0 * so);
+              corr[size_t(NT) * groups + grp] = float(se + so);
+            } else {
+              corr[grp] = float(1032.0 * se + 72.0 * so);
+            }
+          }
         }
       }
     }
@@ -297,7 +309,7 @@ constexpr int kW4ProRegs = 8;
 template <int PRO>
 __device__ __forceinline__ void prologue_w4_t1(const float* __restrict__ x,
                                                const half* __restrict__ gamma, float eps, int k,
-                                               uint8_t* xs, float* red) {
+                                               uint8_t* xs, float* red, bool zp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k4 = k / 4;
   const float4* xt = reinterpret_cast<const float4*>(x);
@@ -344,7 +356,14 @@ __device__ __forceinline__ void prologue_w4_t1(const float* __restrict__ x,
     gs += __shfl_xor_sync(0xffffffffu, gs, 8);
     gs += __shfl_xor_sync(0xffffffffu, gs, 16);
     const float odd = __shfl_sync(0xffffffffu, gs, 4);
-    if (lane == 0) corr[warp + j * kConsumers] = 1032.0f * gs + 72.0f * odd;
+    if (lane == 0) {
+      if (zp) {  // AWQ: base and group sum (see prologue)
+        corr[warp + j * kConsumers] = 1024.0f * gs + 64.0f * odd;
+        corr[k / kW4Group + warp + j * kConsumers] = gs + odd;
+      } else {
+        corr[warp + j * kConsumers] = 1032.0f * gs + 72.0f * odd;
+      }
+    }
   }
   named_sync(1, kConsThreads);
 }
@@ -376,7 +395,8 @@ template <int FMT, int PRO, int EPI, int NT, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_tf_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
                    const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
-                   float* __restrict__ y, int n_stages, const L2Next nx) {
+                   float* __restrict__ y, int n_stages, const L2Next nx,
+                   const uint8_t* __restrict__ wz) {
   using Acc = typename std::conditional<FMT == kINT8, int, float>::type;
   constexpr int CK = TF<FMT>::kChunkK;
   constexpr int CPW = (S / kConsumers) > TF<FMT>::kMinChunksPerWarp ? (S / kConsumers)
@@ -405,9 +425,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int rows = ntile_cta * 16;
   // FP16 / INT8 stage only the T real token rows (a 5-token FP16 verify at
   // K = 14336 keeps a 3-stage ring instead of 2); W4 keeps NT rows
+  const bool zp = FMT == kW4 && wz != nullptr;  // AWQ zero points (W4 only)
   const int xbytes = FMT == kINT8 ? T * k
-                                  : (FMT == kW4 ? NT * 4 * k + NT * (k / kW4Group) * 4 : T * 2 * k);
-  const int sbytes = FMT == kW4 ? rows * groups_k * 2 : (FMT == kINT8 ? rows * 4 : 0);
+                                  : (FMT == kW4 ? NT * 4 * k + 2 * NT * (k / kW4Group) * 4 : T * 2 * k);
+  const int zbytes = zp ? rows * groups_k : 0;  // uint8 [rows][groups] after the scales
+  const int sbytes = (FMT == kW4 ? rows * groups_k * 2 : (FMT == kINT8 ? rows * 4 : 0)) + zbytes;
   uint8_t* xs = smem;
   uint8_t* sc_smem = smem + ((xbytes + 127) & ~127);
   uint8_t* ring = sc_smem + ((sbytes + 127) & ~127);
@@ -434,7 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint8_t* ssrc = static_cast<const uint8_t*>(ws) +
                               size_t(tile_begin) * 16 * (FMT == kW4 ? groups_k * 2 : 4);
         mbar_expect_tx(&sbar, sbytes);
-        bulk_g2s(sc_smem, ssrc, sbytes, &sbar);
+        bulk_g2s(sc_smem, ssrc, sbytes - zbytes, &sbar);
+        if (zp) bulk_g2s(sc_smem + (sbytes - zbytes), wz + size_t(tile_begin) * 16 * groups_k, zbytes, &sbar);
       }
       const uint8_t* src = wtf + size_t(tile_begin) * chunks_tile * kChunkBytes;
       int s = 0;
@@ -562,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (NT > 1 && FMT != kW4)
     prologue_multi<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red2, xscale);
   else
-    prologue<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red, xscale);
+    prologue<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red, xscale, zp);
   named_sync(3, kConsThreads + 32);  // release the epilogue warp (xscale ready)
   const int g = lane >> 2, tq = lane & 3;
   const bool has_tok = g < T;  // this lane's MMA column is a real token
@@ -629,12 +652,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int grp = c >> 1;
             const float slo = __half2float(sc_h[lr * groups_k + grp]);
             const float shi = __half2float(sc_h[(lr + 8) * groups_k + grp]);
-            const float c0 = corr[(2 * tq < NT ? 2 * tq : 0) * groups_k + grp];
-            const float c1 = corr[(2 * tq + 1 < NT ? 2 * tq + 1 : 0) * groups_k + grp];
-            acc[0] = fmaf(slo, cgr[0] - c0, acc[0]);
-            acc[1] = fmaf(slo, cgr[1] - c1, acc[1]);
-            acc[2] = fmaf(shi, cgr[2] - c0, acc[2]);
-            acc[3] = fmaf(shi, cgr[3] - c1, acc[3]);
+            const int t0c = 2 * tq < NT ? 2 * tq : 0, t1c = 2 * tq + 1 < NT ? 2 * tq + 1 : 0;
+            const float c0 = corr[t0c * groups_k + grp];
+            const float c1 = corr[t1c * groups_k + grp];
+            if (zp) {  // AWQ: row offsets B + z * S (zero point per row and group)
+              const uint8_t* zs = sc_smem + rows * groups_k * 2;
+              const float zlo = zs[lr * groups_k + grp], zhi = zs[(lr + 8) * groups_k + grp];
+              const float s0 = corr[(NT + t0c) * groups_k + grp], s1 = corr[(NT + t1c) * groups_k + grp];
+              acc[0] = fmaf(slo, cgr[0] - fmaf(zlo, s0, c0), acc[0]);
+              acc[1] = fmaf(slo, cgr[1] - fmaf(zlo, s1, c1), acc[1]);
+              acc[2] = fmaf(shi, cgr[2] - fmaf(zhi, s0, c0), acc[2]);
+              acc[3] = fmaf(shi, cgr[3] - fmaf(zhi, s1, c1), acc[3]);
+            } else {
+              acc[0] = fmaf(slo, cgr[0] - c0, acc[0]);
+              acc[1] = fmaf(slo, cgr[1] - c1, acc[1]);
+              acc[2] = fmaf(shi, cgr[2] - c0, acc[2]);
+              acc[3] = fmaf(shi, cgr[3] - c1, acc[3]);
+            }
             cgr[0] = cgr[1] = cgr[2] = cgr[3] = 0.f;
           }
         }
@@ -703,7 +737,8 @@ template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_w4_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
                    const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
-                   float* __restrict__ y, int n_stages, const L2Next nx) {
+                   float* __restrict__ y, int n_stages, const L2Next nx,
+                   const uint8_t* __restrict__ wz) {
   constexpr int WPG = kConsumers / GW;  // warps sharing one stage
   constexpr int CPW = S / WPG;          // chunks per warp per stage
   static_assert(CPW == 4, "two 128-k groups per warp per stage");
@@ -725,8 +760,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total_stages = ntile_cta * chunks_tile / S;
   const int groups_k = k / kW4Group;
   const int rows = ntile_cta * 16;
-  const int xbytes = NT * 4 * k + NT * groups_k * 4;
-  const int sbytes = rows * groups_k * 2;
+  const bool zp = wz != nullptr;  // AWQ zero points [rows][groups] after the scales
+  const int xbytes = NT * 4 * k + 2 * NT * groups_k * 4;
+  const int zbytes = zp ? rows * groups_k : 0;
+  const int sbytes = rows * groups_k * 2 + zbytes;
   uint8_t* xs = smem;
   uint8_t* sc_smem = smem + ((xbytes + 127) & ~127);
   uint8_t* ring = sc_smem + ((sbytes + 127) & ~127);
@@ -750,7 +787,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0 && total_stages > 0) {
       mbar_expect_tx(&sbar, sbytes);
       bulk_g2s(sc_smem, static_cast<const uint8_t*>(ws) + size_t(tile_begin) * 16 * groups_k * 2,
-               sbytes, &sbar);
+               sbytes - zbytes, &sbar);
+      if (zp) bulk_g2s(sc_smem + (sbytes - zbytes), wz + size_t(tile_begin) * 16 * groups_k, zbytes, &sbar);
       const uint8_t* src = wtf + size_t(tile_begin) * chunks_tile * kChunkBytes;
       int s = 0;
       uint32_t phase = 0;
@@ -828,9 +866,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) MSW_TP(3);  // dependency resolved
   pdl_trigger();
   if (NT == 1 && k <= kW4ProRegs * 4 * kConsThreads)
-    prologue_w4_t1<PRO>(x, gamma, eps, k, xs, red);
+    prologue_w4_t1<PRO>(x, gamma, eps, k, xs, red, zp);
   else
-    prologue<kW4, PRO, NT>(x, gamma, eps, k, T, xs, red, xscale);
+    prologue<kW4, PRO, NT>(x, gamma, eps, k, T, xs, red, xscale, zp);
   if (threadIdx.x == 0) MSW_TP(4);  // activations staged
   named_sync(3, kConsThreads + 32);
   const int g = lane >> 2, tq = lane & 3;
@@ -844,6 +882,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // XREG: this warp's k-slice is chunks [wi*CPW, wi*CPW + CPW) of every tile
   uint2 bx[XREG ? CPW : 1][2][2];
   float cx[XREG ? CPW / 2 : 1][2];
+  float sx[XREG ? CPW / 2 : 1][2];  // zp: the groups' activation sums S
   if (XREG) {
 #pragma unroll
     for (int j = 0; j < CPW; ++j)
@@ -858,6 +897,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int grp = (wi * CPW) / 2 + jj;
       cx[XREG ? jj : 0][0] = corr[tc0 * groups_k + grp];
       cx[XREG ? jj : 0][1] = corr[tc1 * groups_k + grp];
+      sx[XREG ? jj : 0][0] = zp ? corr[(NT + tc0) * groups_k + grp] : 0.f;
+      sx[XREG ? jj : 0][1] = zp ? corr[(NT + tc1) * groups_k + grp] : 0.f;
     }
   }
   if (total_stages > 0) mbar_wait(&sbar, 0);
@@ -951,10 +992,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         k0 = corr[tc0 * groups_k + grp];
         k1 = corr[tc1 * groups_k + grp];
       }
-      acc[0] = fmaf(slo, cg[0] - k0, acc[0]);
-      acc[1] = fmaf(slo, cg[1] - k1, acc[1]);
-      acc[2] = fmaf(shi, cg[2] - k0, acc[2]);
-      acc[3] = fmaf(shi, cg[3] - k1, acc[3]);
+      if (zp) {  // AWQ: the row's offset is B + z * S (zero point per row and group)
+        const uint8_t* zs = sc_smem + rows * groups_k * 2;
+        const float zlo = zs[lr * groups_k + grp], zhi = zs[(lr + 8) * groups_k + grp];
+        const float s0 = XREG ? sx[XREG ? jj : 0][0] : corr[(NT + tc0) * groups_k + grp];
+        const float s1 = XREG ? sx[XREG ? jj : 0][1] : corr[(NT + tc1) * groups_k + grp];
+        acc[0] = fmaf(slo, cg[0] - fmaf(zlo, s0, k0), acc[0]);
+        acc[1] = fmaf(slo, cg[1] - fmaf(zlo, s1, k1), acc[1]);
+        acc[2] = fmaf(shi, cg[2] - fmaf(zhi, s0, k0), acc[2]);
+        acc[3] = fmaf(shi, cg[3] - fmaf(zhi, s1, k1), acc[3]);
+      } else {
+        acc[0] = fmaf(slo, cg[0] - k0, acc[0]);
+        acc[1] = fmaf(slo, cg[1] - k1, acc[1]);
+        acc[2] = fmaf(shi, cg[2] - k0, acc[2]);
+        acc[3] = fmaf(shi, cg[3] - k1, acc[3]);
+      }
     }
   }
   if (cur >= 0) flush(cur);
@@ -1056,11 +1108,11 @@ void launch_tf_s(const LinearW& W, const float* x, int T, const half* gamma, flo
   const int grid = std::max(1, std::min(ntiles, kNumSMs));
   const int stage_bytes = S * kChunkBytes;
   const size_t xraw = FMT == kINT8 ? size_t(T) * W.k
-                                   : (FMT == kW4 ? size_t(NT) * 4 * W.k + size_t(NT) * (W.k / kW4Group) * 4
+                                   : (FMT == kW4 ? size_t(NT) * 4 * W.k + 2 * size_t(NT) * (W.k / kW4Group) * 4
                                                  : size_t(T) * 2 * W.k);
   const size_t xbytes = (xraw + 127) & ~size_t(127);
   const int per_cta = (ntiles + grid - 1) / grid;
-  const size_t sbytes = FMT == kW4 ? size_t(per_cta) * 16 * (W.k / kW4Group) * 2
+  const size_t sbytes = FMT == kW4 ? size_t(per_cta) * 16 * (W.k / kW4Group) * (W.z ? 3 : 2)
                                    : (FMT == kINT8 ? size_t(per_cta) * 16 * 4 : 0);
   const size_t fixed = xbytes + ((sbytes + 127) & ~size_t(127));
   int stages = int((kSmemBudget - std::min<size_t>(fixed, kSmemBudget - 2 * stage_bytes)) / stage_bytes);
@@ -1075,7 +1127,7 @@ void launch_tf_s(const LinearW& W, const float* x, int T, const half* gamma, flo
   }
   launch_pdl(gemv_tf_kernel<FMT, PRO, EPI, NT, S>, dim3(grid), dim3(kThreads), smem, st,
              static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages,
-             t_next);
+             t_next, FMT == kW4 ? W.z : static_cast<const uint8_t*>(nullptr));
 }
 
 template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
@@ -1085,9 +1137,9 @@ void launch_w4(const LinearW& W, const float* x, int T, const half* gamma, float
   const int grid = std::max(1, std::min(ntiles, kNumSMs));
   const int stage_bytes = S * kChunkBytes;
   const int groups = W.k / kW4Group;
-  const size_t xbytes = (size_t(NT) * 4 * W.k + size_t(NT) * groups * 4 + 127) & ~size_t(127);
+  const size_t xbytes = (size_t(NT) * 4 * W.k + 2 * size_t(NT) * groups * 4 + 127) & ~size_t(127);
   const int per_cta = (ntiles + grid - 1) / grid;
-  const size_t sbytes = (size_t(per_cta) * 16 * groups * 2 + 127) & ~size_t(127);
+  const size_t sbytes = (size_t(per_cta) * 16 * groups * (W.z ? 3 : 2) + 127) & ~size_t(127);
   const size_t fixed = xbytes + sbytes;
   if (fixed + 2 * size_t(stage_bytes) > size_t(kSmemBudget))
     throw ConfigErr("gemv(w4): shared memory budget exceeded");
@@ -1101,7 +1153,7 @@ void launch_w4(const LinearW& W, const float* x, int T, const half* gamma, float
   }
   launch_pdl(gemv_w4_kernel<PRO, EPI, NT, S, GW, XREG>, dim3(grid), dim3(kThreads), smem, st,
              static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages,
-             t_next);
+             t_next, W.z);
 }
 
 template <int FMT, int PRO, int EPI, int NT>

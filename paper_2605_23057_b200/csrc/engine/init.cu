@@ -95,6 +95,50 @@ void launch_quant_w4(const half* w, int n, int k, uint32_t* packed, half* s, cud
   MSW_LAUNCH_CHECK();
 }
 
+__global__ void quant_awq4_kernel(const half* w, int n, int k, uint32_t* packed, half* s,
+                                  uint8_t* zeros) {
+  const int lane = threadIdx.x & 31;
+  const int groups = k / kW4Group;
+  const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= (long long)n * groups) return;
+  const int row = int(item / groups), g = int(item % groups);
+  const half* src = w + (size_t)row * k + (size_t)g * kW4Group + 4 * lane;
+  float v[4];
+  float mx = -INFINITY, mn = INFINITY;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[i] = __half2float(src[i]);
+    mx = fmaxf(mx, v[i]);
+    mn = fminf(mn, v[i]);
+  }
+  mx = warp_max(mx);
+  mn = -warp_max(-mn);
+  const half sh = __float2half_rn(fmaxf(mx - mn, 1e-5f) / 15.0f);
+  const float sf = __half2float(sh);
+  const int z = int(fminf(fmaxf(-rintf(mn / sf), 0.0f), 15.0f));
+  uint32_t word = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = min(15, max(0, int(rintf(v[i] / sf)) + z));
+    const int idx = (lane & 1) * 4 + i;
+    const int pos = (idx >> 1) + 4 * (idx & 1);
+    word |= uint32_t(q) << (4 * pos);
+  }
+  word |= __shfl_xor_sync(0xffffffffu, word, 1);
+  if ((lane & 1) == 0) packed[(size_t)row * (k / 8) + (size_t)g * 16 + (lane >> 1)] = word;
+  if (lane == 0) {
+    s[(size_t)row * groups + g] = sh;
+    zeros[(size_t)row * groups + g] = uint8_t(z);
+  }
+}
+
+void launch_quant_awq4(const half* w, int n, int k, uint32_t* packed, half* s, uint8_t* z,
+                       cudaStream_t st) {
+  const long long items = (long long)n * (k / kW4Group);
+  quant_awq4_kernel<<<ceil_div(items, 8), 256, 0, st>>>(w, n, k, packed, s, z);
+  MSW_LAUNCH_CHECK();
+}
+
 __global__ void unpack_w4_kernel(const uint32_t* packed, long long total, uint8_t* out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {

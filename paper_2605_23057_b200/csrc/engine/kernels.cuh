@@ -18,13 +18,18 @@ struct LinearW {
   const void* w = nullptr;
   const void* s = nullptr;
   const void* w_tf = nullptr;  // the same weights in tile-fragment order (decode GEMV)
+  const uint8_t* z = nullptr;  // kW4 only: AWQ zero points uint8 [n, k/128] (nullptr: GPTQ, zero 8)
   size_t bytes() const {
     const size_t nk = size_t(n) * size_t(k);
     if (fmt == kFP16) return nk * 2;
     if (fmt == kINT8) return nk + size_t(n) * 4;
-    return nk / 2 + size_t(n) * (k / kW4Group) * 2;
+    return nk / 2 + size_t(n) * (k / kW4Group) * (z ? 3 : 2);
   }
 };
+// Engine weight slots: kFP16, kINT8, kW4 (GPTQ) and kSlotAWQ4 (a kW4 LinearW
+// with zero points).
+constexpr int kSlotAWQ4 = 3;
+constexpr int kSlots = 4;
 
 // ---- init.cu: K16 generator, quantisers, successor lm_head ----------------
 void launch_fill_fp16(half* dst, int64_t rows, int64_t cols, uint64_t seed, uint64_t tid,
@@ -32,6 +37,10 @@ void launch_fill_fp16(half* dst, int64_t rows, int64_t cols, uint64_t seed, uint
 void launch_fill_norm(half* dst, int64_t n, uint64_t seed, uint64_t tid, cudaStream_t st);
 void launch_quant_int8(const half* w, int n, int k, int8_t* q, float* s, cudaStream_t st);
 void launch_quant_w4(const half* w, int n, int k, uint32_t* packed, half* s, cudaStream_t st);
+// AWQ format (AutoAWQ pseudo_quantize_tensor, zero_point=True): asymmetric
+// group-128, fp16 scale (max - min) / 15, zero point, same nibble packing as W4
+void launch_quant_awq4(const half* w, int n, int k, uint32_t* packed, half* s, uint8_t* z,
+                       cudaStream_t st);
 void launch_unpack_w4(const uint32_t* packed, int n, int k, uint8_t* nibbles, cudaStream_t st);
 void launch_lm_head(const half* emb, const int* pred, const uint8_t* agree, int is_draft,
                     int V, int H, half* out, cudaStream_t st);

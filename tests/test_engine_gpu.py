@@ -3,11 +3,11 @@ msw_engine_run_batch) against the CPU oracle on the same K16 random-init
 weights and synthetic prompts.
 
 Bars (DESIGN.md "Numerics contract"):
-  * greedy tokens bit-exact in every mode (FP16, INT8, GPTQ4, spec, GPTQ+PC, INT8+CB);
+  * greedy tokens bit-exact in every mode (FP16, INT8, GPTQ4, AWQ4, spec, GPTQ+PC, INT8+CB);
   * speculative decoding: tokens == target greedy, and round/proposal/accept
     counts equal the oracle's (they are a deterministic function of tokens);
   * logits: max |gpu - oracle| / std(oracle logits) < 2e-3 (FP16),
-    < 1e-2 (W4: fp16 partial sums) — per generated step. INT8: < 1e-2 (a 1-ulp
+    < 1e-2 (W4 GPTQ / AWQ: fp16 partial sums) — per generated step. INT8: < 1e-2 (a 1-ulp
     difference in an fp32 activation can flip one int8 activation rounding, and
     the tensor-core prefill attention rounds P to fp16; tokens stay exact).
 """
@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from paper_2605_23057_b200 import (MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_FP16, MODE_GPTQ4,
+from paper_2605_23057_b200 import (MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_FP16, MODE_GPTQ4,
                                    MODE_GPTQ_PC, MODE_INT8, MODE_INT8_CB, MODE_SPEC, engine_cfg,
                                    model_cfg)
 from paper_2605_23057_b200._capi import MswError
@@ -23,9 +23,9 @@ from paper_2605_23057_b200.engine import Engine
 
 pytestmark = pytest.mark.gpu
 
-TOL = {MODE_FP16: 2e-3, MODE_INT8: 1e-2, MODE_GPTQ4: 1e-2, MODE_GPTQ_PC: 1e-2, MODE_INT8_CB: 1e-2,
+TOL = {MODE_FP16: 2e-3, MODE_INT8: 1e-2, MODE_GPTQ4: 1e-2, MODE_AWQ4: 1e-2, MODE_GPTQ_PC: 1e-2, MODE_INT8_CB: 1e-2,
        MODE_SPEC: 2e-3, MODE_CHUNKED_PREFILL: 2e-3, MODE_CUDA_GRAPHS: 2e-3}
-ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_GPTQ_PC: 2, MODE_INT8_CB: 1,
+ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_AWQ4: 3, MODE_GPTQ_PC: 2, MODE_INT8_CB: 1,
                MODE_CHUNKED_PREFILL: 0, MODE_CUDA_GRAPHS: 0}
 
 
@@ -49,7 +49,7 @@ def _check_logits(gpu, ref, tol):
     assert err.max() < tol, f"logit error {err.max():.3g} >= {tol}"
 
 
-@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_CHUNKED_PREFILL,
+@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_AWQ4, MODE_CHUNKED_PREFILL,
                                   MODE_CUDA_GRAPHS])
 @pytest.mark.parametrize("plen,n_new", [(1, 4), (37, 24), (130, 9)])
 def test_batch1_modes_match_oracle(pair, mode, plen, n_new):
@@ -61,7 +61,7 @@ def test_batch1_modes_match_oracle(pair, mode, plen, n_new):
     _check_logits(r.logits, lg, TOL[mode])
 
 
-@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4])
+@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_AWQ4])
 def test_graph_replay_equals_oracle_tokens(pair, mode):
     _, eng, orc, _ = pair
     p = prompt(99 + mode, 50, eng.vocab)
@@ -150,7 +150,7 @@ def test_error_codes(pair):
         eng.run(MODE_FP16, np.array([eng.vocab + 5], dtype=np.int32), 2)
     assert e.value.code == 3
     with pytest.raises(MswError) as e:
-        eng.run(3, np.array([1, 2, 3], dtype=np.int32), 2)  # AWQ4: not an engine mode
+        eng.run(12, np.array([1, 2, 3], dtype=np.int32), 2)  # not an InferenceMode id
     assert e.value.code == 2
     with pytest.raises(MswError) as e:
         eng.run(MODE_FP16, np.arange(10, dtype=np.int32), 5000)

@@ -225,3 +225,55 @@ def test_decode_gemv_stress_repeatable(cuda_ok, fmt, t, n, k):
     ref = O.linear(fmt, ref_w, ref_s, x)
     tol = {_capi.W_FP16: 2e-5, _capi.W_INT8: 0.0, _capi.W_W4: 2e-3}[fmt]
     assert np.abs(first - ref).max() <= tol * np.abs(ref).max()
+
+
+def test_awq4_quantiser_bit_exact(cuda_ok):
+    """msw_quant_awq4_rows (AWQ asymmetric g128: fp16 scale, uint8 zero point)
+    packs the same nibbles, scales and zero points as the oracle's restatement
+    of AutoAWQ pseudo_quantize (pinned in test_oracle_pin.py), including a
+    constant group (max == min) and an all-zero row."""
+    torch = _torch()
+    n, k = 96, 1024
+    w = O.fill_fp16(n, k, 3, 4321, 6)
+    w[5, :] = 0
+    w[7, 128:256] = w[7, 130]
+    w[10:30] &= 0x7FFF  # all-positive rows: zero point 0
+    w[30:50] |= 0x8000  # all-negative rows: zero point 15
+    w[50:60, ::2] &= 0x7FFF  # skewed groups
+    dw = torch.from_numpy(w.view(np.int16)).cuda()
+    q = torch.empty((n, k // 8), dtype=torch.int32, device="cuda")
+    s = torch.empty((n, k // 128), dtype=torch.int16, device="cuda")
+    z = torch.empty((n, k // 128), dtype=torch.uint8, device="cuda")
+    check_engine(engine_lib().msw_quant_awq4_rows(dw.data_ptr(), n, k, q.data_ptr(), s.data_ptr(),
+                                                  z.data_ptr(), None))
+    torch.cuda.synchronize()
+    rq, rs, rz = O.quant_awq4_rows(w)
+    assert np.array_equal(q.cpu().numpy().view(np.uint32), _pack_w4_host(rq))
+    assert np.array_equal(s.cpu().numpy().view(np.uint16), rs)
+    assert np.array_equal(z.cpu().numpy(), rz)
+    assert rz.max() <= 15 and {0, 7, 8, 15} <= set(np.unique(rz).tolist())
+
+
+@pytest.mark.parametrize("t", [1, 2, 5, 6, 7, 129, 300])
+@pytest.mark.parametrize("n,k", [(512, 4096), (4096, 4096), (256, 14336), (96, 256), (2400, 4096)])
+def test_linear_awq4_vs_oracle(cuda_ok, t, n, k):
+    """AWQ4 linears (zero-point W4: decode GEMV t <= 6, tcgen05 GEMM with the
+    packed-weight dequant producer t > 6 and n % 128 == 0, tile GEMM otherwise)
+    against the oracle's (q - z) * s reference; the W4 bar (fp16 partial sums)."""
+    torch = _torch()
+    rng = np.random.default_rng(t * 17 + n + k)
+    w = O.fill_fp16(n, k, 23, 5678 + n, (int(np.ceil(np.log2(k))) + 1) // 2)
+    x = rng.standard_normal((t, k)).astype(np.float32)
+    x[:, 0] = 4.0
+    q, s, z = O.quant_awq4_rows(w)
+    dq = torch.from_numpy(_pack_w4_host(q).view(np.int32)).cuda()
+    ds = torch.from_numpy(s.view(np.int16)).cuda()
+    dz = torch.from_numpy(z).cuda()
+    dx = torch.from_numpy(x).cuda()
+    dy = torch.empty((t, n), dtype=torch.float32, device="cuda")
+    check_engine(engine_lib().msw_linear_awq4(dq.data_ptr(), ds.data_ptr(), dz.data_ptr(), n, k,
+                                              dx.data_ptr(), t, dy.data_ptr(), None))
+    torch.cuda.synchronize()
+    y = dy.cpu().numpy()
+    ref = O.linear_awq4(q, s, z, x)
+    assert np.abs(y - ref).max() / np.abs(ref).max() < 2e-3
