@@ -733,7 +733,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 //     tile (stages may straddle tiles in the GW = 2 configuration).
 // Same numerics as gemv_tf_kernel<kW4>: identical MMA operands, per-group
 // fp32 accumulation of 8 MMAs, correction subtracted before the group scale.
-template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
+template <int PRO, int EPI, int NT, int S, int GW, bool XREG, bool ZP>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_w4_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
                    const float* __restrict__ x, int T, const half* __restrict__ gamma, float eps,
@@ -760,8 +760,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total_stages = ntile_cta * chunks_tile / S;
   const int groups_k = k / kW4Group;
   const int rows = ntile_cta * 16;
-  const bool zp = wz != nullptr;  // AWQ zero points [rows][groups] after the scales
-  const int xbytes = NT * 4 * k + 2 * NT * groups_k * 4;
+  // ZP (AWQ): zero points [rows][groups] after the scales, and the group sums S
+  // after the offsets in the activation region. A template constant: the
+  // GPTQ instantiation carries no zero-point work in its issue-bound loop.
+  constexpr bool zp = ZP;
+  const int xbytes = NT * 4 * k + (ZP ? 2 : 1) * NT * groups_k * 4;
   const int zbytes = zp ? rows * groups_k : 0;
   const int sbytes = rows * groups_k * 2 + zbytes;
   uint8_t* xs = smem;
@@ -1130,14 +1133,14 @@ void launch_tf_s(const LinearW& W, const float* x, int T, const half* gamma, flo
              t_next, FMT == kW4 ? W.z : static_cast<const uint8_t*>(nullptr));
 }
 
-template <int PRO, int EPI, int NT, int S, int GW, bool XREG>
+template <int PRO, int EPI, int NT, int S, int GW, bool XREG, bool ZP>
 void launch_w4(const LinearW& W, const float* x, int T, const half* gamma, float eps, float* y,
                cudaStream_t st) {
   const int ntiles = W.n / 16;
   const int grid = std::max(1, std::min(ntiles, kNumSMs));
   const int stage_bytes = S * kChunkBytes;
   const int groups = W.k / kW4Group;
-  const size_t xbytes = (size_t(NT) * 4 * W.k + 2 * size_t(NT) * groups * 4 + 127) & ~size_t(127);
+  const size_t xbytes = (size_t(NT) * 4 * W.k + (ZP ? 2 : 1) * size_t(NT) * groups * 4 + 127) & ~size_t(127);
   const int per_cta = (ntiles + grid - 1) / grid;
   const size_t sbytes = (size_t(per_cta) * 16 * groups * (W.z ? 3 : 2) + 127) & ~size_t(127);
   const size_t fixed = xbytes + sbytes;
@@ -1147,11 +1150,11 @@ void launch_w4(const LinearW& W, const float* x, int T, const half* gamma, float
   const size_t smem = fixed + size_t(stages) * stage_bytes;
   static bool attr_done = false;
   if (!attr_done) {
-    MSW_CUDA(cudaFuncSetAttribute(gemv_w4_kernel<PRO, EPI, NT, S, GW, XREG>,
+    MSW_CUDA(cudaFuncSetAttribute(gemv_w4_kernel<PRO, EPI, NT, S, GW, XREG, ZP>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_done = true;
   }
-  launch_pdl(gemv_w4_kernel<PRO, EPI, NT, S, GW, XREG>, dim3(grid), dim3(kThreads), smem, st,
+  launch_pdl(gemv_w4_kernel<PRO, EPI, NT, S, GW, XREG, ZP>, dim3(grid), dim3(kThreads), smem, st,
              static_cast<const uint8_t*>(W.w_tf), W.s, W.n, W.k, x, T, gamma, eps, y, stages,
              t_next, W.z);
 }
@@ -1163,10 +1166,17 @@ void launch_tf(const LinearW& W, const float* x, int T, const half* gamma, float
   if constexpr (FMT == kW4 && NT == 1) {  // the GPTQ modes decode batch-1
     static const bool generic = diag_env("MSW_GEMV_W4_GENERIC") != nullptr;  // A/B switch
     if (!generic) {
-    if (chunks_tile == 64) return launch_w4<PRO, EPI, NT, 64, 1, true>(W, x, T, gamma, eps, y, st);
-    if (chunks_tile % 64 == 0) return launch_w4<PRO, EPI, NT, 64, 1, false>(W, x, T, gamma, eps, y, st);
-    if (chunks_tile % 32 == 0 && chunks_tile >= 64)
-      return launch_w4<PRO, EPI, NT, 32, 2, false>(W, x, T, gamma, eps, y, st);
+    if (W.z != nullptr) {  // AWQ zero points
+      if (chunks_tile == 64) return launch_w4<PRO, EPI, NT, 64, 1, true, true>(W, x, T, gamma, eps, y, st);
+      if (chunks_tile % 64 == 0) return launch_w4<PRO, EPI, NT, 64, 1, false, true>(W, x, T, gamma, eps, y, st);
+      if (chunks_tile % 32 == 0 && chunks_tile >= 64)
+        return launch_w4<PRO, EPI, NT, 32, 2, false, true>(W, x, T, gamma, eps, y, st);
+    } else {
+      if (chunks_tile == 64) return launch_w4<PRO, EPI, NT, 64, 1, true, false>(W, x, T, gamma, eps, y, st);
+      if (chunks_tile % 64 == 0) return launch_w4<PRO, EPI, NT, 64, 1, false, false>(W, x, T, gamma, eps, y, st);
+      if (chunks_tile % 32 == 0 && chunks_tile >= 64)
+        return launch_w4<PRO, EPI, NT, 32, 2, false, false>(W, x, T, gamma, eps, y, st);
+    }
     }
   }
   if (chunks_tile % 32 == 0) return launch_tf_s<FMT, PRO, EPI, NT, 32>(W, x, T, gamma, eps, y, st);
