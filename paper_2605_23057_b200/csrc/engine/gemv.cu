@@ -731,8 +731,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 //     weights plus two scale loads per 4096 weights;
 //   * a warp flushes its 16 x 8 tile partial when its slice moves to the next
 //     tile (stages may straddle tiles in the GW = 2 configuration).
-// Same numerics as gemv_tf_kernel<kW4>: identical MMA operands, per-group
-// fp32 accumulation of 8 MMAs, correction subtracted before the group scale.
+// Numerics as gemv_tf_kernel<kW4> (identical MMA operands, per-group fp32
+// accumulation, correction subtracted before the group scale) except that a
+// group's 8 MMAs run as two chains of 4 (low / high nibbles) summed at the
+// group end: a different fp32 summation order, within the W4 bar.
 template <int PRO, int EPI, int NT, int S, int GW, bool XREG, bool ZP>
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_w4_kernel(const uint8_t* __restrict__ wtf, const void* __restrict__ ws, int n, int k,
@@ -955,7 +957,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lr = ti * 16 + g;
 #pragma unroll
     for (int jj = 0; jj < CPW / 2; ++jj) {
-      float cg[4] = {0.f, 0.f, 0.f, 0.f};
+      // two accumulator chains per group (low / high nibbles): the group's
+      // 8 dependent MMAs become 2 x 4, halving the MMA latency chain
+      float cg[4] = {0.f, 0.f, 0.f, 0.f}, ch[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 2 * jj; j < 2 * jj + 2; ++j) {
         const uint32_t wv[4] = {a4[j].x, a4[j].y, a4[j].z, a4[j].w};
@@ -981,9 +985,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             bo = *reinterpret_cast<const uint2*>(xrow16 + kb + 32);
           }
           mma_f16(cg, a_lo, be.x, be.y);
-          mma_f16(cg, a_hi, bo.x, bo.y);
+          mma_f16(ch, a_hi, bo.x, bo.y);
         }
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cg[i] += ch[i];
       const int grp = (c0 >> 1) + jj;
       const float slo = __half2float(sc_h[lr * groups_k + grp]);
       const float shi = __half2float(sc_h[(lr + 8) * groups_k + grp]);
