@@ -44,6 +44,7 @@ enum {
   MSW_MODE_SPECULATIVE = 4,
   MSW_MODE_CHUNKED_PREFILL = 6, /* FP16, prefill in 512-token chunks (screening mode) */
   MSW_MODE_CUDA_GRAPHS = 8,     /* FP16, graph-replayed decode (screening mode) */
+  MSW_MODE_KV_COMPRESSION = 9,  /* FP16 weights, FP8 E4M3 KV cache after prefill (screening mode) */
   MSW_MODE_GPTQ_PREFIX_CACHING = 10,
   MSW_MODE_INT8_CONT_BATCHING = 11
 };
@@ -130,6 +131,11 @@ int msw_engine_weight_bytes(msw_engine* e, int32_t mode, int64_t* bytes);
 int msw_engine_memory_bytes(msw_engine* e, int32_t mode, int32_t tokens, int64_t* bytes);
 /* Drops every cached prefix block (prefix caching) and resets counters. */
 int msw_engine_reset_prefix_cache(msw_engine* e);
+
+/* KV-cache compression mode test entry: q[i] = FP8 E4M3 of the fp16 x[i]
+ * (round to nearest even, saturating to +-448), y[i] = q[i] widened back to
+ * fp16 (exact). n even; device pointers. */
+int msw_fp8_e4m3_roundtrip(const uint16_t* x, int64_t n, uint8_t* q, uint16_t* y, void* stream);
 
 /* ---- kernel-level entry points (device pointers; used by parity tests and
  * bench.py to time the dominant kernel). stream may be NULL (legacy). ---- */

@@ -39,6 +39,7 @@ def lib() -> C.CDLL:
         L.orc_model_tensor.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp]
         L.orc_quant_awq4_rows.argtypes = [vp, i32, i32, vp, vp, vp]
         L.orc_linear_awq4.argtypes = [vp, vp, vp, i32, i32, vp, i32, vp]
+        L.orc_fp8_e4m3_roundtrip.argtypes = [vp, C.c_int64, vp, vp]
         _lib = L
     return _lib
 
@@ -161,6 +162,15 @@ def linear_awq4(q: np.ndarray, s: np.ndarray, z: np.ndarray, x: np.ndarray) -> n
     lib().orc_linear_awq4(_p(np.ascontiguousarray(q)), _p(np.ascontiguousarray(s)),
                           _p(np.ascontiguousarray(z)), n, k, _p(x), x.shape[0], _p(y))
     return y
+
+
+def fp8_e4m3(x16: np.ndarray):
+    """fp16 bits (uint16) -> (E4M3 bytes, their fp16 bits): RNE, saturating."""
+    x16 = np.ascontiguousarray(x16, dtype=np.uint16).ravel()
+    q = np.zeros(x16.size, dtype=np.uint8)
+    y = np.zeros(x16.size, dtype=np.uint16)
+    lib().orc_fp8_e4m3_roundtrip(_p(x16), x16.size, _p(q), _p(y))
+    return q, y
 
 
 def gemv_i8_acc(w: np.ndarray, x: np.ndarray) -> np.ndarray:

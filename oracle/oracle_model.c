@@ -24,6 +24,40 @@ static inline h16 f2h(float f) { /* IEEE round-to-nearest-even */
 }
 static inline float rnd16(float f) { return h2f(f2h(f)); }
 
+/* FP8 E4M3 (OCP "e4m3fn": bias 7, 3 mantissa bits, max 448, no inf) of a
+ * finite value, round to nearest even, saturating to +-448 — the PTX
+ * cvt.rn.satfinite.e4m3x2 the engine's KV-cache compression mode uses.
+ * Normal binades [2^e, 2^(e+1)), e >= -6, have step 2^(e-3); below 2^-6 the
+ * subnormal step is 2^-9. */
+static float e4m3_rn(float x) {
+  const float a = fabsf(x);
+  if (a == 0.0f) return x;
+  int e;
+  frexpf(a, &e); /* a = f * 2^e, f in [0.5, 1): binade 2^(e-1) */
+  int ex = e - 1;
+  if (ex < -6) ex = -6;
+  const float step = ldexpf(1.0f, ex - 3);
+  float q = rintf(a / step) * step; /* exact scaling; rintf = nearest even */
+  if (q > 448.0f) q = 448.0f;
+  return copysignf(q, x);
+}
+static uint8_t e4m3_bits(float q) { /* q already an E4M3 value */
+  const uint8_t sgn = signbit(q) ? 0x80 : 0;
+  const float a = fabsf(q);
+  if (a == 0.0f) return sgn;
+  if (a < ldexpf(1.0f, -6)) return sgn | (uint8_t)lrintf(a / ldexpf(1.0f, -9));
+  int e;
+  const float f = frexpf(a, &e); /* a = f * 2^e */
+  return sgn | (uint8_t)((e - 1 + 7) << 3) | (uint8_t)lrintf(f * 16.0f - 8.0f);
+}
+void orc_fp8_e4m3_roundtrip(const uint16_t* x, int64_t n, uint8_t* q, uint16_t* y) {
+  for (int64_t i = 0; i < n; ++i) {
+    const float v = e4m3_rn(h2f(x[i]));
+    q[i] = e4m3_bits(v);
+    y[i] = f2h(v);
+  }
+}
+
 /* ------------------------------------------------- K16 deterministic init */
 static inline uint64_t mix64(uint64_t z) { /* splitmix64 */
   z += 0x9E3779B97F4A7C15ull;
@@ -585,6 +619,8 @@ static void forward(orc_model* m, int mode, int32_t tok, int32_t pos, float* log
       }
     }
     for (int32_t i = 0; i < (Hq + 2 * Hk) * D; ++i) qkv[i] = rnd16(qkv[i]);
+    if (mode == MSW_MODE_KV_COMPRESSION) /* new K / V at the cache's precision */
+      for (int32_t i = Hq * D; i < (Hq + 2 * Hk) * D; ++i) qkv[i] = e4m3_rn(qkv[i]);
     float* kl = m->kc + ((size_t)l * m->max_ctx) * Hk * D;
     float* vl = m->vc + ((size_t)l * m->max_ctx) * Hk * D;
     memcpy(kl + (size_t)pos * Hk * D, qkv + Hq * D, sizeof(float) * Hk * D);
@@ -647,12 +683,26 @@ int orc_generate(orc_model* m, int mode, const int32_t* prompt, int plen, int n_
   if (plen < 1 || n_new < 1 || plen + n_new > m->max_ctx) return 3;
   const int32_t V = m->c.vocab;
   float* lg = (float*)malloc(sizeof(float) * V);
+  /* KV-cache compression: the prompt is prefilled at fp16 (FP16 mode), then
+   * its cached K / V are rounded to E4M3; decode steps store E4M3 K / V */
+  const int kvc = mode == MSW_MODE_KV_COMPRESSION;
   for (int i = 0; i < plen; ++i) {
     if (prompt[i] < 0 || prompt[i] >= V) {
       free(lg);
       return 3;
     }
-    forward(m, mode, prompt[i], i, lg);
+    forward(m, kvc ? MSW_MODE_FP16 : mode, prompt[i], i, lg);
+  }
+  if (kvc) {
+    const int32_t Hk = m->c.n_kv_heads, D = m->c.head_dim;
+    for (int32_t l = 0; l < m->c.n_layers; ++l) {
+      float* kl = m->kc + ((size_t)l * m->max_ctx) * Hk * D;
+      float* vl = m->vc + ((size_t)l * m->max_ctx) * Hk * D;
+      for (size_t i = 0; i < (size_t)plen * Hk * D; ++i) {
+        kl[i] = e4m3_rn(kl[i]);
+        vl[i] = e4m3_rn(vl[i]);
+      }
+    }
   }
   for (int t = 0; t < n_new; ++t) {
     out[t] = argmax(lg, V);

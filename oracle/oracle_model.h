@@ -71,6 +71,9 @@ void orc_quant_w4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* q_out,
                        uint16_t* scales);
 /* AWQ format, asymmetric group-128: q nibble-per-byte [n, k], fp16 scales and
  * uint8 zero points [n, k/128]; w' = (q - z) * s. */
+/* KV-cache compression: FP8 E4M3 (RNE, saturating) of fp16 values: q the
+ * E4M3 byte, y its fp16 value. */
+void orc_fp8_e4m3_roundtrip(const uint16_t* x, int64_t n, uint8_t* q, uint16_t* y);
 void orc_quant_awq4_rows(const uint16_t* w, int32_t n, int32_t k, uint8_t* q_out,
                          uint16_t* scales, uint8_t* zeros);
 void orc_linear_awq4(const uint8_t* q, const uint16_t* scales, const uint8_t* zeros, int32_t n,

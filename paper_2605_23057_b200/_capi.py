@@ -152,6 +152,7 @@ def engine_lib() -> C.CDLL:
         lib.msw_quant_int8_rows.argtypes = [vp, i32, i32, vp, vp, vp]
         lib.msw_quant_w4_rows.argtypes = [vp, i32, i32, vp, vp, vp]
         lib.msw_linear_awq4.argtypes = [vp, vp, vp, i32, i32, vp, i32, vp, vp]
+        lib.msw_fp8_e4m3_roundtrip.argtypes = [vp, C.c_int64, vp, vp, vp]
         lib.msw_quant_awq4_rows.argtypes = [vp, i32, i32, vp, vp, vp, vp]
         lib.msw_device_pci_bus_id.argtypes = [i32, C.c_char_p, i32]
         lib.msw_attention_decode.argtypes = [vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32,

@@ -26,12 +26,12 @@ SHAPES = {
 }
 
 MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_SPEC, MODE_GPTQ_PC, MODE_INT8_CB = 0, 1, 2, 4, 10, 11
-MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS = 3, 6, 8  # screening modes (not routed)
+MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_KV_COMPRESSION = 3, 6, 8, 9  # screening (not routed)
 ROUTED_MODES = (MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_SPEC, MODE_GPTQ_PC, MODE_INT8_CB)
-SCREENING_MODES = (MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS)
+SCREENING_MODES = (MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_KV_COMPRESSION)
 ALL_MODES = ROUTED_MODES + SCREENING_MODES
 MODE_NAMES = {0: "fp16", 1: "int8", 2: "gptq4", 3: "awq4", 4: "speculative_decoding", 6: "chunked_prefill",
-              8: "cuda_graphs", 10: "gptq_prefix_caching", 11: "int8_continuous_batching"}
+              8: "cuda_graphs", 9: "kv_cache_compression", 10: "gptq_prefix_caching", 11: "int8_continuous_batching"}
 
 
 def model_cfg(name: str) -> ModelCfg:

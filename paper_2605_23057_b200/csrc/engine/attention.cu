@@ -37,6 +37,22 @@ __device__ __forceinline__ size_t kv_off(int slot, int hk, int Hk, int D) {
   return ((size_t(slot >> 4) * Hk + hk) * kKvBlock + (slot & 15)) * size_t(D);
 }
 
+// KV-cache compression (MSW_MODE_KV_COMPRESSION): K / V stored as FP8 E4M3,
+// one byte per element in the same [block][kv_head][16][D] layout.
+// fp16 pair -> e4m3 pair (round to nearest even, saturating to +-448), element
+// 2i in the low byte; and back (exact: e4m3 is a subset of fp16).
+__device__ __forceinline__ uint16_t h2_to_e4m3x2(half lo, half hi) {
+  uint16_t r;
+  const uint32_t v = uint32_t(__half_as_ushort(lo)) | (uint32_t(__half_as_ushort(hi)) << 16);
+  asm("cvt.rn.satfinite.e4m3x2.f16x2 %0, %1;" : "=h"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t e4m3x2_to_h2(uint16_t v) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"(v));
+  return r;
+}
+
 __global__ void rope_table_kernel(const float* __restrict__ inv_freq, int half_d, int max_pos,
                                   float2* __restrict__ table) {
   const int total = max_pos * half_d;
@@ -346,12 +362,17 @@ __device__ __forceinline__ int split_chunk_dec(int ctx, int nsplit) {
 //    the last CTA to finish (atomic counter) combines them, so there is no
 //    separate combine launch.
 
-template <int D, int G, int W>
+// KV8: the paged cache holds FP8 E4M3 (KV-cache compression mode): history
+// rows are widened to fp16 while staged, and this launch's new keys / values
+// are rounded through E4M3 before use and stored as E4M3, so every position
+// the query attends to carries the cache's precision.
+template <int D, int G, int W, bool KV8>
 __global__ void __launch_bounds__(W * 32)
     attn_decode_kernel(const float* __restrict__ qkv, const float2* __restrict__ rope,
                        const int* __restrict__ pos, const int* __restrict__ slot,
                        const int* __restrict__ seq_of, const int* __restrict__ block_table,
-                       int max_blocks, half* __restrict__ kc, half* __restrict__ vc, int Hq, int Hk,
+                       int max_blocks, typename std::conditional<KV8, uint8_t, half>::type* __restrict__ kc,
+                       typename std::conditional<KV8, uint8_t, half>::type* __restrict__ vc, int Hq, int Hk,
                        int nsplit, float* __restrict__ part_o, float* __restrict__ part_ml,
                        int* __restrict__ counters, float* __restrict__ o, int run) {
   constexpr int DPL = D / 32;
@@ -407,8 +428,58 @@ __global__ void __launch_bounds__(W * 32)
       }
     }
   };
+  // KV8: the tile's E4M3 rows are copied asynchronously, raw, into the top
+  // kRaw8 bytes of each staged row (D bytes ending at the padded row end),
+  // then widened in place by widen_tile: lane = row, the row's raw bytes are
+  // all read into registers before any fp16 store, so the overlap of the
+  // fp16 region [0, 2D) with the raw one [2 RS - D, 2 RS) is harmless.
+  constexpr int kRaw8 = 2 * RS - D;  // byte offset of the raw row (multiple of 16)
+  constexpr int CPR8 = D / 16, RPI8 = 32 / CPR8;
+  auto stage_tile8 = [&](int base) {
+    const int c = lane % CPR8;
+#pragma unroll 4
+    for (int i = 0; i < 32 / RPI8; ++i) {
+      const int r = i * RPI8 + lane / CPR8;
+      const int p = base + r;
+      if (p < end && p < p_new) {
+        const int sl = bt[p >> 4] * kKvBlock + (p & 15);
+        cp_async16(reinterpret_cast<uint8_t*>(sK + r * RS) + kRaw8 + c * 16,
+                   kc + kv_off(sl, hk, Hk, D) + c * 16);
+        cp_async16(reinterpret_cast<uint8_t*>(sV + r * RS) + kRaw8 + c * 16,
+                   vc + kv_off(sl, hk, Hk, D) + c * 16);
+      }
+    }
+  };
+  auto widen_tile = [&]() {
+#pragma unroll
+    for (int kv = 0; kv < 2; ++kv) {
+      half* row = (kv == 0 ? sK : sV) + lane * RS;
+      uint4 raw[CPR8];
+#pragma unroll
+      for (int c = 0; c < CPR8; ++c)
+        raw[c] = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(row) + kRaw8 + c * 16);
+#pragma unroll
+      for (int c = 0; c < CPR8; ++c) {
+        const uint32_t w[4] = {raw[c].x, raw[c].y, raw[c].z, raw[c].w};
+        uint4 lo, hi;
+        lo.x = e4m3x2_to_h2(uint16_t(w[0]));
+        lo.y = e4m3x2_to_h2(uint16_t(w[0] >> 16));
+        lo.z = e4m3x2_to_h2(uint16_t(w[1]));
+        lo.w = e4m3x2_to_h2(uint16_t(w[1] >> 16));
+        hi.x = e4m3x2_to_h2(uint16_t(w[2]));
+        hi.y = e4m3x2_to_h2(uint16_t(w[2] >> 16));
+        hi.z = e4m3x2_to_h2(uint16_t(w[3]));
+        hi.w = e4m3x2_to_h2(uint16_t(w[3] >> 16));
+        *reinterpret_cast<uint4*>(row + c * 16) = lo;
+        *reinterpret_cast<uint4*>(row + c * 16 + 8) = hi;
+      }
+    }
+  };
   const int first = begin + warp * 32;
-  if (first < end) stage_tile(first);  // cache history only: safe before the wait
+  if (first < end) {  // cache history only: safe before the wait
+    if constexpr (KV8) stage_tile8(first);
+    else stage_tile(first);
+  }
   // the RoPE row of this position is a cold table row: fetch it before the wait
   // too (pos was written by the previous step's advance, long complete)
   constexpr int kRopeIt = ((G + 1) * (D / 2) + W * 32 - 1) / (W * 32);
@@ -462,12 +533,30 @@ __global__ void __launch_bounds__(W * 32)
     }
   }
   __syncthreads();
+  if constexpr (KV8) {  // the new rows at the cache's precision (E4M3 round trip)
+    const int rows = run ? t + 1 : 1;
+    for (int i = threadIdx.x; i < rows * (D / 2); i += blockDim.x) {
+      const int q = i / (D / 2), d = 2 * (i % (D / 2));
+      const uint32_t kk = e4m3x2_to_h2(h2_to_e4m3x2(knew_all[q][d], knew_all[q][d + 1]));
+      const uint32_t vv = e4m3x2_to_h2(h2_to_e4m3x2(vnew_all[q][d], vnew_all[q][d + 1]));
+      *reinterpret_cast<uint32_t*>(&knew_all[q][d]) = kk;
+      *reinterpret_cast<uint32_t*>(&vnew_all[q][d]) = vv;
+    }
+    __syncthreads();
+  }
   ATT_TP(2);
   if (sp == 0) {
     const size_t off = kv_off(slot[t], hk, Hk, D);
-    for (int d = threadIdx.x; d < D; d += blockDim.x) {
-      kc[off + d] = knew[d];
-      vc[off + d] = vnew[d];
+    if constexpr (KV8) {
+      for (int d = 2 * threadIdx.x; d < D; d += 2 * blockDim.x) {
+        *reinterpret_cast<uint16_t*>(kc + off + d) = h2_to_e4m3x2(knew[d], knew[d + 1]);
+        *reinterpret_cast<uint16_t*>(vc + off + d) = h2_to_e4m3x2(vnew[d], vnew[d + 1]);
+      }
+    } else {
+      for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        kc[off + d] = knew[d];
+        vc[off + d] = vnew[d];
+      }
     }
   }
   const float scale = rsqrtf(float(D));
@@ -492,9 +581,15 @@ __global__ void __launch_bounds__(W * 32)
   for (int base = first; base < end; base += W * 32) {
     if (base != first) {
       __syncwarp();
-      stage_tile(base);
+      if constexpr (KV8) stage_tile8(base);
+      else stage_tile(base);
     }
     cp_async_wait_all();
+    if constexpr (KV8) {
+      __syncwarp();  // every lane's raw rows landed
+      widen_tile();
+      __syncwarp();
+    }
     if (base == first) ATT_TP(6);  // warp 0: first tile staged
     const int p = base + lane;
     if (p >= p_new && p <= p_self) {  // this launch's new rows come from smem, not the cache
@@ -830,10 +925,13 @@ void launch_attention(const half* q, int T, const int* pos, const int* seq_of,
                        st);
 }
 
-void launch_attention_decode(const float* qkv, const float2* rope, int T, const int* pos,
-                             const int* slot, const int* seq_of, const int* block_table, half* kc,
-                             half* vc, const AttnShape& a, int nsplit, float* part_o,
-                             float* part_ml, int* counters, float* o, cudaStream_t st, bool run) {
+template <bool KV8>
+void launch_attention_decode_t(const float* qkv, const float2* rope, int T, const int* pos,
+                               const int* slot, const int* seq_of, const int* block_table,
+                               typename std::conditional<KV8, uint8_t, half>::type* kc,
+                               typename std::conditional<KV8, uint8_t, half>::type* vc,
+                               const AttnShape& a, int nsplit, float* part_o, float* part_ml,
+                               int* counters, float* o, cudaStream_t st, bool run) {
   const int G = a.n_heads / a.n_kv_heads;
   if (run && T > kRunMax) throw ConfigErr("attention: a one-sequence run is at most 6 tokens");
   const dim3 grid(T, a.n_kv_heads, nsplit);
@@ -846,11 +944,11 @@ void launch_attention_decode(const float* qkv, const float2* rope, int T, const 
     const size_t smem = size_t(WW) * 2 * 32 * (DD + kKvPad) * sizeof(half);                   \
     static bool attr = false;                                                                 \
     if (!attr) {                                                                              \
-      MSW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<DD, GG, WW>,                           \
+      MSW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<DD, GG, WW, KV8>,                      \
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); \
       attr = true;                                                                            \
     }                                                                                         \
-    return launch_pdl(attn_decode_kernel<DD, GG, WW>, grid, dim3(WW * 32), smem, st, qkv,     \
+    return launch_pdl(attn_decode_kernel<DD, GG, WW, KV8>, grid, dim3(WW * 32), smem, st, qkv, \
                       rope, pos, slot, seq_of, block_table, a.max_blocks_per_seq, kc, vc,     \
                       a.n_heads, a.n_kv_heads, nsplit, part_o, part_ml, counters, o,          \
                       run ? 1 : 0);                                                           \
@@ -870,6 +968,63 @@ void launch_attention_decode(const float* qkv, const float2* rope, int T, const 
 #undef MSW_DEC
 #undef MSW_DEC_W
   throw ConfigErr("attention: unsupported head_dim / GQA group");
+}
+
+__global__ void kv_compress_kernel(const half* __restrict__ kc, const half* __restrict__ vc,
+                                   uint8_t* __restrict__ kc8, uint8_t* __restrict__ vc8,
+                                   size_t layer_elems, const int* __restrict__ b16,
+                                   const int* __restrict__ b8, int Hk, int D) {
+  const int p = blockIdx.x, l = blockIdx.y;
+  const int s16 = b16[p >> 4] * kKvBlock + (p & 15), s8 = b8[p >> 4] * kKvBlock + (p & 15);
+  const size_t lo = size_t(l) * layer_elems;
+  for (int i = threadIdx.x; i < Hk * D / 2; i += blockDim.x) {
+    const int hk = (2 * i) / D, d = (2 * i) % D;
+    const size_t a = lo + kv_off(s16, hk, Hk, D) + d, b = lo + kv_off(s8, hk, Hk, D) + d;
+    *reinterpret_cast<uint16_t*>(kc8 + b) = h2_to_e4m3x2(kc[a], kc[a + 1]);
+    *reinterpret_cast<uint16_t*>(vc8 + b) = h2_to_e4m3x2(vc[a], vc[a + 1]);
+  }
+}
+
+__global__ void fp8_roundtrip_kernel(const half* __restrict__ x, int64_t n, uint8_t* __restrict__ q,
+                                     half* __restrict__ y) {
+  for (int64_t i = 2 * (blockIdx.x * int64_t(blockDim.x) + threadIdx.x); i + 1 < n;
+       i += 2 * int64_t(gridDim.x) * blockDim.x) {
+    const uint16_t v = h2_to_e4m3x2(x[i], x[i + 1]);
+    *reinterpret_cast<uint16_t*>(q + i) = v;
+    *reinterpret_cast<uint32_t*>(y + i) = e4m3x2_to_h2(v);
+  }
+}
+
+void launch_attention_decode(const float* qkv, const float2* rope, int T, const int* pos,
+                             const int* slot, const int* seq_of, const int* block_table, half* kc,
+                             half* vc, const AttnShape& a, int nsplit, float* part_o,
+                             float* part_ml, int* counters, float* o, cudaStream_t st, bool run) {
+  launch_attention_decode_t<false>(qkv, rope, T, pos, slot, seq_of, block_table, kc, vc, a, nsplit,
+                                   part_o, part_ml, counters, o, st, run);
+}
+
+void launch_attention_decode_kv8(const float* qkv, const float2* rope, int T, const int* pos,
+                                 const int* slot, const int* seq_of, const int* block_table,
+                                 uint8_t* kc, uint8_t* vc, const AttnShape& a, int nsplit,
+                                 float* part_o, float* part_ml, int* counters, float* o,
+                                 cudaStream_t st, bool run) {
+  launch_attention_decode_t<true>(qkv, rope, T, pos, slot, seq_of, block_table, kc, vc, a, nsplit,
+                                  part_o, part_ml, counters, o, st, run);
+}
+
+void launch_kv_compress(const half* kc, const half* vc, uint8_t* kc8, uint8_t* vc8,
+                        size_t layer_elems, int layers, const int* b16, const int* b8, int npos,
+                        int Hk, int D, cudaStream_t st) {
+  if (npos <= 0) return;
+  kv_compress_kernel<<<dim3(npos, layers), 256, 0, st>>>(kc, vc, kc8, vc8, layer_elems, b16, b8, Hk, D);
+  MSW_CUDA(cudaGetLastError());
+}
+
+void launch_fp8_roundtrip(const half* x, int64_t n, uint8_t* q, half* y, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = int(std::min<int64_t>((n / 2 + 255) / 256, 4 * kNumSMs));
+  fp8_roundtrip_kernel<<<std::max(grid, 1), 256, 0, st>>>(x, n, q, y);
+  MSW_CUDA(cudaGetLastError());
 }
 
 }  // namespace msw

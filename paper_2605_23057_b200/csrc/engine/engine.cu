@@ -37,6 +37,7 @@ int fmt_of_mode(int mode) {
     case MSW_MODE_SPECULATIVE:
     case MSW_MODE_CHUNKED_PREFILL:
     case MSW_MODE_CUDA_GRAPHS:
+    case MSW_MODE_KV_COMPRESSION:
       return kFP16;
     case MSW_MODE_INT8:
     case MSW_MODE_INT8_CONT_BATCHING:
@@ -166,6 +167,14 @@ struct Model {
   std::vector<Layer> layers;
   half* kc = nullptr;
   half* vc = nullptr;
+  // KV-cache compression mode: FP8 E4M3 pool, same [layer][block][kv_head][16][D]
+  // layout at one byte per element, its own block allocator
+  uint8_t* kc8 = nullptr;
+  uint8_t* vc8 = nullptr;
+  BlockPool pool8;
+  int* kvc_blocks = nullptr;  // device [2][max_blocks]: fp16 / fp8 block lists of a compress
+  cudaGraphExec_t graph_kv8 = nullptr;
+  int graph_kv8_nodes = 0;
   size_t kv_layer_elems = 0;
   int nblk = 0;
   int max_blocks = 0;  // block-table row stride
@@ -337,6 +346,7 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
     m.fmt_on[kINT8] = mm & ((1u << MSW_MODE_INT8) | (1u << MSW_MODE_INT8_CONT_BATCHING));
     m.fmt_on[kW4] = mm & ((1u << MSW_MODE_GPTQ4) | (1u << MSW_MODE_GPTQ_PREFIX_CACHING));
     m.fmt_on[kSlotAWQ4] = mm & (1u << MSW_MODE_AWQ4);
+    m.fmt_on[kFP16] = m.fmt_on[kFP16] || (mm & (1u << MSW_MODE_KV_COMPRESSION));
   }
 
   const size_t max_elems = std::max({size_t(Hq + 2 * Hk) * D * H, size_t(2) * F * H,
@@ -416,6 +426,14 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
   m.block_table = model_alloc<int>(m, size_t(m.bt_rows) * m.max_blocks);
   MSW_CUDA(cudaMemset(m.block_table, 0, sizeof(int) * size_t(m.bt_rows) * m.max_blocks));
   m.pool.init(m.nblk);
+  if (!is_draft && (cfg.modes_mask & (1u << MSW_MODE_KV_COMPRESSION))) {
+    m.kc8 = model_alloc<uint8_t>(m, m.kv_layer_elems * L);
+    m.vc8 = model_alloc<uint8_t>(m, m.kv_layer_elems * L);
+    MSW_CUDA(cudaMemsetAsync(m.kc8, 0, m.kv_layer_elems * L, st));
+    MSW_CUDA(cudaMemsetAsync(m.vc8, 0, m.kv_layer_elems * L, st));
+    m.pool8.init(m.nblk);
+    m.kvc_blocks = model_alloc<int>(m, size_t(2) * m.max_blocks);
+  }
   m.ash = AttnShape{Hq, Hk, D, m.max_blocks, m.nblk};
   // decode attention splits hold >= 256 positions (attention.cu kDecMinChunk):
   // no more splits than max_seq_len needs, so short-context engines do not
@@ -426,6 +444,7 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
 void free_model(Model& m) {
   for (auto& g : m.graph)
     if (g) cudaGraphExecDestroy(g);
+  if (m.graph_kv8) cudaGraphExecDestroy(m.graph_kv8);
   for (void* p : m.allocations) cudaFree(p);
   m.allocations.clear();
 }
@@ -512,7 +531,8 @@ constexpr bool diag_skip(const char*) { return false; }
 #endif
 
 void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_identity,
-             bool tokens_independent, bool one_seq = false) {
+             bool tokens_independent, bool one_seq = false, bool kv8 = false) {
+  if (kv8 && !(tokens_independent && T == 1)) throw ConfigErr("FP8 KV cache: batch-1 decode steps only");
   Scratch& s = e->sc;
   cudaStream_t st = e->st;
   const msw_model_cfg& c = m.c;
@@ -549,8 +569,13 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
     }
     const bool run = !tokens_independent && one_seq && T <= kGemvMaxTokens;
     if (tokens_independent || run) {  // decode / CB / short runs: RoPE + KV append fused
-      if (!diag_skip("attn")) launch_attention_decode(s.qkv, m.rope, T, s.pos, s.slot, s.seq_of, m.block_table, kc,
-                              vc, m.ash, nsplit, s.part_o, s.part_ml, s.split_cnt, s.o, st, run);
+      if (kv8)
+        launch_attention_decode_kv8(s.qkv, m.rope, T, s.pos, s.slot, s.seq_of, m.block_table,
+                                    m.kc8 + m.kv_layer_elems * l, m.vc8 + m.kv_layer_elems * l,
+                                    m.ash, nsplit, s.part_o, s.part_ml, s.split_cnt, s.o, st, run);
+      else if (!diag_skip("attn"))
+        launch_attention_decode(s.qkv, m.rope, T, s.pos, s.slot, s.seq_of, m.block_table, kc, vc,
+                                m.ash, nsplit, s.part_o, s.part_ml, s.split_cnt, s.o, st, run);
       n += 1;
     } else {
       launch_rope_append(s.qkv, T, s.pos, s.slot, m.rope, m.ash, s.q16, kc, vc, st);
@@ -765,10 +790,10 @@ void prefill_packed(msw_engine* e, Model& m, int fmt, const std::vector<PackSeq>
 }
 
 // One batch-1 decode step for model m / fmt, as a graph or eagerly.
-void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph) {
+void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph, bool kv8 = false) {
   Scratch& s = e->sc;
   auto body = [&]() {
-    forward(e, m, fmt, 1, 1, true, true);
+    forward(e, m, fmt, 1, 1, true, true, false, kv8);
     launch_advance(s.next, s.tok, s.pos, s.slot, s.step, s.hist, m.block_table, e->st);
     ++e->launches;
   };
@@ -776,7 +801,9 @@ void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph) {
     body();
     return;
   }
-  if (!m.graph[fmt]) {
+  cudaGraphExec_t& gx = kv8 ? m.graph_kv8 : m.graph[fmt];
+  int& gn = kv8 ? m.graph_kv8_nodes : m.graph_nodes[fmt];
+  if (!gx) {
     const long long before = e->launches;
     cudaGraph_t g;
     MSW_CUDA(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
@@ -787,13 +814,13 @@ void decode_step(msw_engine* e, Model& m, int fmt, bool use_graph) {
       throw;
     }
     MSW_CUDA(cudaStreamEndCapture(e->st, &g));
-    MSW_CUDA(cudaGraphInstantiate(&m.graph[fmt], g, 0));
+    MSW_CUDA(cudaGraphInstantiate(&gx, g, 0));
     cudaGraphDestroy(g);
-    m.graph_nodes[fmt] = int(e->launches - before);
+    gn = int(e->launches - before);
     e->launches = before;
   }
-  MSW_CUDA(cudaGraphLaunch(m.graph[fmt], e->st));
-  e->launches += m.graph_nodes[fmt];
+  MSW_CUDA(cudaGraphLaunch(gx, e->st));
+  e->launches += gn;
 }
 
 // Sets the batch-1 decode state so the next decode_step processes `tok_src`
@@ -874,6 +901,72 @@ void run_single(msw_engine* e, const msw_request& r, msw_result& res) {
   res.decode_ms = b;
   res.n_out = n_new;
   res.prefix_hit_tokens = sb.hit_tokens;
+  res.total_ms = now_ms() - t0;
+}
+
+// KV-cache compression (screening mode, reference domain.hpp:81): FP16
+// weights; the prompt is prefilled on the fp16 cache (full-precision prefill
+// attention), its K / V are then converted to FP8 E4M3 blocks of a separate
+// pool and the fp16 blocks are released, so the request holds its context at
+// one byte per element for the whole decode; each decode step appends E4M3
+// K / V and attends over the E4M3 cache (attn_decode_kernel<..., KV8>).
+void run_kvc(msw_engine* e, const msw_request& r, msw_result& res) {
+  Model& m = e->target;
+  if (!m.kc8 || !m.fmt_on[kFP16]) throw ConfigErr("mode not resident in this engine");
+  check_request(e, r, 1);
+  Scratch& s = e->sc;
+  const double t0 = now_ms();
+  const int plen = r.prompt_len, n_new = r.max_new_tokens;
+  SeqBlocks s16 = map_sequence(m, 0, plen, r.prompt_ids, plen, false, kFP16, e->st, s.stage);
+  std::vector<int> b8;
+  const bool want_logits = res.logits != nullptr;
+  const bool graphs = e->cfg.use_graphs && !want_logits;
+  bool released16 = false;
+  try {
+    const int nb8 = (plen + n_new + kKvBlock - 1) / kKvBlock;
+    if (nb8 > m.max_blocks) throw DataErr("sequence longer than max_seq_len");
+    for (int i = 0; i < nb8; ++i) b8.push_back(m.pool8.alloc());
+    MSW_CUDA(cudaEventRecord(e->ev[0], e->st));
+    prefill(e, m, kFP16, 0, r.prompt_ids, 0, plen, s16);
+    if (want_logits) copy_logits_row(e, res.logits, 0);
+    // block lists for the conversion, then the row points at the E4M3 blocks
+    const int nb16 = int(s16.blocks.size());
+    int* stg = s.stage;
+    for (int i = 0; i < nb16; ++i) stg[i] = s16.blocks[i];
+    for (int i = 0; i < nb8; ++i) stg[m.max_blocks + i] = b8[i];
+    MSW_CUDA(cudaMemcpyAsync(m.kvc_blocks, stg, sizeof(int) * (m.max_blocks + nb8),
+                             cudaMemcpyHostToDevice, e->st));
+    MSW_CUDA(cudaMemcpyAsync(m.block_table, stg + m.max_blocks, sizeof(int) * nb8,
+                             cudaMemcpyHostToDevice, e->st));
+    launch_kv_compress(m.kc, m.vc, m.kc8, m.vc8, m.kv_layer_elems, m.c.n_layers, m.kvc_blocks,
+                       m.kvc_blocks + m.max_blocks, plen, m.c.n_kv_heads, m.c.head_dim, e->st);
+    ++e->launches;
+    // stream order: anything that reuses these blocks runs after the conversion
+    release_sequence(m, s16);
+    released16 = true;
+    start_decode(e, m, s.next, plen - 1, 0);
+    MSW_CUDA(cudaEventRecord(e->ev[1], e->st));
+    for (int i = 1; i < n_new; ++i) {
+      decode_step(e, m, kFP16, graphs, /*kv8=*/true);
+      if (want_logits) copy_logits_row(e, res.logits + size_t(i) * m.c.vocab, 0);
+    }
+    MSW_CUDA(cudaEventRecord(e->ev[2], e->st));
+    MSW_CUDA(cudaMemcpyAsync(res.out_ids, s.hist, sizeof(int) * n_new, cudaMemcpyDeviceToHost,
+                             e->st));
+    MSW_CUDA(cudaStreamSynchronize(e->st));
+  } catch (...) {
+    cudaStreamSynchronize(e->st);
+    if (!released16) release_sequence(m, s16);
+    for (int b : b8) m.pool8.release(b);
+    throw;
+  }
+  for (int b : b8) m.pool8.release(b);
+  float a = 0, b = 0;
+  MSW_CUDA(cudaEventElapsedTime(&a, e->ev[0], e->ev[1]));
+  MSW_CUDA(cudaEventElapsedTime(&b, e->ev[1], e->ev[2]));
+  res.prefill_ms = a;
+  res.decode_ms = b;
+  res.n_out = n_new;
   res.total_ms = now_ms() - t0;
 }
 
@@ -1277,6 +1370,8 @@ int msw_engine_run(msw_engine* e, const msw_request* req, msw_result* res) {
       run_spec(e, *req, *res);
     } else if (req->mode == MSW_MODE_INT8_CONT_BATCHING) {
       run_cb(e, req, 1, res);
+    } else if (req->mode == MSW_MODE_KV_COMPRESSION) {
+      run_kvc(e, *req, *res);
     } else {
       run_single(e, *req, *res);
     }
@@ -1336,12 +1431,22 @@ int msw_engine_memory_bytes(msw_engine* e, int32_t mode, int32_t tokens, int64_t
     auto kv_pos = [](const Model& m) {
       return int64_t(2) * m.c.n_layers * m.c.n_kv_heads * m.c.head_dim * 2;  // K + V fp16
     };
-    int64_t b = int64_t(e->target.weight_bytes(fmt)) + int64_t(tokens) * kv_pos(e->target);
+    // KV-cache compression holds the request's context at one byte per element
+    const int64_t kv = mode == MSW_MODE_KV_COMPRESSION ? kv_pos(e->target) / 2 : kv_pos(e->target);
+    int64_t b = int64_t(e->target.weight_bytes(fmt)) + int64_t(tokens) * kv;
     if (mode == MSW_MODE_SPECULATIVE) {
       if (!e->cfg.has_draft) throw ConfigErr("speculative decoding needs a draft model");
       b += int64_t(e->draft.weight_bytes(kFP16)) + int64_t(tokens) * kv_pos(e->draft);
     }
     *bytes = b;
+  });
+}
+
+int msw_fp8_e4m3_roundtrip(const uint16_t* x, int64_t n, uint8_t* q, uint16_t* y, void* stream) {
+  return guarded([&] {
+    if (n % 2) throw DataErr("msw_fp8_e4m3_roundtrip: n must be even");
+    launch_fp8_roundtrip(reinterpret_cast<const half*>(x), n, q, reinterpret_cast<half*>(y),
+                         static_cast<cudaStream_t>(stream));
   });
 }
 

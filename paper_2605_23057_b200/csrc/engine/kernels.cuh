@@ -123,6 +123,20 @@ void launch_attention_decode(const float* qkv, const float2* rope, int T, const 
                              half* vc, const AttnShape& a, int nsplit, float* part_o,
                              float* part_ml, int* counters, float* o, cudaStream_t st,
                              bool run = false);
+// KV-cache compression mode: the same kernel on an FP8 E4M3 paged cache
+// (history widened while staged; new keys / values rounded through E4M3).
+void launch_attention_decode_kv8(const float* qkv, const float2* rope, int T, const int* pos,
+                                 const int* slot, const int* seq_of, const int* block_table,
+                                 uint8_t* kc, uint8_t* vc, const AttnShape& a, int nsplit,
+                                 float* part_o, float* part_ml, int* counters, float* o,
+                                 cudaStream_t st, bool run = false);
+// positions [0, npos) of one sequence, every layer: fp16 cache (blocks b16)
+// -> E4M3 cache (blocks b8); b16 / b8 are device block lists
+void launch_kv_compress(const half* kc, const half* vc, uint8_t* kc8, uint8_t* vc8,
+                        size_t layer_elems, int layers, const int* b16, const int* b8, int npos,
+                        int Hk, int D, cudaStream_t st);
+// test entry: q = E4M3(x) (RNE, satfinite), y = fp16(q); n even
+void launch_fp8_roundtrip(const half* x, int64_t n, uint8_t* q, half* y, cudaStream_t st);
 
 // ---- misc.cu ------------------------------------------------------------------
 void launch_embed(const half* emb, const int* tok, int T, int H, float* h, cudaStream_t st);

@@ -24,7 +24,7 @@ import json
 
 import numpy as np
 
-from .configs import (MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_FP16, MODE_GPTQ4, MODE_GPTQ_PC,
+from .configs import (MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_KV_COMPRESSION, MODE_FP16, MODE_GPTQ4, MODE_GPTQ_PC,
                       MODE_INT8, MODE_INT8_CB, MODE_NAMES, MODE_SPEC)
 from .controller import FAMILIES
 
@@ -35,7 +35,7 @@ NOMINAL = {
     "MemoryPressureLongContext": (2048, 64), "MMLUPro": (400, 16), "GSM8K": (250, 256),
     "TruthfulQA": (200, 64), "GPQA": (500, 16), "MLU": (300, 16)}
 PROFILE_MODES = (MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_SPEC, MODE_GPTQ_PC, MODE_INT8_CB,
-                 MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS)
+                 MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_KV_COMPRESSION)
 CB_COHORT = 4  # co-scheduled requests for the continuous-batching cells (batch_pressure 4)
 PREFIX_LEN = 768  # shared tokens of SharedPrefixChat requests
 

@@ -43,7 +43,7 @@ def test_profile_writer_measures_tiny_engine(cuda_ok, tmp_path):
     meas = measure(eng, out_cap=6)
     eng.close()
     prof = build_profile(meas, 1.0, 1.0)
-    assert len(prof["cells"]) == 9 * 11  # every implemented mode (6 routed + 3 screening) x every family
+    assert len(prof["cells"]) == 10 * 11  # every implemented mode (6 routed + 4 screening) x every family
     assert all(c["latency_speedup"] > 0 and c["provenance"] == "measured" for c in prof["cells"])
     path = str(tmp_path / "p.json")
     write_profile(path, prof)

@@ -1,7 +1,7 @@
 """Production-shape parity on the B200: the Llama-3.1-8B-shape engine (the
 shapes the bench runs: K = 4096 / 14336 decode GEMVs, 32 q / 8 kv heads of
 128, vocab 128256) against the CPU oracle on the same K16 weights, batch-1,
-in FP16, INT8, GPTQ4 and AWQ4 (and GPTQ + prefix caching on a repeated prompt).
+in FP16, INT8, GPTQ4, AWQ4 and KV-cache compression (and GPTQ + prefix caching on a repeated prompt).
 
 This is the only test that drives the 8B-specialised decode kernels (the W4
 issue-lean GEMV with register-resident activation fragments, the 8B attention
@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from paper_2605_23057_b200 import (MODE_AWQ4, MODE_FP16, MODE_GPTQ4, MODE_GPTQ_PC, MODE_INT8, MODE_INT8_CB,
+from paper_2605_23057_b200 import (MODE_AWQ4, MODE_FP16, MODE_KV_COMPRESSION, MODE_GPTQ4, MODE_GPTQ_PC, MODE_INT8, MODE_INT8_CB,
                                    MODE_SPEC, engine_cfg, model_cfg)
 from paper_2605_23057_b200.engine import Engine
 
@@ -26,13 +26,15 @@ pytestmark = pytest.mark.gpu
 # exact. The bar: < 5e-2, and no larger than 1.5x the oracle's own INT8-vs-FP16
 # error on the same prompt. The int32 accumulations themselves are bit-exact
 # (test_kernels_gpu).
-TOL = {MODE_FP16: 2e-3, MODE_INT8: 5e-2, MODE_GPTQ4: 1e-2, MODE_AWQ4: 1e-2, MODE_GPTQ_PC: 1e-2}
-ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_AWQ4: 3, MODE_GPTQ_PC: 2}
+TOL = {MODE_FP16: 2e-3, MODE_INT8: 5e-2, MODE_GPTQ4: 1e-2, MODE_AWQ4: 1e-2, MODE_GPTQ_PC: 1e-2,
+       MODE_KV_COMPRESSION: 1e-2}
+ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_AWQ4: 3, MODE_GPTQ_PC: 2, MODE_KV_COMPRESSION: 9}
 
 
 @pytest.fixture(scope="module")
 def pair8b(cuda_ok):
-    modes = (MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_AWQ4, MODE_GPTQ_PC, MODE_SPEC, MODE_INT8_CB)
+    modes = (MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_AWQ4, MODE_GPTQ_PC, MODE_SPEC, MODE_INT8_CB,
+             MODE_KV_COMPRESSION)
     eng = Engine(engine_cfg(target="llama8b", draft="llama1b", modes=modes, seed=3, kv_blocks=256,
                             max_batch=64, max_seq_len=512))
     orc = O.OracleModel(model_cfg("llama8b"), seed=3, max_ctx=512, modes_mask=0b1111)
@@ -41,7 +43,7 @@ def pair8b(cuda_ok):
     orc.close()
 
 
-@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_AWQ4])
+@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_AWQ4, MODE_KV_COMPRESSION])
 def test_8b_batch1_decode_matches_oracle(pair8b, mode):
     eng, orc = pair8b
     p = (np.random.default_rng(40 + mode).integers(0, eng.vocab, size=21)).astype(np.int32)

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from paper_2605_23057_b200 import (MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_FP16, MODE_GPTQ4,
+from paper_2605_23057_b200 import (MODE_AWQ4, MODE_CHUNKED_PREFILL, MODE_CUDA_GRAPHS, MODE_KV_COMPRESSION, MODE_FP16, MODE_GPTQ4,
                                    MODE_GPTQ_PC, MODE_INT8, MODE_INT8_CB, MODE_SPEC, engine_cfg,
                                    model_cfg)
 from paper_2605_23057_b200._capi import MswError
@@ -23,9 +23,9 @@ from paper_2605_23057_b200.engine import Engine
 
 pytestmark = pytest.mark.gpu
 
-TOL = {MODE_FP16: 2e-3, MODE_INT8: 1e-2, MODE_GPTQ4: 1e-2, MODE_AWQ4: 1e-2, MODE_GPTQ_PC: 1e-2, MODE_INT8_CB: 1e-2,
+TOL = {MODE_FP16: 2e-3, MODE_INT8: 1e-2, MODE_GPTQ4: 1e-2, MODE_AWQ4: 1e-2, MODE_KV_COMPRESSION: 1e-2, MODE_GPTQ_PC: 1e-2, MODE_INT8_CB: 1e-2,
        MODE_SPEC: 2e-3, MODE_CHUNKED_PREFILL: 2e-3, MODE_CUDA_GRAPHS: 2e-3}
-ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_AWQ4: 3, MODE_GPTQ_PC: 2, MODE_INT8_CB: 1,
+ORACLE_MODE = {MODE_FP16: 0, MODE_INT8: 1, MODE_GPTQ4: 2, MODE_AWQ4: 3, MODE_KV_COMPRESSION: 9, MODE_GPTQ_PC: 2, MODE_INT8_CB: 1,
                MODE_CHUNKED_PREFILL: 0, MODE_CUDA_GRAPHS: 0}
 
 
@@ -50,7 +50,7 @@ def _check_logits(gpu, ref, tol):
 
 
 @pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_AWQ4, MODE_CHUNKED_PREFILL,
-                                  MODE_CUDA_GRAPHS])
+                                  MODE_CUDA_GRAPHS, MODE_KV_COMPRESSION])
 @pytest.mark.parametrize("plen,n_new", [(1, 4), (37, 24), (130, 9)])
 def test_batch1_modes_match_oracle(pair, mode, plen, n_new):
     _, eng, orc, _ = pair
@@ -61,7 +61,7 @@ def test_batch1_modes_match_oracle(pair, mode, plen, n_new):
     _check_logits(r.logits, lg, TOL[mode])
 
 
-@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_AWQ4])
+@pytest.mark.parametrize("mode", [MODE_FP16, MODE_INT8, MODE_GPTQ4, MODE_AWQ4, MODE_KV_COMPRESSION])
 def test_graph_replay_equals_oracle_tokens(pair, mode):
     _, eng, orc, _ = pair
     p = prompt(99 + mode, 50, eng.vocab)
@@ -272,3 +272,26 @@ def test_continuous_batching_waits_for_kv_blocks(cuda_ok):
         assert e.value.code == 3
     finally:
         eng.close()
+
+
+def test_kv_compression_runs_on_e4m3_cache(pair):
+    """KV-cache compression (screening mode 9): the decode attends over an E4M3
+    cache. Its logits match the oracle's E4M3-cache run far more closely than
+    the FP16 run of the same request (so the compressed path really ran), the
+    request's KV footprint is one byte per element, and repeated requests
+    leave both block pools balanced (fp16 prefill blocks released after the
+    conversion, E4M3 blocks at the end)."""
+    _, eng, orc, _ = pair
+    p = prompt(4242, 90, eng.vocab)
+    ref, lg = orc.generate(9, p, 20, want_logits=True)
+    _, lg16 = orc.generate(0, p, 20, want_logits=True)
+    for _ in range(3):
+        r = eng.run(MODE_KV_COMPRESSION, p, 20, want_logits=True)
+        assert np.array_equal(r.tokens, ref)
+    err = np.abs(r.logits - lg).max(axis=1) / lg.std(axis=1)
+    e16 = np.abs(r.logits - lg16).max(axis=1) / lg16.std(axis=1)
+    assert err.max() < TOL[MODE_KV_COMPRESSION]
+    assert e16[1:].min() > 3 * err[1:].max(), f"KV-compressed run within reach of FP16: {e16} vs {err}"
+    tokens = 110
+    m16, m8 = eng.memory_bytes(MODE_FP16, tokens), eng.memory_bytes(MODE_KV_COMPRESSION, tokens)
+    assert 2 * (m16 - m8) == m16 - eng.memory_bytes(MODE_FP16, 0)

@@ -277,3 +277,24 @@ def test_linear_awq4_vs_oracle(cuda_ok, t, n, k):
     y = dy.cpu().numpy()
     ref = O.linear_awq4(q, s, z, x)
     assert np.abs(y - ref).max() / np.abs(ref).max() < 2e-3
+
+
+def test_fp8_e4m3_kv_rounding_bit_exact(cuda_ok):
+    """The KV-cache compression mode's E4M3 rounding (cvt.rn.satfinite on the
+    device) against the oracle's restatement (itself pinned to torch's
+    float8_e4m3fn in test_oracle_pin.py) on every finite fp16 value: E4M3
+    bytes and their fp16 widening bit-exact, |x| >= 464 saturating to 448."""
+    torch = _torch()
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    x = bits[np.isfinite(bits.view(np.float16))]
+    x = x[: x.size // 2 * 2]
+    dx = torch.from_numpy(x.view(np.int16)).cuda()
+    q = torch.empty(x.size, dtype=torch.uint8, device="cuda")
+    y = torch.empty(x.size, dtype=torch.int16, device="cuda")
+    check_engine(engine_lib().msw_fp8_e4m3_roundtrip(dx.data_ptr(), x.size, q.data_ptr(), y.data_ptr(), None))
+    torch.cuda.synchronize()
+    rq, ry = O.fp8_e4m3(x)
+    assert np.array_equal(q.cpu().numpy(), rq)
+    assert np.array_equal(y.cpu().numpy().view(np.uint16), ry)
+    big = np.abs(x.view(np.float16).astype(np.float32)) >= 464
+    assert big.any() and np.all(np.abs(ry[big].view(np.float16).astype(np.float32)) == 448)

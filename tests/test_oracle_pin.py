@@ -220,3 +220,17 @@ def test_oracle_awq4_matches_autoawq_pseudo_quantize(orc):
     assert np.array_equal(zz.squeeze(2).numpy().astype(np.uint8), z)
     assert np.array_equal(qq.reshape(q.shape).numpy().astype(np.uint8), q)
     assert len(np.unique(z)) > 1  # zero points vary per group (uniform init: 7 or 8)
+
+
+def test_fp8_e4m3_restatement_matches_torch():
+    """oracle fp8_e4m3 (the KV-cache compression mode's rounding) equals
+    torch's float8_e4m3fn conversion (round to nearest even) on every finite
+    fp16 value below the saturation threshold, byte for byte."""
+    import torch
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    v = bits.view(np.float16)
+    x = bits[np.isfinite(v) & (np.abs(v.astype(np.float32)) < 464)]
+    q, y = O.fp8_e4m3(x)
+    t = torch.from_numpy(x.view(np.float16).copy()).to(torch.float8_e4m3fn)
+    assert np.array_equal(t.view(torch.uint8).numpy(), q)
+    assert np.array_equal(t.to(torch.float16).numpy().view(np.uint16), y)
