@@ -437,8 +437,10 @@ void build_model(Model& m, const msw_model_cfg& c, bool is_draft, const msw_engi
   m.ash = AttnShape{Hq, Hk, D, m.max_blocks, m.nblk};
   // decode attention splits hold >= 256 positions (attention.cu kDecMinChunk):
   // no more splits than max_seq_len needs, so short-context engines do not
-  // launch idle CTAs
-  m.nsplit = std::max(1, std::min({32, (2 * kNumSMs) / Hk, (cfg.max_seq_len + 255) / 256}));
+  // launch idle CTAs; and no more (token, kv head, split) CTAs than SMs, so
+  // the 8-warp CTAs (139 KB of staging, one per SM) run in ONE wave (32
+  // splits x 8 kv heads at 8K context ran as two)
+  m.nsplit = std::max(1, std::min({32, kNumSMs / Hk, (cfg.max_seq_len + 255) / 256}));
 }
 
 void free_model(Model& m) {
@@ -542,7 +544,7 @@ void forward(msw_engine* e, Model& m, int fmt, int T, int n_logits, bool rows_id
   const int kfmt = fmt == kSlotAWQ4 ? kW4 : fmt;  // activation handling of the weight slot
   // attention splits: enough CTAs to fill the GPU, fewer as the token count grows
   int nsplit = 1;
-  if (T <= kMaxLogitRows) nsplit = std::max(1, std::min(m.nsplit, (2 * kNumSMs) / (T * Hk)));
+  if (T <= kMaxLogitRows) nsplit = std::max(1, std::min(m.nsplit, kNumSMs / (T * Hk)));
   long long& n = e->launches;
 
   LinearW head;

@@ -137,9 +137,12 @@ struct TcCfg {
   // a short prefill / CB step streams weights at HBM rate only with enough
   // bytes in flight per SM (latency x bandwidth / 148)
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagesFit = (220 * 1024 - kPkStages * kPkBytes) / kStageBytes;
+  // W4 with 128 x 256 tiles: a 4-deep packed ring (16 KB) leaves room for a
+  // 4th operand stage (the dequantisers can only fill a slot the MMA freed)
+  static constexpr int kPk = kIsW4 && BN > 128 ? 4 : kPkStages;
+  static constexpr int kStagesFit = (220 * 1024 - kPk * kPkBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
-  static constexpr int kRingBytes = kStages * (kABytes + kBBytes) + kPkStages * kPkBytes;
+  static constexpr int kRingBytes = kStages * (kABytes + kBBytes) + kPk * kPkBytes;
   static constexpr int kSmem = kRingBytes + 1024 /*align*/ + 512 /*barriers*/;
   // split-K partial tile [BN][128] (fp32 / int32), staged in the A ring once
   // every MMA has completed; up to ks-1 incoming column slices ((ks-1)/ks of
@@ -190,8 +193,8 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kRingBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* pfull = empty + C::kStages;
-  uint64_t* pempty = pfull + kPkStages;
-  uint64_t* done = pempty + kPkStages;
+  uint64_t* pempty = pfull + C::kPk;
+  uint64_t* done = pempty + C::kPk;
   uint64_t* rbar = done + 1;  // split-K: incoming partial slices
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 1);
 
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       mbar_init(&full[s], C::kIsW4 ? 1 + C::kDqWarps : 1);  // TMA arrive (+ dequant warps)
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < kPkStages; ++s) {
+    for (int s = 0; s < C::kPk; ++s) {
       mbar_init(&pfull[s], 1);
       mbar_init(&pempty[s], C::kDqWarps);
     }
@@ -264,10 +267,10 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     umma_commit(done);  // with nk == 0 this still arrives (no MMA issued: D stays unwritten)
   } else if (C::kIsW4 && warp == 3 && lane == 0) {
     // ---- W4 packed-weight producer: 128 rows x 64 k (8 words per row, 4 KB)
-    // per k-tile, kPkStages deep, ahead of the dequantisers
+    // per k-tile, C::kPk deep, ahead of the dequantisers
     for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % kPkStages;
-      const uint32_t ph = (kb / kPkStages) & 1;
+      const int s = kb % C::kPk;
+      const uint32_t ph = (kb / C::kPk) & 1;
       mbar_wait(&pempty[s], ph ^ 1);
       fence_proxy_async();  // dequantisers' generic reads of this slot before the TMA overwrite
       mbar_expect_tx(&pfull[s], C::kPkBytes);
@@ -284,8 +287,8 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     const uint8_t* zrow = wzero ? wzero + size_t(n0 + r) * (K / kW4Group) : nullptr;
     const half2 k1032 = __float2half2_rn(1032.0f);
     for (int kb = 0; kb < nk; ++kb) {
-      const int ps = kb % kPkStages;
-      const uint32_t pph = (kb / kPkStages) & 1;
+      const int ps = kb % C::kPk;
+      const uint32_t pph = (kb / C::kPk) & 1;
       const int s = kb % C::kStages;
       const uint32_t ph = (kb / C::kStages) & 1;
       const int grp = ((kb0 + kb) * 64) / kW4Group;
