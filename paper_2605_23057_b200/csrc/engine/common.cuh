@@ -88,6 +88,11 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
 }
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + expf(-g)); }
+// Prefill-GEMM epilogue SiLU: ex2.approx-based exp and the fast divide (a
+// few ulp of fp32 from silu(); the product is rounded to fp16 or int8 before
+// the next linear). silu() cost ~40 instructions per element, which made the
+// gate_up GEMM's epilogue ~1/3 of its time at 128 x 256 tiles.
+__device__ __forceinline__ float silu_fast(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Intra-CTA timeline probes, compiled only into the diagnostics build
 // (-DMSW_TRACE -> libmsw_engine_trace.so, scripts/gemv_timeline.py). Slot i of

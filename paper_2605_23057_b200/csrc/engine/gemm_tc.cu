@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
                                  : __uint_as_float(u);
     if (EPI == kEpiSwiglu) {  // rows (2i, 2i+1) = (gate_i, up_i) sit in adjacent lanes
       const float up = __shfl_xor_sync(0xffffffffu, v, 1);
-      if (t < T && (lane & 1) == 0) y[size_t(t) * (N / 2) + (n >> 1)] = silu(v) * up;
+      if (t < T && (lane & 1) == 0) y[size_t(t) * (N / 2) + (n >> 1)] = silu_fast(v) * up;
     } else if (t < T) {
       if (EPI == kEpiStore) y[size_t(t) * N + n] = v;
       else y[size_t(t) * N + n] = prev[j & 15] + v;  // prev: this 16-column batch's y
@@ -370,8 +370,27 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
         for (int j = 0; j < 16; ++j) {  // residual: all 16 reads in flight before the adds
           if (EPI == kEpiResid) prev[j] = t0 + j0 + j < T ? y[size_t(t0 + j0 + j) * N + n] : 0.0f;
         }
+        if (EPI == kEpiSwiglu) {
+          // column pairs: the even lane (gate) finishes column j, the odd lane
+          // (up) column j + 1, one shuffle each way: one SiLU per lane per two
+          // columns instead of 16 idle odd lanes per column
 #pragma unroll
-        for (int j = 0; j < 16; ++j) emit(j0 + j, r[j]);
+          for (int j = 0; j < 16; j += 2) {
+            const int ta = t0 + j0 + j, tb = ta + 1;
+            const float v0 = FMT == kINT8 ? (float(int(r[j])) * (ta < T ? xscale[ta] : 0.0f)) * ws
+                                          : __uint_as_float(r[j]);
+            const float v1 = FMT == kINT8 ? (float(int(r[j + 1])) * (tb < T ? xscale[tb] : 0.0f)) * ws
+                                          : __uint_as_float(r[j + 1]);
+            const bool odd = lane & 1;
+            const float got = __shfl_xor_sync(0xffffffffu, odd ? v0 : v1, 1);
+            const float g = odd ? got : v0, u = odd ? v1 : got;
+            const int t = odd ? tb : ta;
+            if (t < T) y[size_t(t) * (N / 2) + (n >> 1)] = silu_fast(g) * u;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) emit(j0 + j, r[j]);
+        }
       }
     }
   } else if constexpr (C::kCanSplit) {
