@@ -10,7 +10,12 @@
 namespace msw {
 namespace {
 
-constexpr int kPrepThreads = 256;
+// One CTA per token; the row is read from HBM once into registers (float4,
+// up to kPrepV per thread) and normalised, reduced and converted there: one
+// read pass instead of two (FP16) or three (INT8: sum of squares, absmax,
+// quantise) over the row.
+constexpr int kPrepThreads = 512;
+constexpr int kPrepV = 8;  // float4 per thread: K <= 16384
 
 __global__ void __launch_bounds__(kPrepThreads)
     prep_act_kernel(int fmt, const float* __restrict__ x, int K, const half* __restrict__ gamma,
@@ -18,29 +23,62 @@ __global__ void __launch_bounds__(kPrepThreads)
                     float* __restrict__ xscale) {
   __shared__ float red[32];
   const size_t t = blockIdx.x;
-  const float* xr = x + t * K;
-  float r = 1.0f;
+  const int n4 = K / 4;
+  const float4* xr = reinterpret_cast<const float4*>(x + t * K);
+  float4 v[kPrepV];
+#pragma unroll
+  for (int j = 0; j < kPrepV; ++j) {
+    const int i = threadIdx.x + j * kPrepThreads;
+    v[j] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   if (gamma != nullptr) {
     float ss = 0.0f;
-    for (int i = threadIdx.x; i < K; i += kPrepThreads) ss = fmaf(xr[i], xr[i], ss);
+#pragma unroll
+    for (int j = 0; j < kPrepV; ++j)
+      ss = fmaf(v[j].x, v[j].x, fmaf(v[j].y, v[j].y, fmaf(v[j].z, v[j].z, fmaf(v[j].w, v[j].w, ss))));
     ss = block_sum(ss, red);
-    r = 1.0f / sqrtf(ss / float(K) + eps);
+    const float r = 1.0f / sqrtf(ss / float(K) + eps);
+#pragma unroll
+    for (int j = 0; j < kPrepV; ++j) {
+      const int i = threadIdx.x + j * kPrepThreads;
+      if (i < n4) {
+        const half2* g = reinterpret_cast<const half2*>(gamma) + 2 * i;
+        const float2 g0 = __half22float2(g[0]), g1 = __half22float2(g[1]);
+        v[j].x = (v[j].x * r) * g0.x;
+        v[j].y = (v[j].y * r) * g0.y;
+        v[j].z = (v[j].z * r) * g1.x;
+        v[j].w = (v[j].w * r) * g1.y;
+      }
+    }
   }
-  auto act = [&](int i) -> float {
-    return gamma != nullptr ? (xr[i] * r) * __half2float(gamma[i]) : xr[i];
-  };
   if (fmt == kINT8) {
     float amax = 0.0f;
-    for (int i = threadIdx.x; i < K; i += kPrepThreads) amax = fmaxf(amax, fabsf(act(i)));
+#pragma unroll
+    for (int j = 0; j < kPrepV; ++j)
+      amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
     amax = block_max(amax, red);
     const float s = amax / 127.0f;
-    for (int i = threadIdx.x; i < K; i += kPrepThreads) {
-      const float v = amax > 0.0f ? rintf(act(i) / s) : 0.0f;
-      xq[t * K + i] = static_cast<int8_t>(fminf(fmaxf(v, -127.0f), 127.0f));
+    auto q = [&](float u) -> int8_t {
+      const float w = amax > 0.0f ? rintf(u / s) : 0.0f;
+      return static_cast<int8_t>(fminf(fmaxf(w, -127.0f), 127.0f));
+    };
+#pragma unroll
+    for (int j = 0; j < kPrepV; ++j) {
+      const int i = threadIdx.x + j * kPrepThreads;
+      if (i < n4)
+        reinterpret_cast<char4*>(xq + t * K)[i] = make_char4(q(v[j].x), q(v[j].y), q(v[j].z), q(v[j].w));
     }
     if (threadIdx.x == 0) xscale[t] = s;
   } else {
-    for (int i = threadIdx.x; i < K; i += kPrepThreads) xh[t * K + i] = __float2half_rn(act(i));
+#pragma unroll
+    for (int j = 0; j < kPrepV; ++j) {
+      const int i = threadIdx.x + j * kPrepThreads;
+      if (i < n4) {
+        half2* o = reinterpret_cast<half2*>(xh + t * K) + 2 * i;
+        o[0] = __floats2half2_rn(v[j].x, v[j].y);
+        o[1] = __floats2half2_rn(v[j].z, v[j].w);
+      }
+    }
   }
 }
 
@@ -172,6 +210,7 @@ void gemm_fmt(const LinearW& W, int epi, const half* xh, const int8_t* xq, const
 
 void launch_prep_act(int fmt, const float* x, int T, int K, const half* gamma, float eps, half* xh,
                      int8_t* xq, float* xscale, cudaStream_t st) {
+  if (K % 4 || K > kPrepThreads * kPrepV * 4) throw ConfigErr("prep_act: K must be a multiple of 4, <= 16384");
   prep_act_kernel<<<T, kPrepThreads, 0, st>>>(fmt, x, K, gamma, eps, xh, xq, xscale);
   MSW_LAUNCH_CHECK();
 }
