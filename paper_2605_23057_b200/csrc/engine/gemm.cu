@@ -22,6 +22,11 @@ __global__ void __launch_bounds__(kPrepThreads)
                     float eps, half* __restrict__ xh, int8_t* __restrict__ xq,
                     float* __restrict__ xscale) {
   __shared__ float red[32];
+  // PDL: the row comes from the previous kernel, and xh / xq may still be
+  // read by the GEMM before that; the next GEMM may launch (and stream its
+  // weights) as soon as every row CTA is past this point
+  pdl_wait();
+  pdl_trigger();
   const size_t t = blockIdx.x;
   const int n4 = K / 4;
   const float4* xr = reinterpret_cast<const float4*>(x + t * K);
@@ -211,8 +216,7 @@ void gemm_fmt(const LinearW& W, int epi, const half* xh, const int8_t* xq, const
 void launch_prep_act(int fmt, const float* x, int T, int K, const half* gamma, float eps, half* xh,
                      int8_t* xq, float* xscale, cudaStream_t st) {
   if (K % 4 || K > kPrepThreads * kPrepV * 4) throw ConfigErr("prep_act: K must be a multiple of 4, <= 16384");
-  prep_act_kernel<<<T, kPrepThreads, 0, st>>>(fmt, x, K, gamma, eps, xh, xq, xscale);
-  MSW_LAUNCH_CHECK();
+  launch_pdl(prep_act_kernel, dim3(T), dim3(kPrepThreads), 0, st, fmt, x, K, gamma, eps, xh, xq, xscale);
 }
 
 void launch_gemm(const LinearW& W, int epi, const half* xh, const int8_t* xq, const float* xscale,

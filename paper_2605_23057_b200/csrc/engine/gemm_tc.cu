@@ -238,13 +238,24 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // ---- TMA producer: activation tiles (+ weight tiles for FP16 / INT8)
+    // ---- TMA producer: activation tiles (+ weight tiles for FP16 / INT8).
+    // PDL: the first ring's weight tiles are requested before
+    // griddepcontrol.wait (weights are never written by a kernel), the
+    // activation tiles only after it
+    const int npre = C::kIsW4 ? 0 : min(nk, C::kStages);
+    for (int kb = 0; kb < npre; ++kb) {  // fresh slots: no empty wait
+      mbar_expect_tx(&full[kb], C::kABytes + C::kBBytes);
+      tma_load_2d(sA + kb * C::kABytes, &tmA, &full[kb], (kb0 + kb) * C::kTileK, n0);
+    }
+    pdl_wait();
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % C::kStages;
       const uint32_t ph = (kb / C::kStages) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      mbar_expect_tx(&full[s], C::kIsW4 ? C::kBBytes : C::kABytes + C::kBBytes);
-      if (!C::kIsW4) tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * C::kTileK, n0);
+      if (kb >= npre) {
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], C::kIsW4 ? C::kBBytes : C::kABytes + C::kBBytes);
+        if (!C::kIsW4) tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * C::kTileK, n0);
+      }
       tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kb) * C::kTileK, t0);
     }
   } else if (warp == 1 && lane == 0) {
@@ -320,6 +331,9 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     }
   }
 
+  // the next kernel may launch once every CTA's mainloop is issued (it
+  // waits for this grid's completion before reading y)
+  pdl_trigger();
   // ---- epilogue (warps 0-3): TMEM lane = weight row, column = token
   __syncwarp();  // reconverge the producer / MMA lanes before .sync.aligned TMEM loads
   const int row = (warp & 3) * 32 + lane;
@@ -535,13 +549,15 @@ void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, f
   cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = ksplit;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (weights before the wait)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   MSW_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<FMT, BN, EPI>, ta, tb, W.n, W.k, T, W.s, xscale,
                               y, ksplit, FMT == kW4 ? W.z : static_cast<const uint8_t*>(nullptr)));
 }
