@@ -91,6 +91,22 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, ui
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
   }
 }
+// A operand from TMEM (the W4 dequantisers' fp16 tile), B from shared memory
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -132,17 +148,27 @@ struct TcCfg {
   // fp16 operand production ahead of the MMA (4 warps bounded W4 prefill below FP16)
   static constexpr int kDqWarps = 8;
   static constexpr int kThreads = kIsW4 ? 128 + kDqWarps * 32 : 128;
-  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  // W4 with 128 x 256 tiles: the dequantised A tile goes to TMEM (tcgen05.st,
+  // MMA with A from TMEM) instead of a swizzled shared-memory tile: the
+  // operand path then moves 36 KB of shared memory per k-tile (B + packed
+  // words) instead of 68 KB (B + packed + A written and read), which bounded
+  // the W4 prefill GEMM below FP16. TMEM: accumulator [0, 256), A stages of
+  // 32 columns (128 rows x 64 k fp16) from column 256.
+  static constexpr bool kAT = kIsW4 && BN == 256;
+  static constexpr int kARing = kAT ? 0 : kABytes;  // A bytes per shared-memory stage
+  static constexpr uint32_t kColA = BN;
+  static constexpr int kTmemCols = kAT ? 512 : (BN < 32 ? 32 : BN);
   // operand ring as deep as ~220 KB of shared memory allows (one CTA per SM):
   // a short prefill / CB step streams weights at HBM rate only with enough
   // bytes in flight per SM (latency x bandwidth / 148)
-  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStageBytes = kARing + kBBytes;
   // W4 with 128 x 256 tiles: a 4-deep packed ring (16 KB) leaves room for a
   // 4th operand stage (the dequantisers can only fill a slot the MMA freed)
   static constexpr int kPk = kIsW4 && BN > 128 ? 4 : kPkStages;
   static constexpr int kStagesFit = (220 * 1024 - kPk * kPkBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
-  static constexpr int kRingBytes = kStages * (kABytes + kBBytes) + kPk * kPkBytes;
+  static constexpr int kRingBytes = kStages * (kARing + kBBytes) + kPk * kPkBytes;
+  static_assert(!kAT || int(kColA) + kStages * 32 <= kTmemCols, "A stages must fit TMEM");
   static constexpr int kSmem = kRingBytes + 1024 /*align*/ + 512 /*barriers*/;
   // split-K partial tile [BN][128] (fp32 / int32), staged in the A ring once
   // every MMA has completed; up to ks-1 incoming column slices ((ks-1)/ks of
@@ -188,7 +214,7 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint8_t* sB = smem + C::kStages * C::kARing;
   uint8_t* sP = sB + C::kStages * C::kBBytes;  // W4 packed ring
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kRingBytes);
   uint64_t* empty = full + C::kStages;
@@ -266,12 +292,16 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       const uint32_t ph = (kb / C::kStages) & 1;
       mbar_wait(&full[s], ph);
       tc_fence_after();
-      const uint32_t a0 = smem_u32(sA + s * C::kABytes);
+      const uint32_t a0 = smem_u32(sA + s * C::kARing);
       const uint32_t b0 = smem_u32(sB + s * C::kBBytes);
 #pragma unroll
       for (int k = 0; k < C::kTileK / C::kUmmaK; ++k) {
         const uint32_t off = k * C::kUmmaK * C::kElt;  // bytes along the swizzled row
-        umma<FMT>(tmem, sw128_desc(a0 + off), sw128_desc(b0 + off), idesc, (kb | k) != 0);
+        if constexpr (C::kAT)  // 16 k = 8 TMEM columns of fp16 pairs per MMA
+          umma_ts(tmem, tmem + C::kColA + uint32_t(s) * 32 + uint32_t(k) * 8, sw128_desc(b0 + off),
+                  idesc, (kb | k) != 0);
+        else
+          umma<FMT>(tmem, sw128_desc(a0 + off), sw128_desc(b0 + off), idesc, (kb | k) != 0);
       }
       umma_commit(&empty[s]);
     }
@@ -310,22 +340,41 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&pempty[ps]);
       mbar_wait(&empty[s], ph ^ 1);
-      uint8_t* rowp = sA + s * C::kABytes + r * 128;
       const uint32_t words[4] = {p0.x, p0.y, p0.z, p0.w};
+      if constexpr (C::kAT) {
+        // TMEM lane = row r (this warp's lane quarter is (warp & 3) = r / 32),
+        // columns 16 hf .. 16 hf + 15 of stage s = k pairs 32 hf .. 32 hf + 31
+        tc_fence_after();  // the MMAs that read this stage (empty barrier) before the overwrite
+        uint32_t out[16];
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {  // chunk c = k 8c..8c+7 = packed word c
-        const int c = 4 * hf + cc;
-        uint32_t out[4];
+        for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint32_t u = lop3_and_or(words[cc] >> (4 * i), 0x000F000Fu, 0x64006400u);
-          const half2 q = __hsub2(*reinterpret_cast<const half2*>(&u), kz);
-          const half2 wv = __hmul2(q, s2);
-          out[i] = *reinterpret_cast<const uint32_t*>(&wv);
+          for (int i = 0; i < 4; ++i) {  // nibbles i, i+4 of word cc = elements 8cc+2i, +1
+            uint32_t u = lop3_and_or(words[cc] >> (4 * i), 0x000F000Fu, 0x64006400u);
+            const half2 q = __hsub2(*reinterpret_cast<const half2*>(&u), kz);
+            const half2 wv = __hmul2(q, s2);
+            out[4 * cc + i] = *reinterpret_cast<const uint32_t*>(&wv);
+          }
+        tmem_st16(tmem + (uint32_t((warp & 3) * 32) << 16) + C::kColA + uint32_t(s) * 32 + 16 * hf, out);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+      } else {
+        uint8_t* rowp = sA + s * C::kABytes + r * 128;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {  // chunk c = k 8c..8c+7 = packed word c
+          const int c = 4 * hf + cc;
+          uint32_t out[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint32_t u = lop3_and_or(words[cc] >> (4 * i), 0x000F000Fu, 0x64006400u);
+            const half2 q = __hsub2(*reinterpret_cast<const half2*>(&u), kz);
+            const half2 wv = __hmul2(q, s2);
+            out[i] = *reinterpret_cast<const uint32_t*>(&wv);
+          }
+          *reinterpret_cast<uint4*>(rowp + ((c ^ (r & 7)) << 4)) = make_uint4(out[0], out[1], out[2], out[3]);
         }
-        *reinterpret_cast<uint4*>(rowp + ((c ^ (r & 7)) << 4)) = make_uint4(out[0], out[1], out[2], out[3]);
+        fence_async_smem();  // generic-proxy stores -> visible to the tensor core
       }
-      fence_async_smem();  // generic-proxy stores -> visible to the tensor core
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[s]);
     }
