@@ -68,12 +68,12 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-template <int FMT, int BN>
+template <int FMT, int BN, int M = kTileM>
 __device__ __forceinline__ constexpr uint32_t instr_desc() {
   // c_format bits 4-5 (F32=1, S32=2); a/b format bits 7-9 / 10-12 (F16=0; INT8 signed=1);
   // K-major A and B; N>>3 at bits 17-22; M>>4 at bits 24-28.
   return (FMT == kINT8 ? (2u << 4) | (1u << 7) | (1u << 10) : (1u << 4)) |
-         (uint32_t(BN >> 3) << 17) | (uint32_t(kTileM >> 4) << 24);
+         (uint32_t(BN >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
 template <int FMT>
@@ -107,6 +107,42 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+// CTA-pair MMA (cta_group::2, issued by the pair's leader): D[256 x N] with A
+// rows 0..127 from the leader's shared memory and 128..255 from the peer's (same
+// offsets), B columns split between the two CTAs, D rows in each CTA's TMEM.
+template <int FMT>
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  if (FMT == kINT8) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  }
+}
+// arrive on the barrier at this offset in both CTAs of the pair once the MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+// TMA into this CTA's shared memory, completion counted on the pair leader's
+// mbarrier at the same offset (peer bit of the shared::cluster address cleared)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -135,14 +171,19 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t
 constexpr int kMaxSplit = 8;  // portable cluster size
 constexpr int kPkStages = 8;  // W4: packed-weight ring depth (4 KB stages)
 
-template <int FMT, int BN>
+// CG = 2: CTA pair (cta_group::2) over two adjacent weight-row tiles sharing
+// a token tile; each CTA holds its 128 weight rows and HALF of the token
+// tile, so one k-tile moves 16 + 16 KB through a CTA's shared memory instead
+// of 16 + 32 KB. With 128 x 256 tiles the single-CTA ring (TMA writes + MMA
+// reads ~190 B/clk/SM at the f16 rate) is shared-memory-bandwidth bound.
+template <int FMT, int BN, int CG = 1>
 struct TcCfg {
   static constexpr bool kIsW4 = FMT == kW4;
   static constexpr int kElt = FMT == kINT8 ? 1 : 2;
   static constexpr int kTileK = kTileKBytes / kElt;           // elements per k-tile
   static constexpr int kUmmaK = FMT == kINT8 ? 32 : 16;       // elements per UMMA
   static constexpr int kABytes = kTileM * kTileKBytes;        // 16 KB
-  static constexpr int kBBytes = BN * kTileKBytes;
+  static constexpr int kBBytes = (BN / CG) * kTileKBytes;  // this CTA's token rows
   static constexpr int kPkBytes = kIsW4 ? kTileM * 32 : 0;    // 128 rows x 8 packed words
   // W4: 8 dequantiser warps (two per weight row, 4 packed words each) keep the
   // fp16 operand production ahead of the MMA (4 warps bounded W4 prefill below FP16)
@@ -175,7 +216,8 @@ struct TcCfg {
   // a tile) land in the B ring
   static_assert(kStages >= (BN > 128 ? 3 : 4), "ring too shallow");
   // split-K (BN <= 128 only; long prefills fill the machine without it)
-  static constexpr bool kCanSplit = BN <= 128;
+  static constexpr bool kCanSplit = BN <= 128 && CG == 1;
+  static_assert(CG == 1 || (!kIsW4 && BN == 256), "CTA pairs: FP16 / INT8 with 128 x 256 tiles");
   static_assert(!kCanSplit || BN * kTileM * 4 <= kStages * kABytes, "partial tile must fit the A ring");
   static_assert(!kCanSplit || BN * kTileM * 4 <= kStages * kBBytes, "incoming slices must fit the B ring");
 };
@@ -203,13 +245,13 @@ __device__ __forceinline__ void bulk_s2s_peer(void* dst, const void* src, uint32
       : "memory");
 }
 
-template <int FMT, int BN, int EPI>
-__global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
+template <int FMT, int BN, int EPI, int CG>
+__global__ void __launch_bounds__(TcCfg<FMT, BN, CG>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int N, int K, int T, const void* __restrict__ wscale,
                    const float* __restrict__ xscale, float* __restrict__ y, int ksplit,
                    const uint8_t* __restrict__ wzero) {
-  using C = TcCfg<FMT, BN>;
+  using C = TcCfg<FMT, BN, CG>;
   using Acc32 = typename std::conditional<FMT == kINT8, int, float>::type;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -230,7 +272,10 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   // (T = 1024: 8 token tiles) reads each weight byte from HBM once and from
   // L2 for the other tiles (weight-tile-major order read it 8 times: 1.89 GB
   // of DRAM for a 235 MB FP16 gate_up)
-  const int t0 = blockIdx.x * BN, n0 = blockIdx.y * kTileM;
+  // CTA pairs sit along x (the pair is two x-adjacent CTAs of a (2,1,1)
+  // cluster): x = 2 * token tile + rank, y = weight-row tile pair
+  const int t0 = (CG == 2 ? (blockIdx.x >> 1) : blockIdx.x) * BN;
+  const int n0 = (CG == 2 ? blockIdx.y * 2 + (blockIdx.x & 1) : blockIdx.y) * kTileM;
   // split-K: blockIdx.z (= cluster rank) owns k-tiles [kb0, kb0 + nk)
   const int nk_all = K / C::kTileK;
   const int nk_per = (nk_all + ksplit - 1) / ksplit;
@@ -253,15 +298,24 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(C::kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(C::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(C::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t prank = CG == 2 ? cluster_ctarank() : 0;  // 0: the pair's leader
+  if (CG == 2) cluster_sync_all();  // both CTAs' barriers initialised before any pair traffic
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer: activation tiles (+ weight tiles for FP16 / INT8).
@@ -269,20 +323,67 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
     // griddepcontrol.wait (weights are never written by a kernel), the
     // activation tiles only after it
     const int npre = C::kIsW4 ? 0 : min(nk, C::kStages);
-    for (int kb = 0; kb < npre; ++kb) {  // fresh slots: no empty wait
-      mbar_expect_tx(&full[kb], C::kABytes + C::kBBytes);
-      tma_load_2d(sA + kb * C::kABytes, &tmA, &full[kb], (kb0 + kb) * C::kTileK, n0);
-    }
-    pdl_wait();
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % C::kStages;
-      const uint32_t ph = (kb / C::kStages) & 1;
-      if (kb >= npre) {
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], C::kIsW4 ? C::kBBytes : C::kABytes + C::kBBytes);
-        if (!C::kIsW4) tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * C::kTileK, n0);
+    if constexpr (CG == 2) {
+      // pair: the leader arms its full barrier for both CTAs' bytes; both
+      // CTAs' loads complete on it. A: this CTA's 128 weight rows; B: its
+      // half of the token tile.
+      constexpr uint32_t kPairBytes = 2u * (C::kABytes + C::kBBytes);
+      const int tb = t0 + int(prank) * (BN / 2);
+      for (int kb = 0; kb < npre; ++kb) {  // fresh slots: no empty wait
+        if (prank == 0) mbar_expect_tx(&full[kb], kPairBytes);
+        tma_load_2d_pair(sA + kb * C::kABytes, &tmA, &full[kb], (kb0 + kb) * C::kTileK, n0);
       }
-      tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kb) * C::kTileK, t0);
+      pdl_wait();
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % C::kStages;
+        const uint32_t ph = (kb / C::kStages) & 1;
+        if (kb >= npre) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (prank == 0) mbar_expect_tx(&full[s], kPairBytes);
+          tma_load_2d_pair(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * C::kTileK, n0);
+        }
+        tma_load_2d_pair(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kb) * C::kTileK, tb);
+      }
+      // drain: every slot released by the leader's MMAs, so no pair commit
+      // arrives on this CTA's barriers after it exits
+      for (int kb = nk; kb < nk + C::kStages; ++kb)
+        if (kb >= C::kStages) mbar_wait(&empty[kb % C::kStages], ((kb / C::kStages) & 1) ^ 1);
+    } else {
+      for (int kb = 0; kb < npre; ++kb) {  // fresh slots: no empty wait
+        mbar_expect_tx(&full[kb], C::kABytes + C::kBBytes);
+        tma_load_2d(sA + kb * C::kABytes, &tmA, &full[kb], (kb0 + kb) * C::kTileK, n0);
+      }
+      pdl_wait();
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % C::kStages;
+        const uint32_t ph = (kb / C::kStages) & 1;
+        if (kb >= npre) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], C::kIsW4 ? C::kBBytes : C::kABytes + C::kBBytes);
+          if (!C::kIsW4) tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * C::kTileK, n0);
+        }
+        tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kb) * C::kTileK, t0);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && CG == 2) {
+    // ---- pair MMA issuer (leader only): M = 256 over both CTAs' weight rows
+    if (prank == 0) {
+      constexpr uint32_t idesc = instr_desc<FMT, BN, 2 * kTileM>();
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % C::kStages;
+        const uint32_t ph = (kb / C::kStages) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + s * C::kABytes);
+        const uint32_t b0 = smem_u32(sB + s * C::kBBytes);
+#pragma unroll
+        for (int k = 0; k < C::kTileK / C::kUmmaK; ++k) {
+          const uint32_t off = k * C::kUmmaK * C::kElt;
+          umma_pair<FMT>(tmem, sw128_desc(a0 + off), sw128_desc(b0 + off), idesc, (kb | k) != 0);
+        }
+        umma_commit_pair(&empty[s]);
+      }
+      umma_commit_pair(done);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer
@@ -512,9 +613,14 @@ __global__ void __launch_bounds__(TcCfg<FMT, BN>::kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();  // the pair's MMAs and commits are complete in both CTAs
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(C::kTmemCols));
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(C::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(C::kTmemCols));
   }
 }
 
@@ -571,15 +677,15 @@ int choose_split(int tiles, int nk, int slots) {
   return ks;
 }
 
-template <int FMT, int BN, int EPI>
+template <int FMT, int BN, int EPI, int CG>
 void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, float* y,
                cudaStream_t st) {
-  using C = TcCfg<FMT, BN>;
+  using C = TcCfg<FMT, BN, CG>;
   static int per_sm = 0;
   if (!per_sm) {
-    MSW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<FMT, BN, EPI>,
+    MSW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<FMT, BN, EPI, CG>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    MSW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_tc_kernel<FMT, BN, EPI>,
+    MSW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_tc_kernel<FMT, BN, EPI, CG>,
                                                            C::kThreads, C::kSmem));
     per_sm = std::max(per_sm, 1);
   }
@@ -590,37 +696,44 @@ void launch_bn(const LinearW& W, const void* xact, const float* xscale, int T, f
       FMT == kW4 ? make_map(W.w, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, W.n, W.k / 8, kTileM, 32,
                             CU_TENSOR_MAP_SWIZZLE_NONE)
                  : make_sw128_map(W.w, elt, W.n, W.k, kTileM);
-  const CUtensorMap tb = make_sw128_map(xact, elt, T, W.k, BN);
+  const CUtensorMap tb = make_sw128_map(xact, elt, T, W.k, BN / CG);
   const int tiles = (W.n / kTileM) * ((T + BN - 1) / BN);
   const int ksplit = C::kCanSplit ? choose_split(tiles, W.k / C::kTileK, kNumSMs * per_sm) : 1;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((T + BN - 1) / BN, W.n / kTileM, ksplit);
+  cfg.gridDim = CG == 2 ? dim3(2 * ((T + BN - 1) / BN), W.n / kTileM / 2, 1)
+                        : dim3((T + BN - 1) / BN, W.n / kTileM, ksplit);
   cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = ksplit;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (weights before the wait)
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  MSW_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<FMT, BN, EPI>, ta, tb, W.n, W.k, T, W.s, xscale,
+  MSW_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<FMT, BN, EPI, CG>, ta, tb, W.n, W.k, T, W.s, xscale,
                               y, ksplit, FMT == kW4 ? W.z : static_cast<const uint8_t*>(nullptr)));
 }
 
 template <int FMT, int EPI>
 void launch_fmt_epi(const LinearW& W, const void* x, const float* xs, int T, float* y,
                     cudaStream_t st) {
-  if (T <= 16) return launch_bn<FMT, 16, EPI>(W, x, xs, T, y, st);
-  if (T <= 32) return launch_bn<FMT, 32, EPI>(W, x, xs, T, y, st);
-  if (T <= 64) return launch_bn<FMT, 64, EPI>(W, x, xs, T, y, st);
-  if (T <= 128) return launch_bn<FMT, 128, EPI>(W, x, xs, T, y, st);
+  if (T <= 16) return launch_bn<FMT, 16, EPI, 1>(W, x, xs, T, y, st);
+  if (T <= 32) return launch_bn<FMT, 32, EPI, 1>(W, x, xs, T, y, st);
+  if (T <= 64) return launch_bn<FMT, 64, EPI, 1>(W, x, xs, T, y, st);
+  if (T <= 128) return launch_bn<FMT, 128, EPI, 1>(W, x, xs, T, y, st);
   // long prefills: 128 x 256 tiles (UMMA N = 256, 256 TMEM columns) halve the
-  // weight-operand traffic (and, for W4, the dequantisation) per FLOP
-  return launch_bn<FMT, 256, EPI>(W, x, xs, T, y, st);
+  // weight-operand traffic (and, for W4, the dequantisation) per FLOP; FP16 /
+  // INT8 run them as CTA pairs (cta_group::2) over adjacent weight-row tiles
+  if constexpr (FMT != kW4) {
+#ifndef MSW_GEMM_NO_PAIR  // A/B builds only
+    if ((W.n / kTileM) % 2 == 0) return launch_bn<FMT, 256, EPI, 2>(W, x, xs, T, y, st);
+#endif
+  }
+  return launch_bn<FMT, 256, EPI, 1>(W, x, xs, T, y, st);
 }
 
 template <int FMT>
