@@ -15,7 +15,7 @@ Placement (shard_trace), over the trace as routed by the reference RulePolicy:
 Predicted time is the reference's own cost model (fp16_latency, profile.cpp:
 281-291, divided by the (mode, family) cell's latency_speedup, sim.cpp:
 132-135) evaluated on a B200-MEASURED profile in the reference schema
-(profiles/r01_b200_profile.json: FP16 2.75 ms per decode token and 0.042 ms per
+(profiles/r02_b200_profile.json: FP16 2.75 ms per decode token and 0.021 ms per
 prefill token, against the reference's A100-derived 11.5 / 0.4). A cohort runs
 its members concurrently, so its time is its slowest member's.
 Each rank keeps its requests in trace order. Results are gathered back and
@@ -33,7 +33,7 @@ from . import controller as ctl
 CB_MODE = "int8_continuous_batching"
 PC_MODE = "gptq_prefix_caching"
 DEFAULT_PROFILE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                               "profiles", "r01_b200_profile.json")
+                               "profiles", "r02_b200_profile.json")
 
 
 class CostModel:

@@ -56,3 +56,16 @@ def test_reference_load_profile_accepts_written_profile(tmp_path):
     prof["cells"][0]["bogus_key"] = 1
     json.dump(prof, open(path, "w"))
     assert subprocess.run([REF, "--check-profile", path], capture_output=True).returncode == 3
+
+
+@pytest.mark.skipif(not os.path.exists(REF), reason="oracle/_ref not built (needs /root/reference)")
+def test_reference_load_profile_accepts_committed_b200_profile():
+    """The B200-measured profile committed under profiles/ (10 modes incl. the
+    four screening modes x 11 families) loads in the reference's own
+    load_profile, so route_oracle / compare_policies can run on it."""
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "r02_b200_profile.json")
+    prof = json.load(open(path))
+    assert len({c["mode"] for c in prof["cells"]}) == 10
+    out = subprocess.run([REF, "--check-profile", path], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.startswith("ok 11 families"), out.stdout + out.stderr
