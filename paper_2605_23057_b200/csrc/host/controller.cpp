@@ -1,8 +1,8 @@
 // Host controller: domain vocabulary, feature extraction, classifier and the
 // seven-rule router. Behaviour restated from the reference
 //   domain.cpp:5-133, classifier.cpp:13-136, routing.cpp:9-229
-// (bit-exact routing is checked against the reference's own library in
-// tests/test_routing_parity.py and by compiling the reference's
+// (bit-exact routing is checked against reference-generated goldens in
+// tests/test_host_controller.py and by compiling the reference's
 // tests/test_domain.cpp against this library).
 #include <chrono>
 #include <cmath>

@@ -7,7 +7,7 @@ import ctypes as C
 import os
 import sys
 
-os.environ["MSW_ENGINE_SO"] = "libmsw_engine_trace.so"
+os.environ.setdefault("MSW_ENGINE_SO", "libmsw_engine_trace.so")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
