@@ -86,6 +86,35 @@ __device__ __forceinline__ float cons_max(float v, float* red) {
   return warp_max(t);
 }
 
+// Register slots per thread of the register-resident prologues: float4 i =
+// tid + 512 j, j < kW4ProRegs (k <= 16384).
+constexpr int kW4ProRegs = 8;
+// RMSNorm weights of the decode prologues (model constants): thread tid's
+// float4 slots i = tid + 512 j, loaded into registers BEFORE griddepcontrol.wait
+// so the only global load left after it is x (a gamma load after the norm
+// reduction was a second dependent L2 round trip on every normed linear).
+template <int PRO>
+__device__ __forceinline__ void preload_gamma(const half* __restrict__ gamma, int k,
+                                              uint2 (&gpre)[kW4ProRegs]) {
+  if constexpr (PRO == kProNorm) {
+    if (k > kW4ProRegs * 4 * kConsThreads) return;
+#pragma unroll
+    for (int j = 0; j < kW4ProRegs; ++j) {
+      const int i = threadIdx.x + j * kConsThreads;
+      if (i < k / 4) gpre[j] = reinterpret_cast<const uint2*>(gamma)[i];
+    }
+  }
+}
+__device__ __forceinline__ float4 apply_norm(float4 a, float r, uint2 gv) {
+  const float2 g0 = __half22float2(*reinterpret_cast<const half2*>(&gv.x));
+  const float2 g1 = __half22float2(*reinterpret_cast<const half2*>(&gv.y));
+  a.x = (a.x * r) * g0.x;
+  a.y = (a.y * r) * g0.y;
+  a.z = (a.z * r) * g1.x;
+  a.w = (a.w * r) * g1.y;
+  return a;
+}
+
 // x fp32 [T, k] -> smem: fp16 [NT][k] (FP16 / W4) or int8 [NT][k] + scale.
 // W4 per-group activation offsets (corr region after the two fp16 copies):
 // GPTQ (zero point 8): C[t][g] = 1032 * Se + 72 * So, one float per group;
@@ -202,7 +231,8 @@ __device__ __forceinline__ void prologue(const float* __restrict__ x, const half
 template <int FMT, int PRO, int NT>
 __device__ __forceinline__ void prologue_multi(const float* __restrict__ x,
                                                const half* __restrict__ gamma, float eps, int k,
-                                               int T, uint8_t* xs, float* red2, float* xscale) {
+                                               int T, uint8_t* xs, float* red2, float* xscale,
+                                               const uint2 (&gpre)[kW4ProRegs]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k4 = k / 4;
   const float4* x4 = reinterpret_cast<const float4*>(x);
@@ -283,6 +313,21 @@ __device__ __forceinline__ void prologue_multi(const float* __restrict__ x,
         }
     }
     if (tid < NT) xscale[tid] = tid < T ? am[tid] / 127.0f : 0.0f;
+  } else if (PRO == kProNorm && k4 <= kW4ProRegs * kConsThreads) {
+    // FP16, normed: the RMSNorm weights come from registers (preload_gamma)
+#pragma unroll
+    for (int j = 0; j < kW4ProRegs; ++j) {
+      const int i = tid + j * kConsThreads;
+      if (i >= k4) break;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        if (t < T) {
+          const float4 v = apply_norm(x4[size_t(t) * k4 + i], r[t], gpre[j]);
+          half* xh = reinterpret_cast<half*>(xs + size_t(t) * 2 * k);
+          *reinterpret_cast<half2*>(xh + perm_f16(4 * i)) = __floats2half2_rn(v.x, v.y);
+          *reinterpret_cast<half2*>(xh + perm_f16(4 * i + 2)) = __floats2half2_rn(v.z, v.w);
+        }
+    }
   } else {
     for (int i = tid; i < k4; i += kConsThreads) {
 #pragma unroll
@@ -305,33 +350,6 @@ __device__ __forceinline__ void prologue_multi(const float* __restrict__ x,
 // lane bit 2 is the k16-step parity: four xor-shuffles (1, 2, 8, 16) leave
 // the even-step sum in lane 0 and the odd-step sum in lane 4.
 // Group sums are fp32 (pairwise tree over the fp16-rounded x).
-constexpr int kW4ProRegs = 8;
-// RMSNorm weights of the batch-1 prologues (model constants): thread tid's
-// float4 slots i = tid + 512 j, loaded into registers BEFORE griddepcontrol.wait
-// so the only global load left after it is x (a gamma load after the norm
-// reduction was a second dependent L2 round trip on every normed linear).
-template <int PRO>
-__device__ __forceinline__ void preload_gamma(const half* __restrict__ gamma, int k,
-                                              uint2 (&gpre)[kW4ProRegs]) {
-  if constexpr (PRO == kProNorm) {
-    if (k > kW4ProRegs * 4 * kConsThreads) return;
-#pragma unroll
-    for (int j = 0; j < kW4ProRegs; ++j) {
-      const int i = threadIdx.x + j * kConsThreads;
-      if (i < k / 4) gpre[j] = reinterpret_cast<const uint2*>(gamma)[i];
-    }
-  }
-}
-__device__ __forceinline__ float4 apply_norm(float4 a, float r, uint2 gv) {
-  const float2 g0 = __half22float2(*reinterpret_cast<const half2*>(&gv.x));
-  const float2 g1 = __half22float2(*reinterpret_cast<const half2*>(&gv.y));
-  a.x = (a.x * r) * g0.x;
-  a.y = (a.y * r) * g0.y;
-  a.z = (a.z * r) * g1.x;
-  a.w = (a.w * r) * g1.y;
-  return a;
-}
-
 // Batch-1 FP16 prologue (k <= 16384): x read once into registers, gamma from
 // preload_gamma; the same arithmetic as prologue<kFP16, PRO, 1>. (The INT8
 // equivalent measured 0.25% slower per 8B decode token than the generic
@@ -674,11 +692,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // consumers
   uint2 gpre[kW4ProRegs];
   constexpr bool kT1 = NT == 1 && FMT == kFP16;
-  if (kT1) preload_gamma<PRO>(gamma, k, gpre);
+  if (FMT == kFP16) preload_gamma<PRO>(gamma, k, gpre);
   pdl_wait();
   pdl_trigger();
   if constexpr (NT > 1 && FMT != kW4)
-    prologue_multi<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red2, xscale);
+    prologue_multi<FMT, PRO, NT>(x, gamma, eps, k, T, xs, red2, xscale, gpre);
   else if (kT1 && k <= kW4ProRegs * 4 * kConsThreads)
     prologue_t1_f16<PRO>(x, gpre, eps, k, xs, red);
   else

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout -s KILL 900 python -m pytest tests/test_kernels_gpu.py tests/test_engine_gpu.py tests/test_engine_8b_gpu.py -m gpu -x -q > gpurun_out/pytest_k.log 2>&1; echo "EXIT $?" >> gpurun_out/pytest_k.log
+bash scripts/ab_decode.sh 4 3 main prev > gpurun_out/ab_spec.txt 2>&1
+bash scripts/ab_decode.sh 0 2 main prev > gpurun_out/ab_f16.txt 2>&1
