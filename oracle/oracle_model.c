@@ -6,6 +6,10 @@
 
 #include <math.h>
 #include <omp.h>
+#if defined(__AVX2__) && defined(__F16C__)
+#include <immintrin.h>
+#define ORC_AVX2 1
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -212,8 +216,37 @@ static float dot8(const float* a, const float* b, int64_t k) {
   return s;
 }
 
+#ifdef ORC_AVX2
+/* dot8's arithmetic in one ymm: lane j accumulates products c = j mod 8 in
+ * increasing c (mul, then add: -ffp-contract=off, no FMA), then the lanes are
+ * summed in order from 0.0f, exactly as the scalar dot8 (bit-identical; the
+ * CPU baseline timing was dominated by the scalar LUT / conversion loops). */
+static inline float hsum8_in_order(__m256 acc) {
+  float a8[8];
+  _mm256_storeu_ps(a8, acc);
+  float s = 0.0f;
+  for (int j = 0; j < 8; ++j) s += a8[j];
+  return s;
+}
+#endif
+
 static void linear_fp16(const h16* w, int32_t n, int32_t k, const float* x16,
                         float* y) {
+#ifdef ORC_AVX2
+  if (k % 8 == 0) {
+#pragma omp parallel for schedule(static)
+    for (int32_t r = 0; r < n; ++r) {
+      const h16* wr = w + (int64_t)r * k;
+      __m256 acc = _mm256_setzero_ps();
+      for (int32_t c = 0; c < k; c += 8) {
+        const __m256 wv = _mm256_cvtph_ps(_mm_loadu_si128((const __m128i*)(wr + c)));
+        acc = _mm256_add_ps(acc, _mm256_mul_ps(wv, _mm256_loadu_ps(x16 + c)));
+      }
+      y[r] = hsum8_in_order(acc);
+    }
+    return;
+  }
+#endif
 #pragma omp parallel
   {
     float* row = (float*)malloc(sizeof(float) * (size_t)k);
@@ -229,6 +262,34 @@ static void linear_fp16(const h16* w, int32_t n, int32_t k, const float* x16,
 static void linear_w4(const uint8_t* q, const h16* s, const uint8_t* zeros, int32_t n,
                       int32_t k, const float* x16, float* y) {
   const int32_t groups = k / MSW_W4_GROUP;
+#ifdef ORC_AVX2
+  /* 16-entry LUT as two 8-float tables: permute by the low 3 bits, select by bit 3 */
+#pragma omp parallel for schedule(static)
+  for (int32_t r = 0; r < n; ++r) {
+    __m256 acc = _mm256_setzero_ps();
+    for (int32_t g = 0; g < groups; ++g) {
+      /* lut[v] = rnd16((float)(v - z) * sc): exact (v - z), one rounded
+       * product, RNE to fp16 and back (vcvtps2ph / vcvtph2ps) */
+      const __m256 sc = _mm256_set1_ps(h2f(s[(int64_t)r * groups + g]));
+      const __m256 zf = _mm256_set1_ps((float)(zeros ? zeros[(int64_t)r * groups + g] : 8));
+      const __m256 plo = _mm256_mul_ps(_mm256_sub_ps(_mm256_setr_ps(0, 1, 2, 3, 4, 5, 6, 7), zf), sc);
+      const __m256 phi = _mm256_mul_ps(_mm256_sub_ps(_mm256_setr_ps(8, 9, 10, 11, 12, 13, 14, 15), zf), sc);
+      const __m256 tlo = _mm256_cvtph_ps(_mm256_cvtps_ph(plo, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC));
+      const __m256 thi = _mm256_cvtph_ps(_mm256_cvtps_ph(phi, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC));
+      const uint8_t* src = q + (int64_t)r * k + (int64_t)g * MSW_W4_GROUP;
+      const float* xg = x16 + (int64_t)g * MSW_W4_GROUP;
+      for (int i = 0; i < MSW_W4_GROUP; i += 8) {
+        const __m256i idx = _mm256_cvtepu8_epi32(_mm_loadl_epi64((const __m128i*)(src + i)));
+        const __m256 hi = _mm256_castsi256_ps(_mm256_cmpgt_epi32(idx, _mm256_set1_epi32(7)));
+        const __m256 wv = _mm256_blendv_ps(_mm256_permutevar8x32_ps(tlo, idx),
+                                           _mm256_permutevar8x32_ps(thi, idx), hi);
+        acc = _mm256_add_ps(acc, _mm256_mul_ps(wv, _mm256_loadu_ps(xg + i)));
+      }
+    }
+    y[r] = hsum8_in_order(acc);
+  }
+  return;
+#endif
 #pragma omp parallel
   {
     float* row = (float*)malloc(sizeof(float) * (size_t)k);
