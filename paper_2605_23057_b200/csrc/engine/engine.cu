@@ -1124,18 +1124,17 @@ void run_spec(msw_engine* e, const msw_request& r, msw_result& res) {
 // one CUDA graph per live-batch size T — and synchronises only at the event.
 // The host knows when the next event is: min over live sequences of the
 // tokens they still have to generate.
-void cb_step(msw_engine* e, Model& m, int T, bool use_graph) {
+void cb_step_body(msw_engine* e, Model& m, int T) {
   Scratch& s = e->sc;
-  auto body = [&]() {
-    forward(e, m, kINT8, T, T, true, true);
-    launch_cb_advance(s.next, T, s.tok, s.pos, s.slot, s.seq_of, s.cb_hbase, s.cb_hist,
-                      m.block_table, m.max_blocks, e->st);
-    ++e->launches;
-  };
-  if (!use_graph) {
-    body();
-    return;
-  }
+  forward(e, m, kINT8, T, T, true, true);
+  launch_cb_advance(s.next, T, s.tok, s.pos, s.slot, s.seq_of, s.cb_hbase, s.cb_hist,
+                    m.block_table, m.max_blocks, e->st);
+  ++e->launches;
+}
+
+// The step graph of a live-batch size T (captured once per engine).
+std::map<int, std::pair<cudaGraphExec_t, int>>::iterator cb_graph(msw_engine* e, Model& m, int T) {
+  auto body = [&]() { cb_step_body(e, m, T); };
   auto it = e->cb_graphs.find(T);
   if (it == e->cb_graphs.end()) {
     const long long before = e->launches;
@@ -1155,6 +1154,15 @@ void cb_step(msw_engine* e, Model& m, int T, bool use_graph) {
     it = e->cb_graphs.emplace(T, std::make_pair(x, int(e->launches - before))).first;
     e->launches = before;
   }
+  return it;
+}
+
+void cb_step(msw_engine* e, Model& m, int T, bool use_graph) {
+  if (!use_graph) {
+    cb_step_body(e, m, T);
+    return;
+  }
+  auto it = cb_graph(e, m, T);
   MSW_CUDA(cudaGraphLaunch(it->second.first, e->st));
   e->launches += it->second.second;
 }
@@ -1180,6 +1188,12 @@ void run_cb(msw_engine* e, const msw_request* reqs, int n, msw_result* res) {
     SeqBlocks sb;
     double t_admit;
   };
+  // the step graphs of every live-batch size are captured once per engine,
+  // before its first cohort (as serving engines capture their batch-size
+  // buckets at start-up): a ragged cohort shrinks through many sizes, and a
+  // capture + instantiate inside the step loop costs milliseconds of host time
+  if (graphs)
+    for (int T = 1; T <= maxb; ++T) cb_graph(e, m, T);
   std::vector<Live> live;
   std::vector<int> free_rows;
   for (int r = maxb - 1; r >= 0; --r) free_rows.push_back(r);
